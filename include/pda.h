@@ -1,0 +1,191 @@
+/*
+ * pda.h -- C ABI of the B200 paged decode attention library (libpda.so).
+ *
+ * The hot path of arXiv 2504.06319 ("L2-cache-oriented asynchronous KV cache
+ * prefetching"): decode-phase attention of one query token per sequence over
+ * a paged KV cache gathered block by block through a block table, with the
+ * K/V blocks a tunable distance ahead prefetched into L2 while the current
+ * block is being computed.  Citations: P:n = PAPER.md line n.
+ *
+ *   out[b, h, :] = sum_t softmax_t(scale * q[b,h,:] . k_t) * v_t,
+ *   t in [0, context_lens[b]),  k_t/v_t gathered through block_tables[b]
+ *   ("logits . V"; QK^T with resident Q; Alg. 1).
+ *
+ * General conventions (apply to every entry point):
+ *  - Tensor pointers passed to the compute entry points are DEVICE pointers
+ *    owned by the caller; the library never allocates, frees or synchronises
+ *    them.  Work is enqueued on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Calls are stateless and thread-safe.
+ *  - Host-side argument errors are returned synchronously before any launch;
+ *    launch failures map to PDA_ERR_CUDA.  No C++ exception crosses the ABI.
+ *  - Device-resident values (block ids, lengths) are not validated: a block
+ *    id outside [0, num_blocks) is undefined behaviour; context_lens[b] is
+ *    clamped to max_blocks_per_seq * block_size.
+ *  - Layouts (all row-major, contiguous):
+ *      q, out        [num_seqs, num_q_heads, head_dim]
+ *      k_cache/v_cache [num_blocks, num_kv_heads, block_size, head_dim]
+ *        -- each (block, kv head) slab is contiguous, "each block exclusively
+ *           stores KV Cache data for a single attention head"; its
+ *           size is Eq. 1's M_block = b * d_h * T_block bytes.
+ *      block_tables  [num_seqs, max_blocks_per_seq] int32 physical block ids
+ *                    (one table per sequence, shared by all heads; Alg. 1 bt)
+ *      context_lens  [num_seqs] int32, 0 <= L_b
+ *  - GQA: q head h reads kv head floor(h / (Hq / Hkv)); Hq % Hkv == 0.
+ *  - Supported: head_dim in {64, 128}, block_size == 16,
+ *    Hq / Hkv <= 16, dtype fp16 or bf16, out dtype = dtype or fp32.
+ *    Base pointers must be 16-byte aligned (TMA / bulk-prefetch requirement).
+ *  - context_lens[b] == 0 yields a zero output row.  Tokens >= L_b inside the
+ *    last block and blocks not referenced by the table are never read into
+ *    the result: they may hold anything, NaN included.
+ */
+#ifndef PDA_H_
+#define PDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PDA_OK = 0,
+    PDA_ERR_NULL = 1,        /* a required pointer is NULL */
+    PDA_ERR_SHAPE = 2,       /* inconsistent or out-of-range sizes */
+    PDA_ERR_UNSUPPORTED = 3, /* valid but not implemented (head_dim, block_size, group) */
+    PDA_ERR_ALIGN = 4,       /* a base pointer is not 16-byte aligned */
+    PDA_ERR_WORKSPACE = 5,   /* workspace NULL or smaller than pda_workspace_bytes() */
+    PDA_ERR_CUDA = 6         /* a CUDA runtime/driver call or launch failed */
+} pda_status;
+
+typedef enum { PDA_F16 = 0, PDA_BF16 = 1, PDA_F32 = 2 /* out_dtype only */ } pda_dtype;
+
+/* L2 prefetch of upcoming KV blocks (Section 3.2). */
+typedef enum {
+    PDA_PF_OFF = 0,     /* no prefetch: the ablation baseline */
+    PDA_PF_BULK_L2 = 1, /* cp.async.bulk.prefetch.L2 of each K and V slab (one instruction per slab) */
+    PDA_PF_LINE_L2 = 2  /* prefetch.global.L2 of every 128-byte line of each slab */
+} pda_prefetch;
+
+typedef enum {
+    PDA_KERNEL_AUTO = 0,   /* = PDA_KERNEL_SPLITK */
+    PDA_KERNEL_PAPER = 1,  /* the paper's structure: grid [Hq, B], 4 warps, warp-per-block,
+                              K/V loaded to registers (Section 3.1) */
+    PDA_KERNEL_SPLITK = 2  /* B200 kernel: split-K over context partitions, TMA ring in
+                              shared memory, mma.sync, GQA group per CTA, combine kernel */
+} pda_kernel;
+
+typedef struct {
+    int32_t num_seqs;           /* B */
+    int32_t num_q_heads;        /* Hq */
+    int32_t num_kv_heads;       /* Hkv */
+    int32_t head_dim;           /* D */
+    int32_t block_size;         /* tokens per KV block (16) */
+    int32_t num_blocks;         /* physical blocks in k_cache / v_cache */
+    int32_t max_blocks_per_seq; /* columns of block_tables */
+    int32_t dtype;              /* pda_dtype of q, k_cache, v_cache */
+    int32_t out_dtype;          /* pda_dtype of out */
+} pda_shape;
+
+typedef struct {
+    int32_t prefetch;          /* pda_prefetch */
+    int32_t prefetch_distance; /* blocks ahead of the block being issued; >= 1 when prefetch on.
+                                  Paper kernel: d = 4 (= warps) reproduces Alg. 1 exactly */
+    int32_t partition_tokens;  /* split-K partition size P in tokens; 0 = planner's choice;
+                                  otherwise a positive multiple of block_size */
+    int32_t smem_stages;       /* split-K shared-memory ring depth in blocks; 0 = default (8);
+                                  supported: 4, 8, 12 */
+    int32_t kernel;            /* pda_kernel */
+    int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
+} pda_options;
+
+/* Result of the (host-only, deterministic) split-K planner. */
+typedef struct {
+    int32_t kernel;           /* the kernel that will run (PDA_KERNEL_PAPER or _SPLITK) */
+    int32_t partition_tokens; /* P (split-K) or max_blocks_per_seq * block_size (paper) */
+    int32_t p_max;            /* partitions per sequence = ceil(max_blocks*bs / P) */
+    int32_t smem_stages;      /* ring depth */
+    int32_t grid_x, grid_y, grid_z; /* main kernel grid */
+    int32_t threads;          /* main kernel block size */
+    int32_t trace_rec_len;    /* int32 words per trace record (see paged_decode_attention_trace) */
+    int32_t trace_records;    /* number of trace records */
+    size_t workspace_bytes;   /* == pda_workspace_bytes() */
+} pda_plan_info;
+
+/* Host-only validation of shape and options (no CUDA context needed). */
+pda_status pda_check_args(const pda_shape* shape, const pda_options* opt);
+
+/* Plan the launch (host-only, deterministic; no CUDA context needed). */
+pda_status pda_plan(const pda_shape* shape, const pda_options* opt, pda_plan_info* plan);
+
+/* Bytes of device workspace paged_decode_attention needs: the split-K
+ * partials (o_p fp32 [B, Hq, P_max, D] and lse_p fp32 [B, Hq, P_max]);
+ * 0 when P_max == 1 or for the paper kernel.  Returns 0 on invalid args. */
+size_t pda_workspace_bytes(const pda_shape* shape, const pda_options* opt);
+
+/* The decode attention step (the method's hot path).
+ *   q            [B, Hq, D] dtype                      (device, read)
+ *   k_cache      [num_blocks, Hkv, bs, D] dtype        (device, read)
+ *   v_cache      [num_blocks, Hkv, bs, D] dtype        (device, read)
+ *   block_tables [B, max_blocks_per_seq] int32         (device, read)
+ *   context_lens [B] int32                             (device, read)
+ *   scale        softmax scale, applied in fp32 to q.k (never folded into q)
+ *   out          [B, Hq, D] out_dtype                  (device, written)
+ *   workspace    device scratch of >= pda_workspace_bytes() (may be NULL if 0)
+ * Results are bit-identical for every prefetch mode and distance and
+ * run-to-run (no atomics; fixed-order combine). */
+pda_status paged_decode_attention(const void* q, const void* k_cache, const void* v_cache,
+                                  const int32_t* block_tables, const int32_t* context_lens,
+                                  float scale, void* out, const pda_shape* shape,
+                                  const pda_options* opt, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
+/* Same computation, additionally writing the kernel's own bookkeeping trace
+ * to the device buffer `trace` (int32, plan.trace_records * plan.trace_rec_len
+ * words, R = (trace_rec_len - 4) / 2):
+ *   split-K: one record per unit u = (b * Hkv + kvh) * P_max + p;
+ *            rec[0..1] = token range [s, e) (s = e = min(p*P, L) when empty)
+ *   paper:   one record per (b, h, warp) u = (b * Hq + h) * 4 + warp;
+ *            rec[0] = first block index (= warp), rec[1] = e = ceil(L / bs)
+ *   rec[2] = visited block count, rec[3] = prefetch count,
+ *   rec[4 .. 4+R)   visited physical block ids in issue order, rest -1,
+ *   rec[4+R .. 4+2R) prefetch targets (physical ids) in issue order, rest -1.
+ * The caller fills nothing; the library initialises the buffer to -1 first. */
+pda_status paged_decode_attention_trace(const void* q, const void* k_cache, const void* v_cache,
+                                        const int32_t* block_tables,
+                                        const int32_t* context_lens, float scale, void* out,
+                                        const pda_shape* shape, const pda_options* opt,
+                                        void* workspace, size_t workspace_bytes, int32_t* trace,
+                                        size_t trace_words, void* stream);
+
+/* End-to-end decode step from HOST buffers: copies this step's inputs
+ * (q, block_tables, context_lens; pinned host memory recommended) to the
+ * device staging buffers, runs paged_decode_attention against the
+ * device-resident caches, and copies out back to host -- all enqueued on
+ * `stream`; the caller synchronises the stream before reading out_host.
+ *   *_host   host pointers (read: q, block_tables, context_lens; written: out)
+ *   *_dev    device staging buffers of the same sizes (caller-owned)
+ *   k_cache, v_cache, workspace: device pointers as above. */
+pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_host,
+                                const int32_t* context_lens_host, void* out_host, void* q_dev,
+                                int32_t* block_tables_dev, int32_t* context_lens_dev,
+                                void* out_dev, const void* k_cache, const void* v_cache,
+                                float scale, const pda_shape* shape, const pda_options* opt,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* Measurement helper (not part of the method): stream-read `bytes` of device
+ * memory at `buf` with 16-byte loads on a grid of num_sms * 4 CTAs, writing a
+ * checksum word to `sink` (device, 16 B).  Gives the in-run read roofline. */
+pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream);
+
+/* Human-readable name of a status code (static string). */
+const char* pda_status_string(pda_status status);
+
+/* ABI version (bumped on any signature change). */
+int32_t pda_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDA_H_ */

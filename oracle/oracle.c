@@ -1,0 +1,272 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct fp64 CPU implementation of what the
+ * paper's hot path computes: single-query (decode) attention over a paged
+ * KV cache, plus the block/prefetch bookkeeping of Algorithm 1.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_2504_06319_b200/) never includes, links or calls anything here, and
+ * this file includes nothing from the product (no shared headers, tables or
+ * helpers).  The trace record layout below is restated independently from
+ * the documentation in include/pda.h, not included from it.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (read at build time only).
+ *
+ * Parity pins (tests/test_oracle.py, `-m "not gpu"`):
+ *   oracle_paged_attention   pinned: brute force vs numpy/torch fp64 SDPA on
+ *                            contiguous gathers, permutation invariance,
+ *                            L=1 -> V row, q=0 -> mean(V), const V -> v,
+ *                            needle, sum of weights = 1.
+ *   oracle_attention_weights pinned: sums to 1, matches numpy softmax.
+ *   oracle_fp16/bf16_to_f64  pinned: numpy float16 / torch bfloat16 decode.
+ *   oracle_plan_splitk       pinned: hand-computed ranges, Alg. 1 guard
+ *                            counts, brute-force plan.
+ *   oracle_plan_paper        pinned: Alg. 1 guard counts, hand examples.
+ *   oracle_eq1/eq2/l2_bound  pinned: 4096 B, 524288 B, 120.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_F16 0
+#define ORACLE_BF16 1
+
+/* IEEE 754 binary16 -> double, written from the format definition
+ * (1 sign bit, 5 exponent bits with bias 15, 10 fraction bits). */
+double oracle_fp16_to_f64(uint16_t h) {
+    int sign = (h >> 15) & 1;
+    int exp = (h >> 10) & 0x1f;
+    int frac = h & 0x3ff;
+    double v;
+    if (exp == 0) {
+        v = ldexp((double)frac, -24); /* subnormal: frac * 2^-14 * 2^-10 */
+    } else if (exp == 31) {
+        v = frac ? NAN : INFINITY;
+    } else {
+        v = ldexp((double)(frac + 1024), exp - 25); /* (1 + f/1024) * 2^(e-15) */
+    }
+    return sign ? -v : v;
+}
+
+/* bfloat16 -> double: bfloat16 is the upper 16 bits of an IEEE binary32
+ * (1 sign bit, 8 exponent bits with bias 127, 7 fraction bits). */
+double oracle_bf16_to_f64(uint16_t h) {
+    int sign = (h >> 15) & 1;
+    int exp = (h >> 7) & 0xff;
+    int frac = h & 0x7f;
+    double v;
+    if (exp == 0) {
+        v = ldexp((double)frac, -133); /* frac * 2^-126 * 2^-7 */
+    } else if (exp == 255) {
+        v = frac ? NAN : INFINITY;
+    } else {
+        v = ldexp((double)(frac + 128), exp - 134); /* (1 + f/128) * 2^(e-127) */
+    }
+    return sign ? -v : v;
+}
+
+static double decode(uint16_t x, int dtype) {
+    return dtype == ORACLE_BF16 ? oracle_bf16_to_f64(x) : oracle_fp16_to_f64(x);
+}
+
+/* Offset of element d of token slot o of (physical block phys, kv head kvh)
+ * in a [num_blocks, Hkv, bs, D] cache.  Layout reading R2 of DESIGN.md: each
+ * (block, head) slab is contiguous, "each block exclusively stores KV Cache
+ * data for a single attention head" (Section 3.1). */
+static size_t kv_offset(int64_t phys, int kvh, int o, int d, int Hkv, int bs, int D) {
+    return (((size_t)phys * Hkv + kvh) * bs + o) * D + d;
+}
+
+/* Score s_t of token t for row (b, h), as the plain definition
+ * s_t = scale * sum_d q[b,h,d] * k_t[d]   (QK^T, Alg. 1 line 9 P:136). */
+static double score(const uint16_t* q, const uint16_t* k, int dtype, const int32_t* bt,
+                    int b, int h, int kvh, int t, int Hq, int Hkv, int D, int bs,
+                    int max_blocks, double scale) {
+    int j = t / bs, o = t % bs;
+    int64_t phys = bt[(size_t)b * max_blocks + j]; /* bt lookup, Alg. 1 */
+    double acc = 0.0;
+    for (int d = 0; d < D; ++d) {
+        double qd = decode(q[((size_t)b * Hq + h) * D + d], dtype);
+        double kd = decode(k[kv_offset(phys, kvh, o, d, Hkv, bs, D)], dtype);
+        acc += qd * kd;
+    }
+    return scale * acc;
+}
+
+/* Softmax weights w_t / Z of one row (b, h) over its L = lens[b] tokens.
+ * Writes L doubles to w.  Returns L (0 => nothing written). */
+int oracle_attention_weights(const uint16_t* q, const uint16_t* k, int dtype,
+                             const int32_t* bt, const int32_t* lens, int b, int h,
+                             int Hq, int Hkv, int D, int bs, int max_blocks, double scale,
+                             double* w) {
+    int g = Hq / Hkv;
+    int kvh = h / g; /* GQA: q head h reads kv head floor(h / g) */
+    int L = lens[b];
+    if (L <= 0) return 0;
+    double m = -INFINITY;
+    for (int t = 0; t < L; ++t) {
+        w[t] = score(q, k, dtype, bt, b, h, kvh, t, Hq, Hkv, D, bs, max_blocks, scale);
+        if (w[t] > m) m = w[t];
+    }
+    double Z = 0.0;
+    for (int t = 0; t < L; ++t) {
+        w[t] = exp(w[t] - m);
+        Z += w[t];
+    }
+    for (int t = 0; t < L; ++t) w[t] /= Z;
+    return L;
+}
+
+/* One output row: out[b,h,:] = sum_t softmax(s)_t * v_t  ("logits . V").
+ * L = 0 gives a zero row (reading R6). */
+static void attend_row(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                       const int32_t* bt, const int32_t* lens, int b, int h, int Hq, int Hkv,
+                       int D, int bs, int max_blocks, double scale, double* w, double* out_row) {
+    int g = Hq / Hkv;
+    int kvh = h / g;
+    for (int d = 0; d < D; ++d) out_row[d] = 0.0;
+    int L = oracle_attention_weights(q, k, dtype, bt, lens, b, h, Hq, Hkv, D, bs, max_blocks,
+                                     scale, w);
+    for (int t = 0; t < L; ++t) {
+        int64_t phys = bt[(size_t)b * max_blocks + t / bs];
+        int o = t % bs;
+        for (int d = 0; d < D; ++d)
+            out_row[d] += w[t] * decode(v[kv_offset(phys, kvh, o, d, Hkv, bs, D)], dtype);
+    }
+}
+
+/* Paged decode attention, fp64.  q: [B, Hq, D]; k, v: [num_blocks, Hkv, bs, D]
+ * (raw 16-bit patterns of dtype); bt: [B, max_blocks]; lens: [B]; out: [B, Hq, D].
+ * rows: optional list of n_rows row ids r = b * Hq + h to compute (NULL = all);
+ * rows not listed are left untouched.  nthreads <= 0: OpenMP default.
+ * Returns 0, or -1 on invalid arguments. */
+int oracle_paged_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                           const int32_t* bt, const int32_t* lens, int B, int Hq, int Hkv,
+                           int D, int bs, int max_blocks, double scale, double* out,
+                           const int64_t* rows, int64_t n_rows, int nthreads) {
+    if (B < 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || D <= 0 || bs <= 0 || max_blocks < 0) return -1;
+    int64_t total = rows ? n_rows : (int64_t)B * Hq;
+    int Lmax = max_blocks * bs;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+    {
+        double* w = (double*)malloc(sizeof(double) * (Lmax > 0 ? Lmax : 1));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t i = 0; i < total; ++i) {
+            int64_t r = rows ? rows[i] : i;
+            int b = (int)(r / Hq), h = (int)(r % Hq);
+            attend_row(q, k, v, dtype, bt, lens, b, h, Hq, Hkv, D, bs, max_blocks, scale, w,
+                       out + (size_t)r * D);
+        }
+        free(w);
+    }
+    return 0;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* ---------------------------------------------------------------------------
+ * Bookkeeping plans (bit-exact targets for the GPU debug trace).
+ *
+ * Record layout, restated from the library documentation (include/pda.h):
+ *   rec[0] = s, rec[1] = e     (split-K: token range [s, e) of the unit;
+ *                               paper kernel: first block index, block end e)
+ *   rec[2] = number of visited blocks, rec[3] = number of prefetches,
+ *   rec[4 .. 4+R)   visited physical block ids in visit order, rest -1,
+ *   rec[4+R .. 4+2R) prefetch target physical ids in issue order, rest -1.
+ * ------------------------------------------------------------------------- */
+
+/* Split-K plan.  Units u = ((b * Hkv) + kvh) * P_max + p, partition size
+ * P tokens (multiple of bs), R = P / bs.  The unit's blocks are
+ * [s/bs, ceil(e/bs)); each is visited in order j = s/bs, s/bs+1, ...; when
+ * block j is issued, block j + d is prefetched iff j + d < e_blk
+ * (Alg. 1 guard "block_idx + w < e", with the stride w replaced by the
+ * distance knob d because one producer issues the blocks in order; reading R8/R9).
+ * d <= 0 means prefetch off. */
+int oracle_plan_splitk(const int32_t* bt, const int32_t* lens, int B, int Hkv, int bs,
+                       int max_blocks, int P, int P_max, int d, int32_t* recs) {
+    if (P <= 0 || P % bs) return -1;
+    int R = P / bs;
+    int rec_len = 4 + 2 * R;
+    for (int b = 0; b < B; ++b) {
+        int L = lens[b];
+        for (int kvh = 0; kvh < Hkv; ++kvh) {
+            for (int p = 0; p < P_max; ++p) {
+                int32_t* rec = recs + ((size_t)(b * Hkv + kvh) * P_max + p) * rec_len;
+                for (int i = 0; i < rec_len; ++i) rec[i] = -1;
+                int s = p * P < L ? p * P : L;
+                int e = (p + 1) * P < L ? (p + 1) * P : L;
+                rec[0] = s;
+                rec[1] = e;
+                int sb = s / bs, eb = e > s ? (e + bs - 1) / bs : sb; /* empty unit: no blocks */
+                int nv = 0, np = 0;
+                for (int j = sb; j < eb; ++j) {
+                    rec[4 + nv++] = bt[(size_t)b * max_blocks + j];
+                    if (d > 0 && j + d < eb) rec[4 + R + np++] = bt[(size_t)b * max_blocks + j + d];
+                }
+                rec[2] = nv;
+                rec[3] = np;
+            }
+        }
+    }
+    return 0;
+}
+
+/* Paper-kernel plan (Section 3.1, Alg. 1): one CTA per (q head h, seq b)
+ * (grid [H, B, 1]), w warps; warp i starts at block_idx = i and strides
+ * by w; while on block_idx it prefetches bt[block_idx + d]
+ * iff block_idx + d < e (Alg. 1 lines 4-7 with w -> d; d = w is the paper).
+ * Records per (b, h, warp) = ((b * Hq) + h) * w + warp, R = ceil(max_blocks / w). */
+int oracle_plan_paper(const int32_t* bt, const int32_t* lens, int B, int Hq, int bs,
+                      int max_blocks, int w, int d, int32_t* recs) {
+    if (w <= 0) return -1;
+    int R = (max_blocks + w - 1) / w;
+    int rec_len = 4 + 2 * R;
+    for (int b = 0; b < B; ++b) {
+        int e = (lens[b] + bs - 1) / bs; /* blocks of the sequence */
+        for (int h = 0; h < Hq; ++h) {
+            for (int wi = 0; wi < w; ++wi) {
+                int32_t* rec = recs + ((size_t)(b * Hq + h) * w + wi) * rec_len;
+                for (int i = 0; i < rec_len; ++i) rec[i] = -1;
+                rec[0] = wi;
+                rec[1] = e;
+                int nv = 0, np = 0;
+                for (int idx = wi; idx < e; idx += w) {
+                    rec[4 + nv++] = bt[(size_t)b * max_blocks + idx];
+                    if (d > 0 && idx + d < e) rec[4 + R + np++] = bt[(size_t)b * max_blocks + idx + d];
+                }
+                rec[2] = nv;
+                rec[3] = np;
+            }
+        }
+    }
+    return 0;
+}
+
+/* Eq. 1: M_block = b * d_h * T_block bytes. */
+int64_t oracle_eq1_block_bytes(int64_t b, int64_t d_h, int64_t T_block) { return b * d_h * T_block; }
+
+/* Eq. 2: M_total = M_block * (N_thread / 32) * H * B. */
+int64_t oracle_eq2_total_bytes(int64_t M_block, int64_t N_thread, int64_t H, int64_t B) {
+    return M_block * (N_thread / 32) * H * B;
+}
+
+/* L2 residency bound: the largest batch whose per-iteration blocks
+ * fit in L2, floor(L2 / M_total(B=1)). */
+int64_t oracle_l2_residency_bound(int64_t l2_bytes, int64_t M_total_b1) { return l2_bytes / M_total_b1; }

@@ -1,0 +1,298 @@
+"""Pins of the fp64 oracle against things other than itself (-m "not gpu").
+
+Each test names what fixes the expected value: the paper's printed numbers
+(tests/golden/paper_constants.txt), closed forms, invariants, library
+routines on contiguous gathers (numpy / torch fp64), or brute force.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "paper_constants.txt")
+
+
+def golden():
+    vals = {}
+    for line in open(GOLDEN):
+        line = line.split("#", 1)[0].strip()
+        if line:
+            k, v = line.split("=")
+            vals[k.strip()] = int(v)
+    return vals
+
+
+def contiguous_reference(inp, b, h):
+    """Gather row (b, h)'s K/V into contiguous fp64 arrays with plain indexing
+    and compute softmax attention with numpy (library primitives only)."""
+    cfg = inp["cfg"]
+    g = cfg.num_q_heads // cfg.num_kv_heads
+    kvh = h // g
+    L = int(inp["context_lens"][b])
+    bs = cfg.block_size
+    k = inp["k_cache"].double().numpy()
+    v = inp["v_cache"].double().numpy()
+    q = inp["q"].double().numpy()[b, h]
+    bt = inp["block_tables"].numpy()
+    if L == 0:
+        return np.zeros(cfg.head_dim)
+    K = np.stack([k[bt[b, t // bs], kvh, t % bs] for t in range(L)])
+    V = np.stack([v[bt[b, t // bs], kvh, t % bs] for t in range(L)])
+    s = inp["scale"] * (K @ q)
+    w = np.exp(s - s.max())
+    w /= w.sum()
+    return w @ V
+
+
+def run_oracle(oracle_mod, inp, **kw):
+    return oracle_mod.paged_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                      inp["context_lens"], inp["scale"], inp["cfg"].dtype, **kw)
+
+
+CFGS = [
+    synth.C1_TINY,
+    synth.Config("mha_d128", 3, 4, 4, 128, (1, 17, 100), "fp16", poison_blocks=2),
+    synth.Config("gqa_bf16", 2, 8, 2, 64, (33, 48), "bf16", poison_blocks=1),
+    synth.Config("gqa8", 2, 16, 2, 128, (5, 70), "bf16"),
+    synth.Config("with_zero", 3, 2, 1, 64, (0, 16, 31), "fp16"),
+]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.name)
+def test_oracle_vs_contiguous_numpy(oracle_mod, cfg):
+    inp = synth.make_inputs(cfg, seed=3)
+    out = run_oracle(oracle_mod, inp)
+    assert np.isfinite(out).all(), "NaN poison leaked into the oracle output"
+    for b in range(cfg.num_seqs):
+        for h in range(cfg.num_q_heads):
+            ref = contiguous_reference(inp, b, h)
+            np.testing.assert_allclose(out[b, h], ref, rtol=0, atol=1e-12)
+
+
+def test_oracle_vs_torch_sdpa(oracle_mod):
+    """Library routine: torch SDPA in fp64 on the contiguous gather (GQA expanded)."""
+    cfg = synth.Config("sdpa", 2, 8, 2, 64, (40, 64), "fp16")
+    inp = synth.make_inputs(cfg, seed=5, poison=False)
+    out = run_oracle(oracle_mod, inp)
+    g = cfg.group
+    for b in range(cfg.num_seqs):
+        L = int(inp["context_lens"][b])
+        ids = inp["block_tables"][b, : math.ceil(L / 16)].long()
+        K = inp["k_cache"][ids].double().permute(1, 0, 2, 3).reshape(cfg.num_kv_heads, -1, 64)[:, :L]
+        V = inp["v_cache"][ids].double().permute(1, 0, 2, 3).reshape(cfg.num_kv_heads, -1, 64)[:, :L]
+        K = K.repeat_interleave(g, 0)
+        V = V.repeat_interleave(g, 0)
+        q = inp["q"][b].double().unsqueeze(1)  # [Hq, 1, D]
+        ref = torch.nn.functional.scaled_dot_product_attention(q, K, V, scale=inp["scale"])
+        np.testing.assert_allclose(out[b], ref[:, 0].numpy(), rtol=0, atol=1e-12)
+
+
+def test_fp16_decode_all_patterns(oracle_mod):
+    bits = np.arange(65536, dtype=np.uint16)
+    ref = bits.view(np.float16).astype(np.float64)
+    got = np.array([oracle_mod.fp16_to_f64(int(x)) for x in bits])
+    nan = np.isnan(ref)
+    assert (np.isnan(got) == nan).all()
+    assert (got[~nan] == ref[~nan]).all()
+
+
+def test_bf16_decode_all_patterns(oracle_mod):
+    bits = np.arange(65536, dtype=np.int32).astype(np.int16)
+    ref = torch.from_numpy(bits).view(torch.bfloat16).double().numpy()
+    got = np.array([oracle_mod.bf16_to_f64(int(x) & 0xFFFF) for x in bits])
+    nan = np.isnan(ref)
+    assert (np.isnan(got) == nan).all()
+    assert (got[~nan] == ref[~nan]).all()
+
+
+def test_permutation_invariance_bitwise(oracle_mod):
+    inp = synth.make_inputs(synth.C1_TINY, seed=0)
+    a = run_oracle(oracle_mod, inp)
+    for s in range(3):
+        b = run_oracle(oracle_mod, synth.permute_placement(inp, seed=11 + s))
+        assert np.array_equal(a, b)
+
+
+def test_context_len_one_returns_v_row(oracle_mod):
+    cfg = synth.Config("l1", 2, 4, 2, 64, (1, 1), "bf16", poison_blocks=3)
+    inp = synth.make_inputs(cfg, seed=1)
+    out = run_oracle(oracle_mod, inp)
+    for b in range(2):
+        for h in range(4):
+            vrow = inp["v_cache"][int(inp["block_tables"][b, 0]), h // 2, 0].double().numpy()
+            assert np.array_equal(out[b, h], vrow)
+
+
+def test_zero_query_gives_mean_of_v(oracle_mod):
+    cfg = synth.Config("q0", 1, 2, 1, 64, (45,), "fp16")
+    inp = synth.make_inputs(cfg, seed=2)
+    inp["q"].zero_()
+    out = run_oracle(oracle_mod, inp)
+    ids = inp["block_tables"][0, :3].long()
+    V = inp["v_cache"][ids, 0].double().reshape(-1, 64)[:45]
+    np.testing.assert_allclose(out[0, 0], V.mean(0).numpy(), rtol=0, atol=1e-14)
+    np.testing.assert_allclose(out[0, 1], V.mean(0).numpy(), rtol=0, atol=1e-14)
+
+
+def test_constant_v_gives_v(oracle_mod):
+    cfg = synth.Config("cv", 2, 4, 4, 128, (29, 64), "bf16")
+    inp = synth.make_inputs(cfg, seed=4, poison=False)
+    inp["v_cache"].fill_(0.375)
+    out = run_oracle(oracle_mod, inp)
+    np.testing.assert_allclose(out, 0.375, rtol=0, atol=1e-14)
+
+
+def test_two_token_closed_form(oracle_mod):
+    """s0 = 0, s1 = ln 3 => weights (1/4, 3/4); v0 = 1, v1 = -1 => out = -1/2."""
+    cfg = synth.Config("two", 1, 1, 1, 64, (2,), "fp16")
+    inp = synth.make_inputs(cfg, seed=0, poison=False)
+    inp["q"].zero_()
+    inp["q"][0, 0, 0] = 1.0
+    blk = int(inp["block_tables"][0, 0])
+    inp["k_cache"][blk].zero_()
+    inp["k_cache"][blk, 0, 1, 0] = 1.0
+    inp["v_cache"][blk, 0, 0] = 1.0
+    inp["v_cache"][blk, 0, 1] = -1.0
+    inp["scale"] = math.log(3.0)
+    out = run_oracle(oracle_mod, inp)
+    np.testing.assert_allclose(out[0, 0], -0.5, rtol=0, atol=1e-15)
+    w = oracle_mod.attention_weights(inp["q"], inp["k_cache"], inp["block_tables"], inp["context_lens"],
+                                     0, 0, inp["scale"], "fp16")
+    np.testing.assert_allclose(w, [0.25, 0.75], rtol=0, atol=1e-15)
+
+
+def test_weights_sum_to_one(oracle_mod):
+    inp = synth.make_inputs(synth.C1_TINY, seed=7)
+    for b in range(2):
+        for h in range(4):
+            w = oracle_mod.attention_weights(inp["q"], inp["k_cache"], inp["block_tables"],
+                                             inp["context_lens"], b, h, inp["scale"], "fp16")
+            assert len(w) == int(inp["context_lens"][b])
+            assert abs(w.sum() - 1.0) < 1e-12 and (w > 0).all()
+
+
+@pytest.mark.parametrize("t_star", [0, 5, 15, 16, 31, 36])
+def test_needle(oracle_mod, t_star):
+    """A key aligned with q at position t* dominates: out ~= v_{t*}."""
+    cfg = synth.Config("needle", 1, 1, 1, 64, (37,), "fp16")
+    inp = synth.make_inputs(cfg, seed=9)
+    inp["q"].zero_()
+    inp["q"][0, 0, 0] = 1.0
+    bt = inp["block_tables"][0]
+    for t in range(37):
+        inp["k_cache"][int(bt[t // 16]), 0, t % 16, 0] = 40.0 if t == t_star else 0.0
+    inp["scale"] = 1.0
+    out = run_oracle(oracle_mod, inp)
+    v = inp["v_cache"][int(bt[t_star // 16]), 0, t_star % 16].double().numpy()
+    np.testing.assert_allclose(out[0, 0], v, rtol=0, atol=1e-14)
+
+
+def test_zero_length_row_is_zero(oracle_mod):
+    cfg = synth.Config("z", 2, 2, 1, 64, (0, 3), "fp16")
+    out = run_oracle(oracle_mod, synth.make_inputs(cfg, seed=0))
+    assert (out[0] == 0).all() and np.isfinite(out).all()
+
+
+def test_gqa_group_sharing(oracle_mod):
+    """Identical q across a GQA group => identical outputs; and GQA equals the
+    MHA problem with each KV head repeated g times."""
+    cfg = synth.Config("gqa", 2, 8, 2, 64, (21, 50), "fp16")
+    inp = synth.make_inputs(cfg, seed=6)
+    inp["q"][:, 1:4] = inp["q"][:, 0:1]
+    out = run_oracle(oracle_mod, inp)
+    for h in (1, 2, 3):
+        assert np.array_equal(out[:, h], out[:, 0])
+    mha = dict(inp)
+    mha["k_cache"] = inp["k_cache"].repeat_interleave(4, dim=1)
+    mha["v_cache"] = inp["v_cache"].repeat_interleave(4, dim=1)
+    mha["cfg"] = cfg.with_heads(8, 8)
+    assert np.array_equal(run_oracle(oracle_mod, mha), out)
+
+
+def test_rows_subset(oracle_mod):
+    inp = synth.make_inputs(synth.C1_TINY, seed=1)
+    full = run_oracle(oracle_mod, inp)
+    part = run_oracle(oracle_mod, inp, rows=[0, 5, 7])
+    for r in (0, 5, 7):
+        assert np.array_equal(part.reshape(-1, 64)[r], full.reshape(-1, 64)[r])
+    assert np.isnan(part.reshape(-1, 64)[1]).all()
+
+
+def test_sample_rows_compaction(oracle_mod):
+    cfg = synth.Config("s", 4, 4, 2, 64, (20, 64, 3, 40), "bf16")
+    inp = synth.make_inputs(cfg, seed=8)
+    full = run_oracle(oracle_mod, inp)
+    sub = synth.sample_rows(inp, [1, 3])
+    out = run_oracle(oracle_mod, sub)
+    assert np.array_equal(out[0], full[1]) and np.array_equal(out[1], full[3])
+
+
+# ---- paper constants (tests/golden/paper_constants.txt) ---------------------
+
+def test_eq1_eq2_and_residency_bound(oracle_mod):
+    g = golden()
+    mb = oracle_mod.eq1_block_bytes(g["table2_b"], g["table2_d_h"], g["table2_T_block"])
+    assert mb == g["eq1_block_bytes_llama2_7b"]
+    mt = oracle_mod.eq2_total_bytes(mb, g["table2_N_thread"], g["table2_H"], 1)
+    assert mt == g["eq2_total_bytes_llama2_7b_b1"]
+    assert oracle_mod.l2_residency_bound(60 * 2**20, mt) == g["l2_residency_bound_60MB"]
+
+
+# ---- bookkeeping plans --------------------------------------------------------
+
+def test_plan_splitk_hand_example(oracle_mod):
+    """L = 37 tokens, P = 32: partitions [0,32) -> blocks 0,1 and [32,37) -> block 2;
+    distance 1 prefetches block j+1 while issuing block j inside the unit only."""
+    bt = np.array([[7, 3, 9, 1]], dtype=np.int32)
+    lens = np.array([37], dtype=np.int32)
+    recs = oracle_mod.plan_splitk(bt, lens, num_kv_heads=1, block_size=16, partition_tokens=32,
+                                  p_max=2, prefetch_distance=1)
+    r0, r1 = recs[0, 0, 0], recs[0, 0, 1]
+    R = 2
+    assert list(r0[:4]) == [0, 32, 2, 1]
+    assert list(r0[4:4 + R]) == [7, 3] and list(r0[4 + R:]) == [3, -1]
+    assert list(r1[:4]) == [32, 37, 1, 0]
+    assert list(r1[4:4 + R]) == [9, -1] and list(r1[4 + R:]) == [-1, -1]
+
+
+def test_plan_splitk_empty_unit(oracle_mod):
+    bt = np.array([[4, 5, 6, 7]], dtype=np.int32)
+    lens = np.array([20], dtype=np.int32)
+    recs = oracle_mod.plan_splitk(bt, lens, 1, 16, 16, 4, 2)
+    assert list(recs[0, 0, 2, :4]) == [20, 20, 0, 0]
+    assert list(recs[0, 0, 3, :4]) == [20, 20, 0, 0]
+    assert list(recs[0, 0, 1, :4]) == [16, 20, 1, 0]
+
+
+def test_plan_paper_guard_counts(oracle_mod):
+    """one block per warp => zero prefetches; two blocks per warp
+    => exactly one prefetch per warp, for its second block (Alg. 1 guard)."""
+    w = 4
+    bt = np.arange(16, dtype=np.int32)[None, :] + 100
+    one = oracle_mod.plan_paper(bt, np.array([16 * w], np.int32), 1, 16, w, w)
+    assert (one[0, 0, :, 2] == 1).all() and (one[0, 0, :, 3] == 0).all()
+    two = oracle_mod.plan_paper(bt, np.array([2 * 16 * w], np.int32), 1, 16, w, w)
+    R = two.shape[-1] // 2 - 2
+    for wi in range(w):
+        rec = two[0, 0, wi]
+        assert rec[2] == 2 and rec[3] == 1
+        assert rec[4 + R] == 100 + wi + w  # prefetch target = the warp's second block
+        assert list(rec[4:6]) == [100 + wi, 100 + wi + w]
+    # total prefetches across warps = max(0, e - w) for d = w
+    for e in range(0, 17):
+        p = oracle_mod.plan_paper(bt, np.array([16 * e], np.int32), 1, 16, w, w)
+        assert p[0, 0, :, 3].sum() == max(0, e - w)
+    # a single-block sequence: warp 0 loads it, no prefetch
+    p = oracle_mod.plan_paper(bt, np.array([16], np.int32), 1, 16, w, w)
+    assert p[0, 0, 0, 2] == 1 and p[0, 0, :, 3].sum() == 0 and (p[0, 0, 1:, 2] == 0).all()
+
+
+def test_plan_splitk_prefetch_off(oracle_mod):
+    bt = np.arange(8, dtype=np.int32)[None, :]
+    recs = oracle_mod.plan_splitk(bt, np.array([128], np.int32), 1, 16, 128, 1, 0)
+    assert recs[0, 0, 0, 2] == 8 and recs[0, 0, 0, 3] == 0
+    assert list(recs[0, 0, 0, 4:12]) == list(range(8))
