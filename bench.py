@@ -1,0 +1,400 @@
+"""Benchmark: B200 paged decode attention with L2 KV prefetch (arXiv 2504.06319).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One "step" is one decode-attention pass over the whole batch (every row of
+the hot-path table: plan, block-table walk, L2 prefetch, KV load, QK^T,
+online softmax, PV, combine; plus the TP output all-gather when N > 1).
+Inputs are seeded synthetic tensors shaped like BASELINE.json's configs
+(default configs[1], Llama-2-7B: B=64, 32 heads, D=128, ctx 4096, fp16),
+resident in HBM before the timed region; KV per step (4.3 GB) is far larger
+than L2 (126 MB), so no flush is needed between steps.
+
+N > 1 (torchrun): tensor parallel over KV heads -- rank r holds
+Hkv/N heads of the same batch and the step ends with an NCCL all-gather of
+the output heads; the total work is fixed (strong scaling).
+
+Prints ONE JSON line (rank 0).  `value` = algorithmic KV+q+out bytes moved
+per step, all ranks, / max-over-ranks device time (GB/s).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode attention us/step & achieved HBM GB/s (prefetch on/off); tokens/s at 1-8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prefetch", default=None, help="bulk|line|off (default: library default)")
+    ap.add_argument("--distance", type=int, default=None)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--partition", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip ablation arms / e2e / cpu baseline")
+    ap.add_argument("--sweep", action="store_true", help="prefetch-distance x stages sweep (extra JSON lines on stderr)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * (mx or max(sm))] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload_config(name: str):
+    import synth
+    if name in synth.PRESETS:
+        return synth.PRESETS[name]
+    if name.startswith("c4_"):  # c4_b{B}_ctx{C}
+        _, b, c = name.split("_")
+        return synth.sweep_cell(int(b[1:]), int(c[3:]))
+    raise SystemExit(f"unknown config {name}")
+
+
+def algorithmic_bytes(cfg, out_elem=2):
+    """KV + q + out + block-table + lens bytes one step must move."""
+    return cfg.kv_bytes() + cfg.other_bytes(out_elem)
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(cfg, seconds: float, seed: int = 0):
+    """Time the fp64 oracle (as it stands) on whole sequences of the workload
+    until ~`seconds` of wall time; returns (GB/s, sample description, threads)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import synth
+    oracle.build()
+    threads = len(os.sched_getaffinity(0))
+    one = synth.Config(cfg.name + "_sample", 1, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+                       (cfg.context_lens[0],), cfg.dtype)
+    inp = synth.make_inputs(one, seed=seed)
+    nbytes = algorithmic_bytes(one)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.paged_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                               inp["context_lens"], inp["scale"], one.dtype, nthreads=threads)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    gbs = done * nbytes / el / 1e9
+    desc = (f"{done} x one sequence of {cfg.name} (all {cfg.num_q_heads} q heads, ctx "
+            f"{cfg.context_lens[0]}), fp64 oracle, {el:.2f} s wall")
+    return gbs, desc, threads, el / done
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle is this tier's reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    cfg = workload_config(args.config)
+    # per step: one sequence of the workload (bounded sample); value scaled as GB/s
+    gbs_w, desc, threads, _ = oracle_sample(cfg, 0.5)
+    times = []
+    import oracle
+    import synth
+    one = synth.Config(cfg.name + "_sample", 1, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim,
+                       (cfg.context_lens[0],), cfg.dtype)
+    inp = synth.make_inputs(one, seed=1)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.paged_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                               inp["context_lens"], inp["scale"], one.dtype, nthreads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    per = sum(times) / len(times)
+    value = algorithmic_bytes(one) / per / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "sample": "one sequence per step (all heads)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": f"one sequence of {cfg.name} per step, {args.steps} steps"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_06319_b200 as pda
+    import synth
+    from paper_2504_06319_b200.tp import TPDecodeAttention
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pda.lib()
+
+    cfg = workload_config(args.config)
+    if cfg.num_kv_heads % world:
+        raise SystemExit(f"{cfg.num_kv_heads} KV heads do not shard over {world} GPUs")
+    local_cfg = cfg.with_heads(cfg.num_q_heads // world, cfg.num_kv_heads // world,
+                               name=f"{cfg.name}_tp{world}_rank{rank}")
+    inp = synth.make_inputs(local_cfg, seed=1234 + rank, device="cuda", poison=True)
+    dt = synth.torch_dtype(cfg.dtype)
+    opt_kw = {}
+    if args.prefetch is not None:
+        opt_kw["prefetch"] = args.prefetch
+    if args.distance is not None:
+        opt_kw["prefetch_distance"] = args.distance
+    if args.stages:
+        opt_kw["smem_stages"] = args.stages
+    if args.partition:
+        opt_kw["partition_tokens"] = args.partition
+
+    def make_step(**kw):
+        return TPDecodeAttention(inp["k_cache"], inp["v_cache"], local_cfg.num_seqs,
+                                 local_cfg.num_q_heads, local_cfg.max_blocks_per_seq, dt, **kw)
+
+    step_main = make_step(**opt_kw)
+    q, bt, lens, scale = inp["q"], inp["block_tables"], inp["context_lens"], inp["scale"]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def time_steps(fn, steps, warmup):
+        for _ in range(warmup):
+            fn(q, bt, lens, scale)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn(q, bt, lens, scale)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    total_bytes = algorithmic_bytes(cfg)  # whole job (all ranks' shards)
+    local_bytes = algorithmic_bytes(local_cfg)
+    peak, peak_src = load_peaks()
+
+    with ClockSampler(local) as clk:
+        ms = time_steps(step_main, args.steps, args.warmup)
+        extras = {}
+        if not args.no_extras:
+            # prefetch ablation arms on the same inputs (ABAB-interleaved)
+            off = make_step(**{**opt_kw, "prefetch": "off"})
+            on_ms, off_ms = [], []
+            for _ in range(3):
+                on_ms.append(time_steps(step_main, max(10, args.steps // 3), 2))
+                off_ms.append(time_steps(off, max(10, args.steps // 3), 2))
+            paper_on = make_step(kernel="paper", prefetch="bulk", prefetch_distance=4)
+            paper_off = make_step(kernel="paper", prefetch="off")
+            p_on, p_off = [], []
+            for _ in range(2):
+                p_on.append(time_steps(paper_on, max(5, args.steps // 10), 2))
+                p_off.append(time_steps(paper_off, max(5, args.steps // 10), 2))
+            extras = {
+                "splitk_prefetch_on_us": statistics.median(on_ms) * 1e3,
+                "splitk_prefetch_off_us": statistics.median(off_ms) * 1e3,
+                "prefetch_speedup": statistics.median(off_ms) / statistics.median(on_ms),
+                "paper_kernel": {
+                    "prefetch_on_us": statistics.median(p_on) * 1e3,
+                    "prefetch_off_us": statistics.median(p_off) * 1e3,
+                    "prefetch_speedup": statistics.median(p_off) / statistics.median(p_on),
+                    "desc": "paper structure: grid [Hq,B], 4 warps, warp-per-block LDG, Alg. 1 d=4",
+                },
+            }
+            # in-run read roofline (read-only stream over a 4 GiB buffer)
+            buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
+            sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+            for _ in range(2):
+                pda.read_roofline(buf, sink)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                pda.read_roofline(buf, sink)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            extras["read_roofline_gbs"] = buf.numel() * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            del buf
+
+    # the dominant kernel's own launch time (attention call alone, no gather)
+    def attn_only(q_, bt_, lens_, scale_):
+        pda.paged_decode_attention(q_, inp["k_cache"], inp["v_cache"], bt_, lens_, scale_,
+                                   out=step_main.out_local, workspace=step_main.ws, **opt_kw)
+    attn_ms = time_steps(attn_only, args.steps, 2)
+    achieved = local_bytes / (attn_ms * 1e-3) / 1e9
+
+    # end to end through the public C-ABI host entry (pinned host q/bt/lens in, out back)
+    e2e = None
+    if not args.no_extras:
+        host = pda.HostDecodeStep(inp["k_cache"], inp["v_cache"], local_cfg.num_seqs,
+                                  local_cfg.num_q_heads, local_cfg.max_blocks_per_seq, dt, **opt_kw)
+        qh, bth, lh = q.cpu().pin_memory(), bt.cpu().pin_memory(), lens.cpu().pin_memory()
+
+        def e2e_step(*_):
+            host(qh, bth, lh, scale)
+            if world > 1:
+                pass  # the gathered output of the TP step is measured on the device path
+        e2e_ms = time_steps(e2e_step, max(10, args.steps // 2), 2)
+        e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": host.h2d_bytes() * world,
+               "d2h_bytes_per_step": host.d2h_bytes() * world,
+               "path": "pda_decode_step_host (H2D q/bt/lens from pinned memory, kernels, D2H out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        gbs, desc, threads, _ = oracle_sample(cfg, 2.0)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc}
+
+    value = total_bytes / (ms * 1e-3) / 1e9
+    pl = step_main.plan
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "us_per_step": ms * 1e3,
+        "tokens_per_s": cfg.num_seqs / (ms * 1e-3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": cfg.dtype,
+        "data": "synthetic",
+        "config": {
+            "workload": cfg.name, "batch": cfg.num_seqs, "q_heads": cfg.num_q_heads,
+            "kv_heads": cfg.num_kv_heads, "head_dim": cfg.head_dim,
+            "ctx": max(cfg.context_lens), "block_size": cfg.block_size, "tp": world,
+            "kernel": "splitk", "prefetch": opt_kw.get("prefetch", pda._lib.DEFAULT_PREFETCH),
+            "prefetch_distance": opt_kw.get("prefetch_distance", pda._lib.DEFAULT_DISTANCE),
+            "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
+            "p_max": pl["p_max"],
+            "l2": f"no flush: inputs larger than L2 ({cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)",
+            "bytes_per_step": total_bytes,
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": load_traffic(cfg.name),
+            "kernel": "splitk_kernel" + (" + combine_kernel" if pl["p_max"] > 1 else ""),
+            "launch_us": attn_ms * 1e3, "algorithmic_bytes_per_launch": local_bytes,
+            "peak_source": peak_src,
+        },
+        "gpu_launches": args.steps * step_main.launches_per_step(),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    line.update(extras)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

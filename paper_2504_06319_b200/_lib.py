@@ -1,0 +1,257 @@
+"""ctypes binding of libpda.so (include/pda.h): argument marshalling only.
+
+Every step of the decode path runs in the CUDA kernels behind the C ABI;
+this module turns torch tensors into device pointers + the current stream
+and turns status codes into exceptions.  There is no fallback: if the
+library is missing or a tensor is not on a CUDA device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpda.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
+
+PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
+PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
+KERNEL = {"auto": 0, "paper": 1, "splitk": 2}
+
+DEFAULT_PREFETCH = "bulk"
+DEFAULT_DISTANCE = 4
+
+
+class PdaError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)} (status {status})")
+        self.status = status
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "num_seqs", "num_q_heads", "num_kv_heads", "head_dim", "block_size", "num_blocks",
+        "max_blocks_per_seq", "dtype", "out_dtype")]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms")]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "kernel", "partition_tokens", "p_max", "smem_stages", "grid_x", "grid_y", "grid_z",
+        "threads", "trace_rec_len", "trace_records")] + [("workspace_bytes", ctypes.c_size_t)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libpda.so (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build the CUDA extension first "
+                    "(python -c 'import __graft_entry__ as g; g.build()')")
+            L = ctypes.CDLL(LIB_PATH)
+            p, sz, i32, f32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_float
+            ps, po, ppl = ctypes.POINTER(Shape), ctypes.POINTER(Options), ctypes.POINTER(PlanInfo)
+            L.pda_check_args.argtypes = [ps, po]
+            L.pda_check_args.restype = i32
+            L.pda_plan.argtypes = [ps, po, ppl]
+            L.pda_plan.restype = i32
+            L.pda_workspace_bytes.argtypes = [ps, po]
+            L.pda_workspace_bytes.restype = sz
+            L.paged_decode_attention.argtypes = [p, p, p, p, p, f32, p, ps, po, p, sz, p]
+            L.paged_decode_attention.restype = i32
+            L.paged_decode_attention_trace.argtypes = [p, p, p, p, p, f32, p, ps, po, p, sz, p, sz, p]
+            L.paged_decode_attention_trace.restype = i32
+            L.pda_decode_step_host.argtypes = [p, p, p, p, p, p, p, p, p, p, f32, ps, po, p, sz, p]
+            L.pda_decode_step_host.restype = i32
+            L.pda_read_roofline.argtypes = [p, sz, p, p]
+            L.pda_read_roofline.restype = i32
+            L.pda_status_string.argtypes = [i32]
+            L.pda_status_string.restype = ctypes.c_char_p
+            L.pda_abi_version.restype = ctypes.c_int32
+            _lib = L
+    return _lib
+
+
+def header_symbols():
+    """Function names declared in include/pda.h."""
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\*?\s+\*?(\w+)\(", text, re.M)))
+
+
+def status_string(status: int) -> str:
+    return lib().pda_status_string(int(status)).decode()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise PdaError(status, what)
+
+
+def _dtype_code(dt) -> int:
+    import torch
+    if dt == torch.float16:
+        return PDA_F16
+    if dt == torch.bfloat16:
+        return PDA_BF16
+    if dt == torch.float32:
+        return PDA_F32
+    raise TypeError(f"unsupported dtype {dt}")
+
+
+def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
+    B, Hq, D = q.shape
+    nb, Hkv, bs, D2 = k_cache.shape
+    if D2 != D:
+        raise ValueError("q and k_cache head_dim differ")
+    return Shape(B, Hq, Hkv, D, bs, nb, block_tables.shape[1], _dtype_code(q.dtype),
+                 _dtype_code(out_dtype if out_dtype is not None else q.dtype))
+
+
+def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
+                 smem_stages=0, kernel="auto", num_sms=0) -> Options:
+    mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
+    if prefetch_distance is None:
+        prefetch_distance = DEFAULT_DISTANCE if mode else 0
+    kern = KERNEL[kernel] if not isinstance(kernel, int) else kernel
+    return Options(mode, int(prefetch_distance), int(partition_tokens), int(smem_stages), kern,
+                   int(num_sms))
+
+
+def plan(shape: Shape, opts: Options) -> dict:
+    info = PlanInfo()
+    _check(lib().pda_plan(ctypes.byref(shape), ctypes.byref(opts), ctypes.byref(info)), "pda_plan")
+    return info.as_dict()
+
+
+def check_args(shape: Shape, opts: Options) -> int:
+    return lib().pda_check_args(ctypes.byref(shape), ctypes.byref(opts))
+
+
+def workspace_bytes(shape: Shape, opts: Options) -> int:
+    return lib().pda_workspace_bytes(ctypes.byref(shape), ctypes.byref(opts))
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("paged_decode_attention runs on CUDA tensors only (no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scale=None, out=None, *,
+                           out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
+                           partition_tokens=0, smem_stages=0, kernel="auto", workspace=None,
+                           stream=None, trace=False):
+    """Decode attention over a paged KV cache (see include/pda.h).
+
+    q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16),
+    block_tables [B, max_blocks] int32, context_lens [B] int32, all CUDA.
+    Returns out [B, Hq, D] (and the int32 bookkeeping trace if trace=True).
+    """
+    import torch
+    _require_cuda(q, k_cache, v_cache, block_tables, context_lens)
+    if block_tables.dtype != torch.int32 or context_lens.dtype != torch.int32:
+        raise TypeError("block_tables / context_lens must be int32")
+    if out is not None:
+        out_dtype = out.dtype
+    shape = make_shape(q, k_cache, block_tables, out_dtype)
+    opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel)
+    if scale is None:
+        scale = q.shape[-1] ** -0.5
+    info = plan(shape, opts)
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype or q.dtype, device=q.device)
+    _require_cuda(out)
+    wsb = info["workspace_bytes"]
+    if wsb and (workspace is None or workspace.numel() * workspace.element_size() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=q.device)
+    ws_ptr = workspace.data_ptr() if (workspace is not None and wsb) else None
+    s = _stream_handle(stream)
+    L = lib()
+    if trace:
+        words = info["trace_records"] * info["trace_rec_len"]
+        tr = torch.empty(max(1, words), dtype=torch.int32, device=q.device)
+        st = L.paged_decode_attention_trace(
+            q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(),
+            context_lens.data_ptr(), float(scale), out.data_ptr(), ctypes.byref(shape),
+            ctypes.byref(opts), ws_ptr, wsb, tr.data_ptr(), words, s)
+        _check(st, "paged_decode_attention_trace")
+        return out, tr, info
+    st = L.paged_decode_attention(
+        q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(),
+        context_lens.data_ptr(), float(scale), out.data_ptr(), ctypes.byref(shape), ctypes.byref(opts),
+        ws_ptr, wsb, s)
+    _check(st, "paged_decode_attention")
+    return out
+
+
+class HostDecodeStep:
+    """End-to-end step from pinned host buffers through pda_decode_step_host:
+    H2D of q / block_tables / context_lens, the decode kernel(s) against the
+    device-resident caches, D2H of out -- all on one stream."""
+
+    def __init__(self, k_cache, v_cache, num_seqs, num_q_heads, max_blocks, dtype, out_dtype=None,
+                 **opt_kw):
+        import torch
+        _require_cuda(k_cache, v_cache)
+        dev = k_cache.device
+        D = k_cache.shape[-1]
+        self.k, self.v = k_cache, v_cache
+        self.out_dtype = out_dtype or dtype
+        self.q_dev = torch.empty((num_seqs, num_q_heads, D), dtype=dtype, device=dev)
+        self.bt_dev = torch.empty((num_seqs, max_blocks), dtype=torch.int32, device=dev)
+        self.lens_dev = torch.empty((num_seqs,), dtype=torch.int32, device=dev)
+        self.out_dev = torch.empty((num_seqs, num_q_heads, D), dtype=self.out_dtype, device=dev)
+        self.out_host = torch.empty(self.out_dev.shape, dtype=self.out_dtype, pin_memory=True)
+        self.shape = make_shape(self.q_dev, k_cache, self.bt_dev, self.out_dtype)
+        self.opts = make_options(**opt_kw)
+        wsb = workspace_bytes(self.shape, self.opts)
+        self.ws = torch.empty(max(1, wsb), dtype=torch.uint8, device=dev)
+        self.wsb = wsb
+
+    def h2d_bytes(self):
+        return sum(t.numel() * t.element_size() for t in (self.q_dev, self.bt_dev, self.lens_dev))
+
+    def d2h_bytes(self):
+        return self.out_dev.numel() * self.out_dev.element_size()
+
+    def __call__(self, q_host, bt_host, lens_host, scale, stream=None):
+        st = lib().pda_decode_step_host(
+            q_host.data_ptr(), bt_host.data_ptr(), lens_host.data_ptr(), self.out_host.data_ptr(),
+            self.q_dev.data_ptr(), self.bt_dev.data_ptr(), self.lens_dev.data_ptr(),
+            self.out_dev.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), float(scale),
+            ctypes.byref(self.shape), ctypes.byref(self.opts), self.ws.data_ptr() if self.wsb else None,
+            self.wsb, _stream_handle(stream))
+        _check(st, "pda_decode_step_host")
+        return self.out_host
+
+
+def read_roofline(buf, sink, stream=None):
+    """Launch the read-only streaming probe over `buf` (CUDA tensor)."""
+    _require_cuda(buf, sink)
+    st = lib().pda_read_roofline(buf.data_ptr(), buf.numel() * buf.element_size(), sink.data_ptr(),
+                                 _stream_handle(stream))
+    _check(st, "pda_read_roofline")

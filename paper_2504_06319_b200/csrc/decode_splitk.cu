@@ -1,0 +1,517 @@
+// decode_splitk.cu -- the B200 decode paged-attention kernel (split-K over
+// context partitions) and its combine kernel.
+//
+// One CTA per unit (partition p, kv head, sequence b); grid (P_max, Hkv, B).
+//  * Producer warp (warp 4): walks the unit's block-table slice (S1, Alg. 1
+//    line 3 "Lookup bt[block_idx]"), issues TMA tensor loads of the K
+//    and V slabs of each 16-token block into an S-stage shared-memory ring
+//    (S3, "Load K Block"), and -- the paper's method -- while issuing
+//    block j prefetches the K and V slabs of block j + d into L2 with
+//    cp.async.bulk.prefetch.L2 iff j + d < e (S2, Alg. 1 lines 5-7,
+//    P:132-135; V blocks likewise).
+//  * 4 consumer warps take ring stages round-robin and compute, per block,
+//    S^T = K Q^T for the GQA group's g heads (S4; tokens as the MMA M dim,
+//    heads as N: one m16n8k16 tile covers g <= 8), the online softmax (S5),
+//    and O^T += V^T P (S6), all on mma.sync tensor cores with fp32
+//    accumulation.  Q stays in registers for the whole unit.
+//  * Epilogue (S7): the 4 warps' (m, l, acc) are merged through shared
+//    memory; a sequence with a single partition writes `out` directly,
+//    otherwise the normalised partial and its log2-sum-exp go to the
+//    workspace and combine_kernel (S8) merges partitions in fixed order.
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace pda {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+template <int D>
+struct Geometry {
+    static constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1: M_block = b * d_h * T_block
+    static constexpr int kStage = 2 * kSlab;          // K slab + V slab
+    static constexpr int kChunks = D / 64;            // 128-byte column chunks (TMA boxes)
+};
+
+// Byte offset of the 16-byte unit holding column `col` of token row `t`
+// inside a slab written by TMA with SWIZZLE_128B: the slab is D/64 column
+// chunks of [16 rows][128 B]; unit u of row t sits at unit u ^ (t % 8).
+__device__ __forceinline__ uint32_t swz(int t, int col) {
+    const int ch = col >> 6;
+    const int u = (col & 63) >> 3;
+    return ch * 2048 + t * 128 + ((u ^ (t & 7)) << 4);
+}
+
+__device__ __forceinline__ void store_out(void* out, size_t idx, float x, int out_dtype) {
+    if (out_dtype == 2) {
+        static_cast<float*>(out)[idx] = x;
+    } else if (out_dtype == 1) {
+        static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(x);
+    } else {
+        static_cast<__half*>(out)[idx] = __float2half_rn(x);
+    }
+}
+
+template <bool BF16, int D, int NT, int STAGES, bool TRACE>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
+    splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const SplitKParams p) {
+    using G = Geometry<D>;
+    constexpr int NH = 8 * NT;  // padded heads per CTA
+    constexpr int KSTEPS = D / 16;
+    constexpr int MT = D / 16;  // m-tiles of O^T
+
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-B alignment for the 128-B swizzle atoms.
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* ring = smem;
+    constexpr int kRingBytes = STAGES * G::kStage;
+    constexpr int kMergeAccBytes = kConsumerWarps * NH * (D + 4) * 4;
+    constexpr int kBigBytes = kRingBytes > kMergeAccBytes ? kRingBytes : kMergeAccBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBigBytes);
+    uint64_t* empty = full + STAGES;
+    float* merge_m = reinterpret_cast<float*>(empty + STAGES);
+    float* merge_l = merge_m + kConsumerWarps * NH;
+    float* merge_acc = reinterpret_cast<float*>(ring);
+
+    const int part = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int g = p.g;
+
+    const int max_tokens = p.max_blocks * kBlockSize;
+    int L = p.lens[b];
+    L = L < max_tokens ? L : max_tokens;
+    const int P = p.part_tokens;
+    const int s_tok = part * P < L ? part * P : L;
+    const int e_tok = (part + 1) * P < L ? (part + 1) * P : L;
+
+    int32_t* rec = nullptr;
+    if constexpr (TRACE) {
+        rec = p.trace + ((size_t)(b * p.Hkv + kvh) * p.p_max + part) * p.trace_rec_len;
+    }
+
+    if (e_tok <= s_tok) {  // empty unit (S0): nothing to read
+        if constexpr (TRACE) {
+            if (threadIdx.x == 0) {
+                rec[0] = s_tok;
+                rec[1] = s_tok;
+                rec[2] = 0;
+                rec[3] = 0;
+            }
+        }
+        if (part == 0 && L <= 0) {  // context_len == 0 => zero row (reading R6)
+            for (int i = threadIdx.x; i < g * D; i += blockDim.x)
+                store_out(p.out, ((size_t)b * p.Hq + kvh * g) * D + i, 0.f, p.out_dtype);
+        }
+        return;
+    }
+    const int sb = s_tok / kBlockSize;
+    const int n = (e_tok + kBlockSize - 1) / kBlockSize - sb;  // blocks in this unit
+    const int n_parts = (L + P - 1) / P;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);    // producer's arrive.expect_tx (+ TMA bytes)
+            mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ============================ producer warp ============================
+        if (lane == 0) {
+            prefetch_tmap(&tmK);
+            prefetch_tmap(&tmV);
+        }
+        const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
+        const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
+        // block ids for 32 blocks at a time, the next chunk loaded one chunk ahead
+        int cur = lane < n ? btrow[lane] : 0;
+        int pfv = (d > 0 && lane + d < n) ? btrow[lane + d] : -1;
+        int npf = 0;
+        const size_t slab_elems = (size_t)kBlockSize * D;
+        for (int c = 0; c < n; c += 32) {
+            const int nxt = c + 32 + lane < n ? btrow[c + 32 + lane] : 0;
+            const int pfn = (d > 0 && c + 32 + lane + d < n) ? btrow[c + 32 + lane + d] : -1;
+            const int m = n - c < 32 ? n - c : 32;
+            for (int i = 0; i < m; ++i) {
+                const int j = c + i;
+                const int phys = __shfl_sync(kFull, cur, i);
+                const int pf = __shfl_sync(kFull, pfv, i);
+                const int stage = j % STAGES;
+                const uint32_t round = j / STAGES;
+                if (lane == 0) {
+                    if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
+                    mbar_arrive_expect_tx(&full[stage], G::kStage);
+                    const int row = (phys * p.Hkv + kvh) * kBlockSize;
+                    uint8_t* dst = ring + stage * G::kStage;
+#pragma unroll
+                    for (int ch = 0; ch < G::kChunks; ++ch)
+                        tma_load_2d(dst + ch * 2048, &tmK, ch * 64, row, &full[stage]);
+#pragma unroll
+                    for (int ch = 0; ch < G::kChunks; ++ch)
+                        tma_load_2d(dst + G::kSlab + ch * 2048, &tmV, ch * 64, row, &full[stage]);
+                    if constexpr (TRACE) rec[4 + j] = phys;
+                }
+                __syncwarp();
+                if (pf >= 0) {  // warp-uniform: j + d < e (Alg. 1 guard)
+                    const size_t off = ((size_t)pf * p.Hkv + kvh) * slab_elems;
+                    if (p.pf_mode == kPfBulk) {
+                        if (lane == 0) {
+                            bulk_prefetch_l2(p.k + off, G::kSlab);
+                            bulk_prefetch_l2(p.v + off, G::kSlab);
+                        }
+                    } else {
+                        constexpr int kLines = G::kSlab / 128;
+                        if (lane < kLines) {
+                            prefetch_line_l2(p.k + off + lane * 64);
+                            prefetch_line_l2(p.v + off + lane * 64);
+                        }
+                    }
+                    if constexpr (TRACE) {
+                        if (lane == 0) rec[4 + (p.trace_rec_len - 4) / 2 + npf] = pf;
+                    }
+                    ++npf;
+                }
+            }
+            cur = nxt;
+            pfv = pfn;
+        }
+        if constexpr (TRACE) {
+            if (lane == 0) {
+                rec[0] = s_tok;
+                rec[1] = e_tok;
+                rec[2] = n;
+                rec[3] = npf;
+            }
+        }
+        return;
+    }
+
+    // ============================== consumer warps ==============================
+    // Q as the B operand of S^T = K Q^T: B[k = d][n = h], register-resident.
+    uint32_t qf[KSTEPS][NT][2];
+    {
+        const int h = lane >> 2;
+        const int dq = 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int hh = nt * 8 + h;
+            const uint32_t* qrow =
+                reinterpret_cast<const uint32_t*>(p.q + ((size_t)b * p.Hq + kvh * g + hh) * D);
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                qf[kk][nt][0] = hh < g ? qrow[(kk * 16 + dq) >> 1] : 0u;
+                qf[kk][nt][1] = hh < g ? qrow[(kk * 16 + dq + 8) >> 1] : 0u;
+            }
+        }
+    }
+
+    float acc[MT][NT][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[i][nt][r] = 0.f;
+    float m_run[NT][2], l_run[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        m_run[nt][0] = m_run[nt][1] = -INFINITY;
+        l_run[nt][0] = l_run[nt][1] = 0.f;
+    }
+
+    // per-lane ldmatrix row/col selectors
+    const int k_t = (lane & 7) + ((lane >> 3) & 1) * 8;  // K rows (tokens) for A = K
+    const int k_c = (lane >> 4) * 8;
+    const int v_t = (lane & 7) + (lane >> 4) * 8;  // V rows (tokens) for A = V^T (trans)
+    const int v_c = ((lane >> 3) & 1) * 8;
+    const int r0 = lane >> 2;        // S^T accumulator rows (tokens) r0 and r0 + 8
+    const int t0 = 2 * (lane & 3);   // V^T fragment token columns t0, t0+1 (+8)
+
+    for (int j = warp; j < n; j += kConsumerWarps) {
+        const int stage = j % STAGES;
+        const uint32_t round = j / STAGES;
+        mbar_wait(&full[stage], round & 1);
+        const uint32_t kbase = smem_u32(ring + stage * G::kStage);
+        const uint32_t vbase = kbase + G::kSlab;
+        const int valid = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
+
+        // ---- S4: S^T[t][h] = sum_d K[t][d] Q[h][d]  (two accumulator chains)
+        float s[NT][4], s2[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            uint32_t a[4];
+            ldsm_x4(kbase + swz(k_t, kk * 16 + k_c), a[0], a[1], a[2], a[3]);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                if (kk & 1)
+                    mma_16816<BF16>(s2[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
+                else
+                    mma_16816<BF16>(s[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
+            }
+        }
+
+        // ---- S5: scale (fp32), mask t >= L, online softmax per head column
+        uint32_t pb[NT][2];      // P as PV B fragments (hi part for bf16)
+        uint32_t pb_lo[NT][2];   // bf16 residual part
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[nt][r] = (s[nt][r] + s2[nt][r]) * p.scale_log2;
+            if (valid < kBlockSize) {
+                if (r0 >= valid) s[nt][0] = s[nt][1] = -INFINITY;
+                if (r0 + 8 >= valid) s[nt][2] = s[nt][3] = -INFINITY;
+            }
+            float pr[4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float mx = fmaxf(s[nt][c], s[nt][c + 2]);
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
+                const float m_new = fmaxf(m_run[nt][c], mx);
+                const float alpha = ex2(m_run[nt][c] - m_new);
+                m_run[nt][c] = m_new;
+                pr[c] = ex2(s[nt][c] - m_new);
+                pr[c + 2] = ex2(s[nt][c + 2] - m_new);
+                l_run[nt][c] = l_run[nt][c] * alpha + pr[c] + pr[c + 2];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    acc[i][nt][c] *= alpha;
+                    acc[i][nt][c + 2] *= alpha;
+                }
+            }
+            // [t][h] 8x8 fragments -> transpose -> B[k = t][n = h]
+            const uint32_t w0 = pack2<BF16>(pr[0], pr[1]);
+            const uint32_t w1 = pack2<BF16>(pr[2], pr[3]);
+            pb[nt][0] = movmatrix_trans(w0);
+            pb[nt][1] = movmatrix_trans(w1);
+            if constexpr (BF16) {
+                // bf16 P keeps only 8 mantissa bits: carry the residual in a
+                // second bf16 term so P enters PV with ~16 bits (R19).
+                const float2 h0 = unpack2<true>(w0), h1 = unpack2<true>(w1);
+                pb_lo[nt][0] = movmatrix_trans(pack2<true>(pr[0] - h0.x, pr[1] - h0.y));
+                pb_lo[nt][1] = movmatrix_trans(pack2<true>(pr[2] - h1.x, pr[3] - h1.y));
+            }
+        }
+
+        // ---- S6: O^T[d][h] += sum_t V^T[d][t] P[t][h]
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            uint32_t a[4];
+            ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
+            if (valid < kBlockSize) {  // zero V rows t >= L (0 * NaN would poison)
+                const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+                const uint32_t m1 =
+                    (t0 + 8 < valid ? 0xffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
+                a[0] &= m0;
+                a[1] &= m0;
+                a[2] &= m1;
+                a[3] &= m1;
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                mma_16816<BF16>(acc[i][nt], a, pb[nt][0], pb[nt][1]);
+                if constexpr (BF16) mma_16816<BF16>(acc[i][nt], a, pb_lo[nt][0], pb_lo[nt][1]);
+            }
+        }
+        mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
+    }
+
+    // ---- S7: merge the consumer warps of this unit
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            float l = l_run[nt][c];
+            l += __shfl_xor_sync(kFull, l, 4);
+            l += __shfl_xor_sync(kFull, l, 8);
+            l += __shfl_xor_sync(kFull, l, 16);
+            l_run[nt][c] = l;
+        }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring reads done
+    if (lane < 4) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int h = nt * 8 + 2 * lane + c;
+                merge_m[warp * NH + h] = m_run[nt][c];
+                merge_l[warp * NH + h] = l_run[nt][c];
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int dd = i * 16 + r0 + 8 * (r >> 1);
+                const int h = nt * 8 + t0 + (r & 1);
+                merge_acc[(warp * NH + h) * (D + 4) + dd] = acc[i][nt][r];
+            }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+
+    const bool direct = n_parts == 1;
+    for (int idx = threadIdx.x; idx < g * D; idx += kConsumerWarps * 32) {
+        const int h = idx / D, dd = idx % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, merge_m[w * NH + h]);
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            const float sc = ex2(merge_m[w * NH + h] - M);
+            den += sc * merge_l[w * NH + h];
+            num += sc * merge_acc[(w * NH + h) * (D + 4) + dd];
+        }
+        const float o = num / den;
+        const size_t row = (size_t)b * p.Hq + kvh * g + h;
+        if (direct) {
+            store_out(p.out, row * D + dd, o, p.out_dtype);
+        } else {
+            p.ws_o[(row * p.p_max + part) * D + dd] = o;
+            if (dd == 0) p.ws_lse[row * p.p_max + part] = M + __log2f(den);
+        }
+    }
+}
+
+// S8: out = sum_p 2^(lse_p - M) o_p / sum_p 2^(lse_p - M), partitions in fixed order.
+template <int D>
+__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
+    constexpr int PER = D / 32;
+    const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= p.B * p.Hq) return;
+    const int b = row / p.Hq;
+    int L = p.lens[b];
+    L = L < p.max_tokens ? L : p.max_tokens;
+    const int n_parts = (L + p.part_tokens - 1) / p.part_tokens;
+    if (n_parts <= 1) return;  // written by the main kernel
+    const float* lse = p.ws_lse + (size_t)row * p.p_max;
+    float M = -INFINITY;
+    for (int i = lane; i < n_parts; i += 32) M = fmaxf(M, lse[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+    float accv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) accv[e] = 0.f;
+    float den = 0.f;
+    const float* o_base = p.ws_o + (size_t)row * p.p_max * D + lane * PER;
+    for (int part = 0; part < n_parts; ++part) {
+        const float w = ex2(lse[part] - M);
+        den += w;
+        const float* op = o_base + (size_t)part * D;
+        if constexpr (PER == 4) {
+            const float4 x = *reinterpret_cast<const float4*>(op);
+            accv[0] += w * x.x;
+            accv[1] += w * x.y;
+            accv[2] += w * x.z;
+            accv[3] += w * x.w;
+        } else {
+            const float2 x = *reinterpret_cast<const float2*>(op);
+            accv[0] += w * x.x;
+            accv[1] += w * x.y;
+        }
+    }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int e = 0; e < PER; ++e)
+        store_out(p.out, (size_t)row * D + lane * PER + e, accv[e] * inv, p.out_dtype);
+}
+
+template <int D, int NT, int STAGES>
+constexpr size_t smem_bytes_for() {
+    constexpr int ring = STAGES * Geometry<D>::kStage;
+    constexpr int merge = kConsumerWarps * 8 * NT * (D + 4) * 4;
+    constexpr int big = ring > merge ? ring : merge;
+    return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
+}
+
+template <bool BF16, int D, int NT, int STAGES, bool TRACE>
+cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                       dim3 grid, cudaStream_t stream) {
+    auto kern = splitk_kernel<BF16, D, NT, STAGES, TRACE>;
+    constexpr size_t smem = smem_bytes_for<D, NT, STAGES>();
+    static int configured_device = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_device != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured_device = dev;
+    }
+    kern<<<grid, (kConsumerWarps + 1) * 32, smem, stream>>>(tmK, tmV, p);
+    return cudaGetLastError();
+}
+
+template <bool BF16, int D, int NT, bool TRACE>
+cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                            int stages, dim3 grid, cudaStream_t s) {
+    switch (stages) {
+        case 4: return launch_one<BF16, D, NT, 4, TRACE>(tmK, tmV, p, grid, s);
+        case 8: return launch_one<BF16, D, NT, 8, TRACE>(tmK, tmV, p, grid, s);
+        case 12: return launch_one<BF16, D, NT, 12, TRACE>(tmK, tmV, p, grid, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool BF16, int D, bool TRACE>
+cudaError_t dispatch_nt(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                        int n_tiles, int stages, dim3 grid, cudaStream_t s) {
+    return n_tiles == 1 ? dispatch_stages<BF16, D, 1, TRACE>(tmK, tmV, p, stages, grid, s)
+                        : dispatch_stages<BF16, D, 2, TRACE>(tmK, tmV, p, stages, grid, s);
+}
+
+template <bool BF16, bool TRACE>
+cudaError_t dispatch_d(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                       int head_dim, int n_tiles, int stages, dim3 grid, cudaStream_t s) {
+    return head_dim == 64 ? dispatch_nt<BF16, 64, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s)
+                          : dispatch_nt<BF16, 128, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s);
+}
+
+}  // namespace
+
+size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages) {
+#define PDA_SMEM_CASE(DD, NN, SS) \
+    if (head_dim == DD && n_tiles == NN && stages == SS) return smem_bytes_for<DD, NN, SS>();
+    PDA_SMEM_CASE(64, 1, 4) PDA_SMEM_CASE(64, 1, 8) PDA_SMEM_CASE(64, 1, 12)
+    PDA_SMEM_CASE(64, 2, 4) PDA_SMEM_CASE(64, 2, 8) PDA_SMEM_CASE(64, 2, 12)
+    PDA_SMEM_CASE(128, 1, 4) PDA_SMEM_CASE(128, 1, 8) PDA_SMEM_CASE(128, 1, 12)
+    PDA_SMEM_CASE(128, 2, 4) PDA_SMEM_CASE(128, 2, 8) PDA_SMEM_CASE(128, 2, 12)
+#undef PDA_SMEM_CASE
+    return 0;
+}
+
+int splitk_threads() { return (kConsumerWarps + 1) * 32; }
+
+cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                          bool bf16, int head_dim, int n_tiles, int stages, bool trace, dim3 grid,
+                          cudaStream_t stream) {
+    if (bf16) {
+        return trace ? dispatch_d<true, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
+                     : dispatch_d<true, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);
+    }
+    return trace ? dispatch_d<false, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
+                 : dispatch_d<false, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);
+}
+
+cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream) {
+    const int rows = p.B * p.Hq;
+    const dim3 grid((rows + 3) / 4);
+    if (head_dim == 64)
+        combine_kernel<64><<<grid, 128, 0, stream>>>(p);
+    else
+        combine_kernel<128><<<grid, 128, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace pda

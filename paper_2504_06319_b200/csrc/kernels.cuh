@@ -1,0 +1,73 @@
+// kernels.cuh -- parameter blocks and host launchers shared by pda.cu and
+// the kernel translation units (internal; not part of the C ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pda {
+
+constexpr int kBlockSize = 16;     // tokens per KV block
+constexpr int kConsumerWarps = 4;  // split-K kernel consumer warps
+constexpr int kPaperWarps = 4;     // paper kernel: 128 threads = 4 warps (Table 2)
+
+enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };
+
+struct SplitKParams {
+    const uint16_t* q;  // [B, Hq, D]
+    const uint16_t* k;  // [num_blocks, Hkv, 16, D] (raw pointer: prefetch addresses)
+    const uint16_t* v;
+    const int32_t* bt;    // [B, max_blocks]
+    const int32_t* lens;  // [B]
+    void* out;            // [B, Hq, D]
+    float* ws_o;          // [B, Hq, P_max, D]   split-K partial outputs (normalised)
+    float* ws_lse;        // [B, Hq, P_max]      log2-sum-exp of each partition
+    int32_t* trace;       // debug trace (TRACE instantiation only)
+    int B, Hq, Hkv, g, max_blocks, part_tokens, p_max;
+    int out_dtype;
+    int pf_mode, pf_dist;
+    int trace_rec_len;
+    float scale_log2;  // scale * log2(e), fp32
+};
+
+struct PaperParams {
+    const uint16_t* q;
+    const uint16_t* k;
+    const uint16_t* v;
+    const int32_t* bt;
+    const int32_t* lens;
+    void* out;
+    int32_t* trace;
+    int B, Hq, Hkv, g, max_blocks;
+    int out_dtype;
+    int pf_mode, pf_dist;
+    int trace_rec_len;
+    float scale_log2;
+};
+
+struct CombineParams {
+    const float* ws_o;
+    const float* ws_lse;
+    const int32_t* lens;
+    void* out;
+    int B, Hq, p_max, part_tokens, max_tokens;
+    int out_dtype;
+};
+
+// Host launchers (return the launch's cudaError_t).
+cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                          bool bf16, int head_dim, int n_tiles, int stages, bool trace,
+                          dim3 grid, cudaStream_t stream);
+size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages);
+int splitk_threads();
+
+cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
+
+cudaError_t launch_paper(const PaperParams& p, bool bf16, int head_dim, bool trace, dim3 grid,
+                         cudaStream_t stream);
+
+cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms,
+                                 cudaStream_t stream);
+
+}  // namespace pda

@@ -1,0 +1,341 @@
+// pda.cu -- the C ABI (include/pda.h): argument validation, the split-K
+// planner (S0), TMA tensor-map construction and kernel dispatch.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/pda.h"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int kDefaultStages = 8;
+constexpr int kDefaultSms = 148;  // B200
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+size_t elem_bytes(int dt) { return dt == PDA_F32 ? 4 : 2; }
+
+pda_status validate(const pda_shape* s, const pda_options* o) {
+    if (!s || !o) return PDA_ERR_NULL;
+    if (s->num_seqs < 0 || s->num_seqs > 65535 || s->num_q_heads <= 0 || s->num_kv_heads <= 0 ||
+        s->num_q_heads % s->num_kv_heads != 0 || s->head_dim <= 0 || s->block_size <= 0 ||
+        s->num_blocks <= 0 || s->max_blocks_per_seq <= 0 || s->num_q_heads > 65535)
+        return PDA_ERR_SHAPE;
+    if ((int64_t)s->num_blocks * s->num_kv_heads * s->block_size >= (int64_t(1) << 31))
+        return PDA_ERR_SHAPE;  // TMA row coordinates are int32
+    if ((int64_t)s->max_blocks_per_seq * s->block_size >= (int64_t(1) << 30)) return PDA_ERR_SHAPE;
+    if (s->dtype != PDA_F16 && s->dtype != PDA_BF16) return PDA_ERR_UNSUPPORTED;
+    if (s->out_dtype != s->dtype && s->out_dtype != PDA_F32) return PDA_ERR_UNSUPPORTED;
+    if (s->head_dim != 64 && s->head_dim != 128) return PDA_ERR_UNSUPPORTED;
+    if (s->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
+    if (s->num_q_heads / s->num_kv_heads > 16) return PDA_ERR_UNSUPPORTED;
+    if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_LINE_L2) return PDA_ERR_SHAPE;
+    if (o->prefetch != PDA_PF_OFF && (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
+        return PDA_ERR_SHAPE;
+    if (o->partition_tokens < 0 || o->partition_tokens % s->block_size != 0) return PDA_ERR_SHAPE;
+    if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 && o->smem_stages != 12)
+        return PDA_ERR_UNSUPPORTED;
+    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_SPLITK) return PDA_ERR_SHAPE;
+    if (o->num_sms < 0) return PDA_ERR_SHAPE;
+    return PDA_OK;
+}
+
+pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
+    pda_status st = validate(s, o);
+    if (st != PDA_OK) return st;
+    std::memset(pl, 0, sizeof(*pl));
+    const int B = s->num_seqs, Hq = s->num_q_heads, Hkv = s->num_kv_heads, D = s->head_dim;
+    const int64_t max_tokens = (int64_t)s->max_blocks_per_seq * s->block_size;
+    if (o->kernel == PDA_KERNEL_PAPER) {
+        // grid [H, B, 1], N_thread = 128 (Table 2)
+        pl->kernel = PDA_KERNEL_PAPER;
+        pl->partition_tokens = (int32_t)max_tokens;
+        pl->p_max = 1;
+        pl->smem_stages = 0;
+        pl->grid_x = Hq;
+        pl->grid_y = B;
+        pl->grid_z = 1;
+        pl->threads = pda::kPaperWarps * 32;
+        const int R = (int)ceil_div(s->max_blocks_per_seq, pda::kPaperWarps);
+        pl->trace_rec_len = 4 + 2 * R;
+        pl->trace_records = B * Hq * pda::kPaperWarps;
+        pl->workspace_bytes = 0;
+        return PDA_OK;
+    }
+    // S0: split-K plan.  Units (partition, kv head, seq) are independent; pick
+    // the partition size so the grid holds >= 4 waves of resident CTAs while a
+    // partition keeps >= 512 tokens (32 blocks) to amortise pipeline fill.
+    const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
+    const int stages = o->smem_stages ? o->smem_stages : kDefaultStages;
+    const int sms = o->num_sms ? o->num_sms : kDefaultSms;
+    int64_t P;
+    if (o->partition_tokens > 0) {
+        P = o->partition_tokens;
+    } else {
+        const int64_t units0 = (int64_t)B * Hkv;
+        const int64_t conc = (int64_t)sms * (n_tiles == 1 ? 3 : 2);
+        int64_t split = 1;
+        while (units0 * split < 4 * conc && max_tokens / (split * 2) >= 512) split *= 2;
+        P = ceil_div(ceil_div(max_tokens, split), s->block_size) * s->block_size;
+    }
+    const int64_t p_max = ceil_div(max_tokens, P);
+    pl->kernel = PDA_KERNEL_SPLITK;
+    pl->partition_tokens = (int32_t)(P < max_tokens ? P : ceil_div(max_tokens, s->block_size) * s->block_size);
+    pl->p_max = (int32_t)p_max;
+    pl->smem_stages = stages;
+    pl->grid_x = (int32_t)p_max;
+    pl->grid_y = Hkv;
+    pl->grid_z = B;
+    pl->threads = pda::splitk_threads();
+    pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
+    pl->trace_records = (int32_t)(B * Hkv * p_max);
+    pl->workspace_bytes =
+        p_max > 1 ? align256((size_t)B * Hq * p_max * D * 4) + align256((size_t)B * Hq * p_max * 4) : 0;
+    return PDA_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D view of a [num_blocks, Hkv, 16, D] cache: rows = num_blocks * Hkv * 16,
+// cols = D; box = 16 rows x 64 cols (one 128-byte swizzle atom wide).
+bool encode_cache_map(CUtensorMap* m, const void* base, const pda_shape* s) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)s->head_dim,
+                                (cuuint64_t)s->num_blocks * s->num_kv_heads * s->block_size};
+    const cuuint64_t strides[1] = {(cuuint64_t)s->head_dim * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)s->block_size};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The caller's tensors may live on any device of the process: run on theirs.
+pda_status use_device_of(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return PDA_ERR_CUDA;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return PDA_OK;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != a.device && cudaSetDevice(a.device) != cudaSuccess) return PDA_ERR_CUDA;
+    return PDA_OK;
+}
+
+pda_status run(const void* q, const void* k_cache, const void* v_cache, const int32_t* bt,
+               const int32_t* lens, float scale, void* out, const pda_shape* s,
+               const pda_options* o, void* ws, size_t ws_bytes, int32_t* trace, size_t trace_words,
+               cudaStream_t stream) {
+    pda_plan_info pl;
+    pda_status st = plan(s, o, &pl);
+    if (st != PDA_OK) return st;
+    if (!q || !k_cache || !v_cache || !bt || !lens || !out) return PDA_ERR_NULL;
+    if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out) ||
+        !aligned16(ws))
+        return PDA_ERR_ALIGN;
+    if (pl.workspace_bytes > 0 && (!ws || ws_bytes < pl.workspace_bytes)) return PDA_ERR_WORKSPACE;
+    if (trace && trace_words < (size_t)pl.trace_records * pl.trace_rec_len) return PDA_ERR_SHAPE;
+    if (s->num_seqs == 0) return PDA_OK;
+    st = use_device_of(out);
+    if (st != PDA_OK) return st;
+
+    const float scale_log2 = (float)((double)scale * 1.4426950408889634);
+    const int prefetch_mode = o->prefetch;
+    const int pf_dist = o->prefetch != PDA_PF_OFF ? o->prefetch_distance : 0;
+    if (trace && cudaMemsetAsync(trace, 0xff, (size_t)pl.trace_records * pl.trace_rec_len * 4,
+                                 stream) != cudaSuccess)
+        return PDA_ERR_CUDA;
+
+    cudaError_t err;
+    if (pl.kernel == PDA_KERNEL_PAPER) {
+        pda::PaperParams p{};
+        p.q = static_cast<const uint16_t*>(q);
+        p.k = static_cast<const uint16_t*>(k_cache);
+        p.v = static_cast<const uint16_t*>(v_cache);
+        p.bt = bt;
+        p.lens = lens;
+        p.out = out;
+        p.trace = trace;
+        p.B = s->num_seqs;
+        p.Hq = s->num_q_heads;
+        p.Hkv = s->num_kv_heads;
+        p.g = s->num_q_heads / s->num_kv_heads;
+        p.max_blocks = s->max_blocks_per_seq;
+        p.out_dtype = s->out_dtype;
+        p.pf_mode = prefetch_mode;
+        p.pf_dist = pf_dist;
+        p.trace_rec_len = pl.trace_rec_len;
+        p.scale_log2 = scale_log2;
+        err = pda::launch_paper(p, s->dtype == PDA_BF16, s->head_dim, trace != nullptr,
+                                dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream);
+        return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
+    }
+
+    CUtensorMap tmK, tmV;
+    if (!encode_cache_map(&tmK, k_cache, s) || !encode_cache_map(&tmV, v_cache, s))
+        return PDA_ERR_CUDA;
+    pda::SplitKParams p{};
+    p.q = static_cast<const uint16_t*>(q);
+    p.k = static_cast<const uint16_t*>(k_cache);
+    p.v = static_cast<const uint16_t*>(v_cache);
+    p.bt = bt;
+    p.lens = lens;
+    p.out = out;
+    const size_t o_bytes = align256((size_t)s->num_seqs * s->num_q_heads * pl.p_max * s->head_dim * 4);
+    p.ws_o = pl.p_max > 1 ? static_cast<float*>(ws) : nullptr;
+    p.ws_lse = pl.p_max > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
+    p.trace = trace;
+    p.B = s->num_seqs;
+    p.Hq = s->num_q_heads;
+    p.Hkv = s->num_kv_heads;
+    p.g = s->num_q_heads / s->num_kv_heads;
+    p.max_blocks = s->max_blocks_per_seq;
+    p.part_tokens = pl.partition_tokens;
+    p.p_max = pl.p_max;
+    p.out_dtype = s->out_dtype;
+    p.pf_mode = prefetch_mode;
+    p.pf_dist = pf_dist;
+    p.trace_rec_len = pl.trace_rec_len;
+    p.scale_log2 = scale_log2;
+    const int n_tiles = p.g <= 8 ? 1 : 2;
+    err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
+                             pl.smem_stages, trace != nullptr,
+                             dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream);
+    if (err != cudaSuccess) return PDA_ERR_CUDA;
+    if (pl.p_max > 1) {
+        pda::CombineParams c{};
+        c.ws_o = p.ws_o;
+        c.ws_lse = p.ws_lse;
+        c.lens = lens;
+        c.out = out;
+        c.B = p.B;
+        c.Hq = p.Hq;
+        c.p_max = p.p_max;
+        c.part_tokens = p.part_tokens;
+        c.max_tokens = s->max_blocks_per_seq * s->block_size;
+        c.out_dtype = s->out_dtype;
+        err = pda::launch_combine(c, s->head_dim, stream);
+        if (err != cudaSuccess) return PDA_ERR_CUDA;
+    }
+    return PDA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pda_status pda_check_args(const pda_shape* shape, const pda_options* opt) {
+    return validate(shape, opt);
+}
+
+pda_status pda_plan(const pda_shape* shape, const pda_options* opt, pda_plan_info* out) {
+    if (!out) return PDA_ERR_NULL;
+    return plan(shape, opt, out);
+}
+
+size_t pda_workspace_bytes(const pda_shape* shape, const pda_options* opt) {
+    pda_plan_info pl;
+    return plan(shape, opt, &pl) == PDA_OK ? pl.workspace_bytes : 0;
+}
+
+pda_status paged_decode_attention(const void* q, const void* k_cache, const void* v_cache,
+                                  const int32_t* block_tables, const int32_t* context_lens,
+                                  float scale, void* out, const pda_shape* shape,
+                                  const pda_options* opt, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
+               workspace_bytes, nullptr, 0, static_cast<cudaStream_t>(stream));
+}
+
+pda_status paged_decode_attention_trace(const void* q, const void* k_cache, const void* v_cache,
+                                        const int32_t* block_tables,
+                                        const int32_t* context_lens, float scale, void* out,
+                                        const pda_shape* shape, const pda_options* opt,
+                                        void* workspace, size_t workspace_bytes, int32_t* trace,
+                                        size_t trace_words, void* stream) {
+    if (!trace) return PDA_ERR_NULL;
+    return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
+               workspace_bytes, trace, trace_words, static_cast<cudaStream_t>(stream));
+}
+
+pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_host,
+                                const int32_t* context_lens_host, void* out_host, void* q_dev,
+                                int32_t* block_tables_dev, int32_t* context_lens_dev,
+                                void* out_dev, const void* k_cache, const void* v_cache,
+                                float scale, const pda_shape* shape, const pda_options* opt,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+    pda_status st = validate(shape, opt);
+    if (st != PDA_OK) return st;
+    if (!q_host || !block_tables_host || !context_lens_host || !out_host || !q_dev ||
+        !block_tables_dev || !context_lens_dev || !out_dev)
+        return PDA_ERR_NULL;
+    st = use_device_of(out_dev);
+    if (st != PDA_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t B = shape->num_seqs;
+    const size_t q_bytes = B * shape->num_q_heads * shape->head_dim * 2;
+    const size_t bt_bytes = B * shape->max_blocks_per_seq * 4;
+    const size_t out_bytes = B * shape->num_q_heads * shape->head_dim * elem_bytes(shape->out_dtype);
+    if (cudaMemcpyAsync(q_dev, q_host, q_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(block_tables_dev, block_tables_host, bt_bytes, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(context_lens_dev, context_lens_host, B * 4, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess)
+        return PDA_ERR_CUDA;
+    st = run(q_dev, k_cache, v_cache, block_tables_dev, context_lens_dev, scale, out_dev, shape, opt,
+             workspace, workspace_bytes, nullptr, 0, s);
+    if (st != PDA_OK) return st;
+    if (cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return PDA_ERR_CUDA;
+    return PDA_OK;
+}
+
+pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream) {
+    if (!buf || !sink) return PDA_ERR_NULL;
+    if (!aligned16(buf) || !aligned16(sink)) return PDA_ERR_ALIGN;
+    pda_status st = use_device_of(buf);
+    if (st != PDA_OK) return st;
+    int dev = 0, sms = kDefaultSms;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return pda::launch_read_roofline(buf, bytes, sink, sms, static_cast<cudaStream_t>(stream)) ==
+                   cudaSuccess
+               ? PDA_OK
+               : PDA_ERR_CUDA;
+}
+
+const char* pda_status_string(pda_status status) {
+    switch (status) {
+        case PDA_OK: return "PDA_OK";
+        case PDA_ERR_NULL: return "PDA_ERR_NULL: a required pointer is NULL";
+        case PDA_ERR_SHAPE: return "PDA_ERR_SHAPE: inconsistent or out-of-range sizes/options";
+        case PDA_ERR_UNSUPPORTED: return "PDA_ERR_UNSUPPORTED: head_dim/block_size/group/dtype not supported";
+        case PDA_ERR_ALIGN: return "PDA_ERR_ALIGN: a base pointer is not 16-byte aligned";
+        case PDA_ERR_WORKSPACE: return "PDA_ERR_WORKSPACE: workspace missing or too small";
+        case PDA_ERR_CUDA: return "PDA_ERR_CUDA: a CUDA call or kernel launch failed";
+    }
+    return "PDA_ERR_UNKNOWN";
+}
+
+int32_t pda_abi_version(void) { return 1; }
+
+}  // extern "C"

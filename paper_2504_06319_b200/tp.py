@@ -1,0 +1,74 @@
+"""Tensor-parallel decode attention: KV heads sharded across ranks (one
+process per GPU), NCCL all-gather of the per-rank output heads.
+
+The paper runs vLLM tensor parallelism, where "each GPU processes 1/N of the
+heads".  A GQA group is never split: rank r owns KV heads
+[r*Hkv/N, (r+1)*Hkv/N) and the q heads that read them,
+[r*Hq/N, (r+1)*Hq/N); block tables and context lengths are replicated.  The
+only exchange is the output all-gather: each rank's
+[B, Hq/N, D] slice goes out with one all_gather_into_tensor on the compute
+stream; the gathered [N, B, Hq/N, D] buffer is returned as a [B, N, Hq/N, D]
+view whose flattening is [B, Hq, D] -- no extra copy on the step.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def shard_range(num_heads: int, rank: int, world: int):
+    if num_heads % world:
+        raise ValueError(f"{num_heads} heads do not divide over {world} ranks")
+    n = num_heads // world
+    return rank * n, (rank + 1) * n
+
+
+def gather_heads(out_local: torch.Tensor, group=None, gathered: torch.Tensor | None = None):
+    """All-gather [B, Hq/N, D] slices -> [B, N, Hq/N, D] view (head order = rank order)."""
+    world = dist.get_world_size(group)
+    B, hl, D = out_local.shape
+    if gathered is None:
+        gathered = torch.empty((world * B, hl, D), dtype=out_local.dtype, device=out_local.device)
+    dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group)
+    return gathered.view(world, B, hl, D).permute(1, 0, 2, 3)
+
+
+class TPDecodeAttention:
+    """One rank's share of a tensor-parallel decode attention step.
+
+    k_cache / v_cache hold only this rank's KV heads ([num_blocks, Hkv/N, 16, D]);
+    q_local holds this rank's q heads.  __call__ runs the CUDA decode kernels
+    on the local shard and all-gathers the heads.
+    """
+
+    def __init__(self, k_cache, v_cache, num_seqs, num_q_heads_local, max_blocks, dtype, group=None,
+                 **opts):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        D = k_cache.shape[-1]
+        dev = k_cache.device
+        self.k, self.v = k_cache, v_cache
+        self.opts = opts
+        self.out_local = torch.empty((num_seqs, num_q_heads_local, D), dtype=dtype, device=dev)
+        self.gathered = torch.empty((self.world * num_seqs, num_q_heads_local, D), dtype=dtype,
+                                    device=dev)
+        shape = _lib.make_shape(self.out_local, k_cache,
+                                torch.empty((num_seqs, max_blocks), dtype=torch.int32, device="meta"))
+        opt = _lib.make_options(**{k: v for k, v in opts.items()
+                                   if k in ("prefetch", "prefetch_distance", "partition_tokens",
+                                            "smem_stages", "kernel")})
+        self.plan = _lib.plan(shape, opt)
+        wsb = self.plan["workspace_bytes"]
+        self.ws = torch.empty(max(1, wsb), dtype=torch.uint8, device=dev)
+
+    def launches_per_step(self) -> int:
+        return 1 + (1 if self.plan["p_max"] > 1 else 0)
+
+    def __call__(self, q_local, block_tables, context_lens, scale):
+        _lib.paged_decode_attention(q_local, self.k, self.v, block_tables, context_lens, scale,
+                                    out=self.out_local, workspace=self.ws, **self.opts)
+        if self.world == 1:
+            return self.out_local.unsqueeze(1)
+        return gather_heads(self.out_local, self.group, self.gathered)

@@ -1,0 +1,155 @@
+"""Host-only checks of the C ABI (-m "not gpu"): the library loads, exports
+every symbol include/pda.h declares, validates arguments synchronously
+without a CUDA context, and plans launches deterministically."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+import paper_2504_06319_b200 as pda
+from paper_2504_06319_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2504_06319_b200 import build
+    build.build()
+
+
+def test_exports_every_header_symbol():
+    syms = pda.header_symbols()
+    assert {"paged_decode_attention", "paged_decode_attention_trace", "pda_check_args", "pda_plan",
+            "pda_workspace_bytes", "pda_decode_step_host", "pda_read_roofline", "pda_status_string",
+            "pda_abi_version"} <= set(syms)
+    L = pda.lib()
+    for s in syms:
+        assert hasattr(L, s), f"libpda.so does not export {s}"
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for s in syms:
+        assert f" T {s}" in nm
+
+
+def test_sass_targets_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for mnemonic in ("UTMALDG", "UBLKPF", "HMMA.16816.F32", "LDSM", "MOVM", "SYNCS"):
+        assert mnemonic in sass, f"{mnemonic} missing from SASS"
+
+
+def shape(**kw):
+    d = dict(num_seqs=2, num_q_heads=4, num_kv_heads=2, head_dim=64, block_size=16, num_blocks=32,
+             max_blocks_per_seq=16, dtype=0, out_dtype=0)
+    d.update(kw)
+    return _lib.Shape(**d)
+
+
+def opts(**kw):
+    d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0)
+    d.update(kw)
+    return _lib.Options(**d)
+
+
+@pytest.mark.parametrize("kw,status", [
+    ({}, 0),
+    (dict(head_dim=96), 3),
+    (dict(block_size=32), 3),
+    (dict(num_q_heads=6, num_kv_heads=4), 2),
+    (dict(num_q_heads=34, num_kv_heads=2), 3),
+    (dict(dtype=2), 3),
+    (dict(out_dtype=1), 3),
+    (dict(out_dtype=2), 0),
+    (dict(num_seqs=-1), 2),
+    (dict(num_blocks=0), 2),
+])
+def test_check_args_shape(kw, status):
+    assert pda.check_args(shape(**kw), opts()) == status
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(prefetch=1, prefetch_distance=0), 2),
+    (dict(prefetch=0, prefetch_distance=0), 0),
+    (dict(prefetch=3), 2),
+    (dict(partition_tokens=24), 2),
+    (dict(partition_tokens=32), 0),
+    (dict(smem_stages=6), 3),
+    (dict(kernel=7), 2),
+])
+def test_check_args_options(kw, status):
+    assert pda.check_args(shape(), opts(**kw)) == status
+
+
+def test_null_args():
+    L = pda.lib()
+    assert L.pda_check_args(None, ctypes.byref(opts())) == 1
+    assert L.pda_workspace_bytes(None, None) == 0
+    rc = L.paged_decode_attention(None, None, None, None, None, 1.0, None, ctypes.byref(shape()),
+                                  ctypes.byref(opts()), None, 0, None)
+    assert rc == 1
+
+
+def test_misaligned_pointer_rejected_before_launch():
+    L = pda.lib()
+    base = 0x10000000
+    rc = L.paged_decode_attention(base + 2, base, base, base, base, 1.0, base, ctypes.byref(shape()),
+                                  ctypes.byref(opts()), None, 0, None)
+    assert rc == 4
+
+
+def test_workspace_required():
+    L = pda.lib()
+    s, o = shape(max_blocks_per_seq=64), opts(partition_tokens=256)
+    need = pda.workspace_bytes(s, o)
+    assert need > 0
+    base = 0x10000000
+    rc = L.paged_decode_attention(base, base, base, base, base, 1.0, base, ctypes.byref(s),
+                                  ctypes.byref(o), None, 0, None)
+    assert rc == 5
+
+
+def test_plan_no_split_llama2():
+    # C2: B=64, 32 kv heads, ctx 4096: 2048 units already fill >= 4 waves -> one partition
+    s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
+              max_blocks_per_seq=256)
+    p = pda.plan(s, opts())
+    assert p["p_max"] == 1 and p["partition_tokens"] == 4096 and p["workspace_bytes"] == 0
+    assert (p["grid_x"], p["grid_y"], p["grid_z"]) == (1, 32, 64) and p["threads"] == 160
+    assert p["trace_rec_len"] == 4 + 2 * 256 and p["trace_records"] == 64 * 32
+
+
+def test_plan_split_llama3_8b():
+    # C3: 1024 units < 4 waves of 444 -> split 2 -> P = 4096
+    s = shape(num_seqs=128, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=65537,
+              max_blocks_per_seq=512, dtype=1, out_dtype=1)
+    p = pda.plan(s, opts())
+    assert p["p_max"] == 2 and p["partition_tokens"] == 4096
+    B, Hq, P, D = 128, 32, 2, 128
+    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
+
+
+def test_plan_explicit_partition_and_paper():
+    s = shape()
+    p = pda.plan(s, opts(partition_tokens=48))
+    assert p["partition_tokens"] == 48 and p["p_max"] == 6 and p["trace_rec_len"] == 4 + 2 * 3
+    pp = pda.plan(s, opts(kernel=1))
+    assert pp["kernel"] == 1 and (pp["grid_x"], pp["grid_y"]) == (4, 2) and pp["threads"] == 128
+    assert pp["trace_rec_len"] == 4 + 2 * 4 and pp["trace_records"] == 2 * 4 * 4
+
+
+def test_status_strings():
+    for code in range(7):
+        assert pda.status_string(code).startswith("PDA_")
+    assert pda.lib().pda_abi_version() == 1
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2504_06319_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "oracle.c" not in text and "liboracle" not in text, f

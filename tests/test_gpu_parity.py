@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle (-m gpu).
+
+Tolerance (BASELINE.json north_star): max abs error <= 2e-3 for fp16/bf16
+inputs with fp32 accumulation; bookkeeping (visited blocks, partition
+ranges, prefetch targets and counts) bit-exact against oracle plans;
+prefetch on/off, placement and run-to-run bitwise invariant.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def pda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_06319_b200 as m
+    m.lib()  # must load; no fallback
+    return m
+
+
+def oracle_out(oracle_mod, inp, rows=None):
+    return oracle_mod.paged_attention(inp["q"].cpu(), inp["k_cache"].cpu(), inp["v_cache"].cpu(),
+                                      inp["block_tables"].cpu(), inp["context_lens"].cpu(), inp["scale"],
+                                      inp["cfg"].dtype, rows=rows)
+
+
+def to_dev(inp):
+    d = dict(inp)
+    for k in ("q", "k_cache", "v_cache", "block_tables", "context_lens"):
+        d[k] = inp[k].cuda()
+    return d
+
+
+def gpu(pda, inp, **kw):
+    return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                      inp["context_lens"], inp["scale"], **kw)
+
+
+def max_err(gpu_out, ref):
+    g = gpu_out.double().cpu().numpy()
+    assert np.isfinite(g).all(), "non-finite output"
+    return float(np.abs(g - ref).max())
+
+
+SHAPES = [
+    synth.C1_TINY,
+    synth.Config("mha128_ragged", 4, 4, 4, 128, (1, 15, 17, 300), "fp16", poison_blocks=5),
+    synth.Config("gqa4_bf16", 3, 16, 4, 128, (100, 1000, 513), "bf16", poison_blocks=3),
+    synth.Config("gqa8_bf16", 2, 16, 2, 128, (777, 64), "bf16", poison_blocks=2),
+    synth.Config("gqa16_fp16", 2, 32, 2, 128, (95, 250), "fp16", poison_blocks=2),
+    synth.Config("gqa7_d64", 2, 14, 2, 64, (123, 40), "bf16", poison_blocks=2),
+    synth.Config("zero_len", 3, 4, 2, 64, (0, 5, 0), "fp16", poison_blocks=1),
+]
+KERNELS = [dict(kernel="splitk"), dict(kernel="splitk", partition_tokens=16),
+           dict(kernel="splitk", partition_tokens=64), dict(kernel="splitk", smem_stages=4),
+           dict(kernel="splitk", smem_stages=12, partition_tokens=256), dict(kernel="paper")]
+
+
+@pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: c.name)
+@pytest.mark.parametrize("kw", KERNELS, ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()))
+def test_parity_vs_oracle(pda, oracle_mod, cfg, kw):
+    inp = synth.make_inputs(cfg, seed=17)
+    ref = oracle_out(oracle_mod, inp)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, **kw)
+    torch.cuda.synchronize()
+    assert max_err(out, ref) <= TOL
+    out32 = gpu(pda, dev, out_dtype=torch.float32, **kw)
+    assert max_err(out32, ref) <= TOL
+
+
+@pytest.mark.parametrize("cfg", SHAPES[:4], ids=lambda c: c.name)
+@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+def test_prefetch_is_bitwise_invisible(pda, cfg, kernel):
+    """Prefetch changes where data is found, not what is computed."""
+    dev = to_dev(synth.make_inputs(cfg, seed=3))
+    base = gpu(pda, dev, kernel=kernel, prefetch="off")
+    for mode in ("bulk", "line"):
+        for d in (1, 2, 4, 7, 64):
+            o = gpu(pda, dev, kernel=kernel, prefetch=mode, prefetch_distance=d)
+            assert torch.equal(o, base), (mode, d)
+
+
+@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+def test_placement_invariance_bitwise(pda, kernel):
+    inp = synth.make_inputs(SHAPES[2], seed=5)
+    a = gpu(pda, to_dev(inp), kernel=kernel)
+    b = gpu(pda, to_dev(synth.permute_placement(inp, seed=99)), kernel=kernel)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+def test_run_to_run_bitwise(pda, kernel):
+    dev = to_dev(synth.make_inputs(SHAPES[3], seed=8))
+    a = gpu(pda, dev, kernel=kernel, partition_tokens=0 if kernel == "paper" else 128)
+    for _ in range(3):
+        b = gpu(pda, dev, kernel=kernel, partition_tokens=0 if kernel == "paper" else 128)
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+def test_context_len_one_returns_v_row_exactly(pda, dtype, kernel):
+    cfg = synth.Config("l1", 3, 8, 2, 128, (1, 1, 1), dtype, poison_blocks=4)
+    inp = synth.make_inputs(cfg, seed=2)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, kernel=kernel)
+    for b in range(3):
+        blk = int(inp["block_tables"][b, 0])
+        for h in range(8):
+            assert torch.equal(out[b, h].cpu(), inp["v_cache"][blk, h // 4, 0])
+
+
+@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+def test_needle_every_position(pda, kernel):
+    cfg = synth.Config("needle", 1, 2, 1, 64, (37,), "fp16", poison_blocks=2)
+    base = synth.make_inputs(cfg, seed=9)
+    bt = base["block_tables"][0]
+    for t_star in range(37):
+        inp = {k: (v.clone() if torch.is_tensor(v) else v) for k, v in base.items()}
+        inp["q"].zero_()
+        inp["q"][0, :, 0] = 1.0
+        for t in range(37):
+            inp["k_cache"][int(bt[t // 16]), 0, t % 16, 0] = 40.0 if t == t_star else 0.0
+        inp["scale"] = 1.0
+        out = gpu(pda, to_dev(inp), kernel=kernel, out_dtype=torch.float32, partition_tokens=0
+                  if kernel == "paper" else 16)
+        v = inp["v_cache"][int(bt[t_star // 16]), 0, t_star % 16].float()
+        assert torch.allclose(out[0, 0].cpu(), v, atol=1e-5, rtol=0), t_star
+
+
+def test_gqa_identical_queries_identical_outputs(pda):
+    cfg = synth.Config("gqa", 2, 8, 2, 128, (200, 33), "bf16")
+    inp = synth.make_inputs(cfg, seed=4)
+    inp["q"][:, 1:4] = inp["q"][:, 0:1]
+    out = gpu(pda, to_dev(inp))
+    for h in (1, 2, 3):
+        assert torch.equal(out[:, h], out[:, 0])
+
+
+def test_split_sizes_agree(pda, oracle_mod):
+    cfg = synth.Config("splits", 2, 8, 2, 128, (1000, 517), "fp16", poison_blocks=1)
+    inp = synth.make_inputs(cfg, seed=12)
+    ref = oracle_out(oracle_mod, inp)
+    dev = to_dev(inp)
+    outs = [gpu(pda, dev, partition_tokens=p, out_dtype=torch.float32) for p in (16, 64, 256, 1024, 0)]
+    for o in outs:
+        assert max_err(o, ref) <= 5e-4  # fp32 out: only P / accumulation rounding remains
+
+
+def test_trace_splitk_matches_oracle_plan(pda, oracle_mod):
+    cfg = synth.Config("trace", 3, 8, 2, 64, (37, 256, 0), "fp16", poison_blocks=3)
+    dev = to_dev(synth.make_inputs(cfg, seed=1))
+    for P in (16, 64, 128, 0):
+        for mode, d in (("off", 0), ("bulk", 1), ("bulk", 3), ("line", 4), ("bulk", 40)):
+            _, tr, info = gpu(pda, dev, kernel="splitk", partition_tokens=P, prefetch=mode,
+                              prefetch_distance=d or None, trace=True)
+            ref = oracle_mod.plan_splitk(dev["block_tables"], dev["context_lens"], cfg.num_kv_heads, 16,
+                                         info["partition_tokens"], info["p_max"], d)
+            got = tr.cpu().numpy().reshape(ref.shape)
+            assert np.array_equal(got, ref), (P, mode, d)
+
+
+def test_trace_paper_matches_alg1(pda, oracle_mod):
+    cfg = synth.Config("trace_p", 3, 4, 2, 128, (16, 128, 300), "fp16", poison_blocks=3)
+    dev = to_dev(synth.make_inputs(cfg, seed=2))
+    for mode, d in (("off", 0), ("bulk", 4), ("line", 4), ("bulk", 1), ("bulk", 9)):
+        _, tr, info = gpu(pda, dev, kernel="paper", prefetch=mode, prefetch_distance=d or None,
+                          trace=True)
+        ref = oracle_mod.plan_paper(dev["block_tables"], dev["context_lens"], cfg.num_q_heads, 16, 4, d)
+        got = tr.cpu().numpy().reshape(ref.shape)
+        assert np.array_equal(got, ref), (mode, d)
+        if d == 4:  # 1 block/warp -> 0 prefetches; 2 blocks/warp -> 1 per warp
+            assert got[0, :, :, 3].sum() == 0
+            assert (got[1, :, :, 3] == 1).all()
+
+
+def test_host_e2e_step_matches_device_path(pda):
+    cfg = synth.Config("e2e", 4, 8, 2, 128, (300, 64, 1, 999), "bf16")
+    inp = synth.make_inputs(cfg, seed=21)
+    dev = to_dev(inp)
+    ref = gpu(pda, dev)
+    step = pda.HostDecodeStep(dev["k_cache"], dev["v_cache"], 4, 8, cfg.max_blocks_per_seq, torch.bfloat16)
+    qh = inp["q"].pin_memory()
+    bth = inp["block_tables"].pin_memory()
+    lh = inp["context_lens"].pin_memory()
+    out = step(qh, bth, lh, inp["scale"])
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref.cpu())
+
+
+def test_nan_poison_never_leaks(pda):
+    cfg = synth.Config("poison", 4, 8, 8, 128, (17, 31, 33, 1), "fp16", poison_blocks=20)
+    dev = to_dev(synth.make_inputs(cfg, seed=3))
+    for kw in KERNELS:
+        assert torch.isfinite(gpu(pda, dev, **kw)).all()
+
+
+def test_rejects_cpu_tensors(pda):
+    inp = synth.make_inputs(synth.C1_TINY, seed=0)
+    with pytest.raises(ValueError):
+        gpu(pda, inp)
+
+
+# ---- full BASELINE sizes, in bench.py's launch configuration, sampled rows ----
+
+def sampled_check(pda, oracle_mod, cfg, seqs, **kw):
+    inp = synth.make_inputs(cfg, seed=0, device="cuda")
+    out = gpu(pda, inp, **kw)
+    torch.cuda.synchronize()
+    sub = synth.sample_rows(inp, seqs)
+    ref = oracle_out(oracle_mod, sub)
+    got = out[list(seqs)]
+    assert max_err(got, ref) <= TOL
+    assert torch.isfinite(out).all()
+    del inp, out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
+def test_full_size_sampled(pda, oracle_mod, cfg):
+    B = cfg.num_seqs
+    sampled_check(pda, oracle_mod, cfg, [0, B // 2, B - 1])
+    sampled_check(pda, oracle_mod, cfg, [1, B - 2], prefetch="off")
+
+
+def test_full_size_c5_tp8_shard(pda, oracle_mod):
+    """Llama-3-70B shape, one TP=8 rank's shard (1 KV head, 8 q heads)."""
+    cfg = synth.C5_LLAMA3_70B.with_heads(8, 1, name="c5_tp8_rank")
+    sampled_check(pda, oracle_mod, cfg, [0, 128, 255])
+
+
+def test_sweep_cell_ragged(pda, oracle_mod):
+    cfg = synth.sweep_cell(16, 8192, seed=3)
+    sampled_check(pda, oracle_mod, cfg, list(range(0, 16, 5)))
