@@ -125,11 +125,18 @@ def make_inputs(cfg: Config, seed: int = 0, device="cpu", poison: bool = True,
     gdev = torch.Generator(device=device).manual_seed(seed + 1) if device.type == "cuda" else gcpu
 
     def draw(shape):
-        if values == "normal":
-            x = torch.randn(shape, generator=gdev, device=device, dtype=torch.float32)
-        else:
-            x = torch.rand(shape, generator=gdev, device=device, dtype=torch.float32).mul_(2).sub_(1)
-        return x.to(dt)
+        # drawn in fp32 chunks (bounded temporaries for multi-GB caches), rounded to dtype
+        out = torch.empty(shape, dtype=dt, device=device)
+        flat = out.view(-1)
+        chunk = 1 << 28
+        for s in range(0, flat.numel(), chunk):
+            n = min(chunk, flat.numel() - s)
+            if values == "normal":
+                x = torch.randn(n, generator=gdev, device=device, dtype=torch.float32)
+            else:
+                x = torch.rand(n, generator=gdev, device=device, dtype=torch.float32).mul_(2).sub_(1)
+            flat[s:s + n] = x
+        return out
 
     q = draw((B, Hq, D))
     k = draw((nb, Hkv, bs, D))

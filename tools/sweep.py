@@ -1,0 +1,112 @@
+"""Prefetch ablation sweep (BASELINE configs[2]/[3]): batch x context x kernel x
+ring depth x prefetch mode/distance, on one B200.
+
+    python tools/sweep.py --out gpurun_out/sweep.jsonl [--quick]
+
+Every variant of a cell runs on the same inputs; variants are interleaved in
+rounds (ABAB...) and each timed iteration is preceded by an L2 flush (a
+512 MiB memset, untimed) so small cells do not run out of L2.  Times are
+CUDA-event medians per iteration.  One JSON line per (cell, variant).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def variants(quick):
+    vs = []
+    stages = [4, 8] if quick else [4, 8, 12]
+    dists = [2, 8] if quick else [1, 2, 4, 8, 16, 32]
+    for s in stages:
+        vs.append(dict(kernel="splitk", smem_stages=s, prefetch="off"))
+        for d in dists:
+            vs.append(dict(kernel="splitk", smem_stages=s, prefetch="bulk", prefetch_distance=d))
+        vs.append(dict(kernel="splitk", smem_stages=s, prefetch="line", prefetch_distance=4))
+    vs.append(dict(kernel="paper", prefetch="off"))
+    for d in ([4] if quick else [1, 2, 4, 8, 16]):
+        vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=d))
+    vs.append(dict(kernel="paper", prefetch="line", prefetch_distance=4))
+    return vs
+
+
+def cells(quick):
+    import synth
+    out = [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B]
+    bs = [1, 16, 64, 256] if quick else [1, 4, 16, 64, 256]
+    cs = [512, 4096, 32768]
+    for b in bs:
+        for c in cs:
+            out.append(synth.sweep_cell(b, c, seed=b * 7 + c))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--reps", type=int, default=7)
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--cells", default="", help="comma list of cell names to keep")
+    a = ap.parse_args()
+
+    import torch
+
+    import paper_2504_06319_b200 as pda
+    import synth
+    pda.lib()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    keep = set(filter(None, a.cells.split(",")))
+    f = open(a.out, "a")
+    for cfg in cells(a.quick):
+        if keep and cfg.name not in keep:
+            continue
+        inp = synth.make_inputs(cfg, seed=5, device="cuda")
+        kvb = cfg.kv_bytes()
+        total = kvb + cfg.other_bytes()
+        vs = variants(a.quick)
+        times = {i: [] for i in range(len(vs))}
+        outs = {}
+        ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        for rnd in range(a.rounds):
+            for i, v in enumerate(vs):
+                def run():
+                    return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"],
+                                                      inp["block_tables"], inp["context_lens"],
+                                                      inp["scale"], workspace=ws, **v)
+                if rnd == 0:
+                    o = run()
+                    outs[i] = o
+                for _ in range(a.reps):
+                    flush.zero_()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    run()
+                    e1.record()
+                    e1.synchronize()
+                    times[i].append(e0.elapsed_time(e1) * 1e3)
+        # bitwise invariance of prefetch within each kernel/stages family
+        for i, v in enumerate(vs):
+            base = next(j for j, w in enumerate(vs) if w["kernel"] == v["kernel"]
+                        and w.get("smem_stages") == v.get("smem_stages") and w["prefetch"] == "off")
+            us = statistics.median(times[i])
+            rec = dict(cell=cfg.name, batch=cfg.num_seqs, ctx=max(cfg.context_lens),
+                       q_heads=cfg.num_q_heads, kv_heads=cfg.num_kv_heads, dtype=cfg.dtype,
+                       kv_bytes=kvb, **v, us_median=us, us_p10=sorted(times[i])[len(times[i]) // 10],
+                       us_p90=sorted(times[i])[(9 * len(times[i])) // 10], gbs=total / (us * 1e-6) / 1e9,
+                       speedup_vs_off=statistics.median(times[base]) / us,
+                       bitwise_equal_to_off=bool(torch.equal(outs[i], outs[base])))
+            f.write(json.dumps(rec) + "\n")
+            f.flush()
+            print(json.dumps(rec), flush=True)
+        del inp, ws, outs
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
