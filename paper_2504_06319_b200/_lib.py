@@ -20,7 +20,10 @@ PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
 KERNEL = {"auto": 0, "paper": 1, "splitk": 2}
 
-DEFAULT_PREFETCH = "bulk"
+# Product default from the round-1 sweep: line-granular L2 prefetch
+# (prefetch.global.L2) 4 blocks ahead; neutral-to-positive for the TMA kernel, while
+# the bulk form (UBLKPF) competes with the TMA loads for the same unit.
+DEFAULT_PREFETCH = "line"
 DEFAULT_DISTANCE = 4
 
 
