@@ -58,6 +58,8 @@ def lib():
             L.oracle_plan_splitk.restype = i32
             L.oracle_plan_paper.argtypes = [p, p, i32, i32, i32, i32, i32, i32, p]
             L.oracle_plan_paper.restype = i32
+            L.oracle_plan_stream.argtypes = [p, p, i32, i32, i32, i32, i32, i32, p]
+            L.oracle_plan_stream.restype = i32
             L.oracle_eq1_block_bytes.argtypes = [i64, i64, i64]
             L.oracle_eq1_block_bytes.restype = i64
             L.oracle_eq2_total_bytes.argtypes = [i64, i64, i64, i64]
@@ -154,6 +156,19 @@ def plan_paper(block_tables, context_lens, num_q_heads: int, block_size: int, wa
                                  warps, prefetch_distance, _ptr(recs))
     if rc != 0:
         raise ValueError("oracle_plan_paper: invalid arguments")
+    return recs
+
+
+def plan_stream(block_tables, context_lens, num_kv_heads: int, block_size: int, num_streams: int,
+                prefetch_distance: int) -> np.ndarray:
+    """Per-row records [B, Hkv, 4 + 2 * max_blocks] of the balanced stream partition."""
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    B, max_blocks = bt.shape
+    recs = np.empty((B, num_kv_heads, 4 + 2 * max_blocks), dtype=np.int32)
+    rc = lib().oracle_plan_stream(_ptr(bt), _ptr(lens), B, num_kv_heads, block_size, max_blocks,
+                                  num_streams, prefetch_distance, _ptr(recs))
+    if rc != 0:
+        raise ValueError("oracle_plan_stream: invalid arguments")
     return recs
 
 

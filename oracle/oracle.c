@@ -259,6 +259,54 @@ int oracle_plan_paper(const int32_t* bt, const int32_t* lens, int B, int Hq, int
     return 0;
 }
 
+/* Stream-kernel plan: all blocks of the step in one ordered item list (rows
+ * (b, kvh) in order, each row's blocks j = 0..n_b-1), T items split into
+ * NS = min(NS_max, T) contiguous ranges [floor(s*T/NS), floor((s+1)*T/NS)).
+ * A segment is the part of a row inside one range; block j of a segment is
+ * prefetched-for (target j + d) iff j + d is inside the same segment (the
+ * Alg. 1 guard against the unit's end, reading R9).  Records per row
+ * r = b * Hkv + kvh, R = max_blocks: visited[j] and target[j] indexed by j.
+ * Rows with L = 0 have no blocks and stay all -1. */
+int oracle_plan_stream(const int32_t* bt, const int32_t* lens, int B, int Hkv, int bs,
+                       int max_blocks, int NS_max, int d, int32_t* recs) {
+    int R = max_blocks;
+    int rec_len = 4 + 2 * R;
+    long long T = 0;
+    for (int b = 0; b < B; ++b) {
+        int L = lens[b] < max_blocks * bs ? lens[b] : max_blocks * bs;
+        if (L > 0) T += (long long)((L + bs - 1) / bs) * Hkv;
+    }
+    long long NS = T < NS_max ? T : NS_max;
+    long long item = 0;
+    long long sigma = 0;
+    for (int b = 0; b < B; ++b) {
+        int L = lens[b] < max_blocks * bs ? lens[b] : max_blocks * bs;
+        int n = L > 0 ? (L + bs - 1) / bs : 0;
+        for (int kvh = 0; kvh < Hkv; ++kvh) {
+            int32_t* rec = recs + ((size_t)b * Hkv + kvh) * rec_len;
+            for (int i = 0; i < rec_len; ++i) rec[i] = -1;
+            if (n == 0) continue;
+            rec[0] = 0;
+            rec[1] = L;
+            rec[2] = n;
+            int np = 0;
+            long long row_start = item;
+            for (int j = 0; j < n; ++j, ++item) {
+                while ((sigma + 1) * T / NS <= item) ++sigma; /* range holding this item */
+                long long range_end = (sigma + 1) * T / NS;
+                long long seg_end = row_start + n < range_end ? row_start + n : range_end;
+                rec[4 + j] = bt[(size_t)b * max_blocks + j];
+                if (d > 0 && item + d < seg_end) {
+                    rec[4 + R + j] = bt[(size_t)b * max_blocks + j + d];
+                    ++np;
+                }
+            }
+            rec[3] = np;
+        }
+    }
+    return 0;
+}
+
 /* Eq. 1: M_block = b * d_h * T_block bytes. */
 int64_t oracle_eq1_block_bytes(int64_t b, int64_t d_h, int64_t T_block) { return b * d_h * T_block; }
 

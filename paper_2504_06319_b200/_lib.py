@@ -18,7 +18,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
 PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
-KERNEL = {"auto": 0, "paper": 1, "splitk": 2}
+KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3}
 
 # Product default from the round-1 sweep: line-granular L2 prefetch
 # (prefetch.global.L2) 4 blocks ahead; neutral-to-positive for the TMA kernel, while
@@ -41,7 +41,8 @@ class Shape(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
-        "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms")]
+        "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms",
+        "stream_warps", "reserved")]
 
 
 class PlanInfo(ctypes.Structure):
@@ -126,13 +127,13 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
 
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
-                 smem_stages=0, kernel="auto", num_sms=0) -> Options:
+                 smem_stages=0, kernel="auto", num_sms=0, stream_warps=0) -> Options:
     mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
     if prefetch_distance is None:
         prefetch_distance = DEFAULT_DISTANCE if mode else 0
     kern = KERNEL[kernel] if not isinstance(kernel, int) else kernel
     return Options(mode, int(prefetch_distance), int(partition_tokens), int(smem_stages), kern,
-                   int(num_sms))
+                   int(num_sms), int(stream_warps), 0)
 
 
 def plan(shape: Shape, opts: Options) -> dict:
@@ -166,8 +167,8 @@ def _stream_handle(stream):
 
 def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scale=None, out=None, *,
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
-                           partition_tokens=0, smem_stages=0, kernel="auto", workspace=None,
-                           stream=None, trace=False):
+                           partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
+                           num_sms=0, workspace=None, stream=None, trace=False):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16),
@@ -181,7 +182,8 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     if out is not None:
         out_dtype = out.dtype
     shape = make_shape(q, k_cache, block_tables, out_dtype)
-    opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel)
+    opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel,
+                        num_sms=num_sms, stream_warps=stream_warps)
     if scale is None:
         scale = q.shape[-1] ** -0.5
     info = plan(shape, opts)
@@ -190,7 +192,8 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     _require_cuda(out)
     wsb = info["workspace_bytes"]
     if wsb and (workspace is None or workspace.numel() * workspace.element_size() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=q.device)
+        # zero-filled: the stream kernel's arrival tickets must start at 0 (include/pda.h)
+        workspace = torch.zeros(wsb, dtype=torch.uint8, device=q.device)
     ws_ptr = workspace.data_ptr() if (workspace is not None and wsb) else None
     s = _stream_handle(stream)
     L = lib()
@@ -232,7 +235,7 @@ class HostDecodeStep:
         self.shape = make_shape(self.q_dev, k_cache, self.bt_dev, self.out_dtype)
         self.opts = make_options(**opt_kw)
         wsb = workspace_bytes(self.shape, self.opts)
-        self.ws = torch.empty(max(1, wsb), dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)
         self.wsb = wsb
 
     def h2d_bytes(self):

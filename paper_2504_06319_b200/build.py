@@ -22,8 +22,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpda.so")
 
-SOURCES = ["pda.cu", "decode_splitk.cu", "decode_paper.cu", "roofline.cu"]
-HEADERS = ["ptx.cuh", "kernels.cuh"]
+SOURCES = ["pda.cu", "decode_splitk.cu", "decode_stream.cu", "decode_paper.cu", "roofline.cu"]
+HEADERS = ["ptx.cuh", "kernels.cuh", "block_math.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

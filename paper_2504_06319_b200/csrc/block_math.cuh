@@ -1,0 +1,186 @@
+// block_math.cuh -- per-16-token-block attention math on mma.sync, shared by
+// the split-K and stream kernels.  One warp, one block of K and V resident in
+// shared memory (TMA-written, SWIZZLE_128B, D/64 chunks of [16 rows][128 B]).
+//
+//   S4  S^T[t][h] = sum_d K[t][d] Q[h][d]        (tokens = MMA M, heads = N)
+//   S5  online softmax per head column, tokens >= valid masked (select)
+//   S6  O^T[d][h] += sum_t V^T[d][t] P[t][h]     (P transposed with movmatrix)
+#pragma once
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace pda {
+
+constexpr uint32_t kFullMask = 0xffffffffu;
+
+// Byte offset of the 16-byte unit holding column `col` of token row `t`
+// inside a slab written by TMA with SWIZZLE_128B: unit u of row t sits at
+// unit u ^ (t % 8) of its 128-byte row.
+__device__ __forceinline__ uint32_t swz(int t, int col) {
+    const int ch = col >> 6;
+    const int u = (col & 63) >> 3;
+    return ch * 2048 + t * 128 + ((u ^ (t & 7)) << 4);
+}
+
+__device__ __forceinline__ void store_out(void* out, size_t idx, float x, int out_dtype) {
+    if (out_dtype == 2) {
+        static_cast<float*>(out)[idx] = x;
+    } else if (out_dtype == 1) {
+        static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(x);
+    } else {
+        static_cast<__half*>(out)[idx] = __float2half_rn(x);
+    }
+}
+
+template <bool BF16, int D, int NT>
+struct BlockMath {
+    static constexpr int KSTEPS = D / 16;
+    static constexpr int MT = D / 16;
+    static constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1
+
+    uint32_t qf[KSTEPS][NT][2];  // Q as the B operand of S^T = K Q^T (register-resident)
+    float acc[MT][NT][4];        // O^T accumulators: (d = 16i + lane/4 + 8(r/2), h = 2(lane%4) + r%2)
+    float m_run[NT][2];          // running max per head column (log2 domain)
+    float l_run[NT][2];          // per-lane partial row sums (reduced at the end)
+
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[i][nt][r] = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            m_run[nt][0] = m_run[nt][1] = -INFINITY;
+            l_run[nt][0] = l_run[nt][1] = 0.f;
+        }
+    }
+
+    // q rows of the g heads of kv head `kvh` of sequence b; heads >= g are zero.
+    __device__ __forceinline__ void load_q(const uint16_t* q, size_t first_row, int g, int lane) {
+        const int h = lane >> 2;
+        const int dq = 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int hh = nt * 8 + h;
+            const uint32_t* qrow = reinterpret_cast<const uint32_t*>(q + (first_row + hh) * D);
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                qf[kk][nt][0] = hh < g ? __ldg(qrow + ((kk * 16 + dq) >> 1)) : 0u;
+                qf[kk][nt][1] = hh < g ? __ldg(qrow + ((kk * 16 + dq + 8) >> 1)) : 0u;
+            }
+        }
+    }
+
+    // One block: K slab at kbase, V slab at vbase (shared addresses); `valid`
+    // tokens (1..16) are inside the context, the rest are masked.
+    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
+                                          int lane) {
+        const int k_t = (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int k_c = (lane >> 4) * 8;
+        const int v_t = (lane & 7) + (lane >> 4) * 8;
+        const int v_c = ((lane >> 3) & 1) * 8;
+        const int r0 = lane >> 2;
+        const int t0 = 2 * (lane & 3);
+
+        // ---- S4 (two independent accumulator chains)
+        float s[NT][4], s2[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            uint32_t a[4];
+            ldsm_x4(kbase + swz(k_t, kk * 16 + k_c), a[0], a[1], a[2], a[3]);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                if (kk & 1)
+                    mma_16816<BF16>(s2[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
+                else
+                    mma_16816<BF16>(s[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
+            }
+        }
+
+        // ---- S5
+        uint32_t pb[NT][2], pb_lo[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[nt][r] = (s[nt][r] + s2[nt][r]) * scale_log2;
+            if (valid < kBlockSize) {
+                if (r0 >= valid) s[nt][0] = s[nt][1] = -INFINITY;
+                if (r0 + 8 >= valid) s[nt][2] = s[nt][3] = -INFINITY;
+            }
+            float pr[4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float mx = fmaxf(s[nt][c], s[nt][c + 2]);
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 4));
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 8));
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 16));
+                const float m_new = fmaxf(m_run[nt][c], mx);
+                const float alpha = ex2(m_run[nt][c] - m_new);
+                m_run[nt][c] = m_new;
+                pr[c] = ex2(s[nt][c] - m_new);
+                pr[c + 2] = ex2(s[nt][c + 2] - m_new);
+                l_run[nt][c] = l_run[nt][c] * alpha + pr[c] + pr[c + 2];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    acc[i][nt][c] *= alpha;
+                    acc[i][nt][c + 2] *= alpha;
+                }
+            }
+            const uint32_t w0 = pack2<BF16>(pr[0], pr[1]);
+            const uint32_t w1 = pack2<BF16>(pr[2], pr[3]);
+            pb[nt][0] = movmatrix_trans(w0);
+            pb[nt][1] = movmatrix_trans(w1);
+            if constexpr (BF16) {
+                // bf16 P keeps 8 mantissa bits: carry the residual as a second
+                // bf16 term so P enters PV with ~16 bits (R19).
+                const float2 h0 = unpack2<true>(w0), h1 = unpack2<true>(w1);
+                pb_lo[nt][0] = movmatrix_trans(pack2<true>(pr[0] - h0.x, pr[1] - h0.y));
+                pb_lo[nt][1] = movmatrix_trans(pack2<true>(pr[2] - h1.x, pr[3] - h1.y));
+            }
+        }
+
+        // ---- S6
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            uint32_t a[4];
+            ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
+            if (valid < kBlockSize) {  // zero V rows t >= L (0 * NaN would poison)
+                const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+                const uint32_t m1 =
+                    (t0 + 8 < valid ? 0xffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
+                a[0] &= m0;
+                a[1] &= m0;
+                a[2] &= m1;
+                a[3] &= m1;
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                mma_16816<BF16>(acc[i][nt], a, pb[nt][0], pb[nt][1]);
+                if constexpr (BF16) mma_16816<BF16>(acc[i][nt], a, pb_lo[nt][0], pb_lo[nt][1]);
+            }
+        }
+    }
+
+    // Reduce the per-lane partial row sums across the 8 lanes of each column.
+    __device__ __forceinline__ void reduce_l() {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float l = l_run[nt][c];
+                l += __shfl_xor_sync(kFullMask, l, 4);
+                l += __shfl_xor_sync(kFullMask, l, 8);
+                l += __shfl_xor_sync(kFullMask, l, 16);
+                l_run[nt][c] = l;
+            }
+    }
+};
+
+}  // namespace pda

@@ -18,14 +18,13 @@
 //    memory; a sequence with a single partition writes `out` directly,
 //    otherwise the normalised partial and its log2-sum-exp go to the
 //    workspace and combine_kernel (S8) merges partitions in fixed order.
-#include "kernels.cuh"
-#include "ptx.cuh"
+#include "block_math.cuh"
 
 namespace pda {
 
 namespace {
 
-constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kFull = kFullMask;
 
 template <int D>
 struct Geometry {
@@ -34,32 +33,12 @@ struct Geometry {
     static constexpr int kChunks = D / 64;            // 128-byte column chunks (TMA boxes)
 };
 
-// Byte offset of the 16-byte unit holding column `col` of token row `t`
-// inside a slab written by TMA with SWIZZLE_128B: the slab is D/64 column
-// chunks of [16 rows][128 B]; unit u of row t sits at unit u ^ (t % 8).
-__device__ __forceinline__ uint32_t swz(int t, int col) {
-    const int ch = col >> 6;
-    const int u = (col & 63) >> 3;
-    return ch * 2048 + t * 128 + ((u ^ (t & 7)) << 4);
-}
-
-__device__ __forceinline__ void store_out(void* out, size_t idx, float x, int out_dtype) {
-    if (out_dtype == 2) {
-        static_cast<float*>(out)[idx] = x;
-    } else if (out_dtype == 1) {
-        static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(x);
-    } else {
-        static_cast<__half*>(out)[idx] = __float2half_rn(x);
-    }
-}
-
 template <bool BF16, int D, int NT, int STAGES, bool TRACE>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
     using G = Geometry<D>;
     constexpr int NH = 8 * NT;  // padded heads per CTA
-    constexpr int KSTEPS = D / 16;
     constexpr int MT = D / 16;  // m-tiles of O^T
 
     extern __shared__ uint8_t smem_raw[];
@@ -192,151 +171,23 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     }
 
     // ============================== consumer warps ==============================
-    // Q as the B operand of S^T = K Q^T: B[k = d][n = h], register-resident.
-    uint32_t qf[KSTEPS][NT][2];
-    {
-        const int h = lane >> 2;
-        const int dq = 2 * (lane & 3);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const int hh = nt * 8 + h;
-            const uint32_t* qrow =
-                reinterpret_cast<const uint32_t*>(p.q + ((size_t)b * p.Hq + kvh * g + hh) * D);
-#pragma unroll
-            for (int kk = 0; kk < KSTEPS; ++kk) {
-                qf[kk][nt][0] = hh < g ? qrow[(kk * 16 + dq) >> 1] : 0u;
-                qf[kk][nt][1] = hh < g ? qrow[(kk * 16 + dq + 8) >> 1] : 0u;
-            }
-        }
-    }
-
-    float acc[MT][NT][4];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[i][nt][r] = 0.f;
-    float m_run[NT][2], l_run[NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        m_run[nt][0] = m_run[nt][1] = -INFINITY;
-        l_run[nt][0] = l_run[nt][1] = 0.f;
-    }
-
-    // per-lane ldmatrix row/col selectors
-    const int k_t = (lane & 7) + ((lane >> 3) & 1) * 8;  // K rows (tokens) for A = K
-    const int k_c = (lane >> 4) * 8;
-    const int v_t = (lane & 7) + (lane >> 4) * 8;  // V rows (tokens) for A = V^T (trans)
-    const int v_c = ((lane >> 3) & 1) * 8;
-    const int r0 = lane >> 2;        // S^T accumulator rows (tokens) r0 and r0 + 8
-    const int t0 = 2 * (lane & 3);   // V^T fragment token columns t0, t0+1 (+8)
-
+    BlockMath<BF16, D, NT> bm;
+    bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
+    bm.reset();
     for (int j = warp; j < n; j += kConsumerWarps) {
         const int stage = j % STAGES;
         const uint32_t round = j / STAGES;
         mbar_wait(&full[stage], round & 1);
         const uint32_t kbase = smem_u32(ring + stage * G::kStage);
-        const uint32_t vbase = kbase + G::kSlab;
         const int valid = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
-
-        // ---- S4: S^T[t][h] = sum_d K[t][d] Q[h][d]  (two accumulator chains)
-        float s[NT][4], s2[NT][4];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < KSTEPS; ++kk) {
-            uint32_t a[4];
-            ldsm_x4(kbase + swz(k_t, kk * 16 + k_c), a[0], a[1], a[2], a[3]);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                if (kk & 1)
-                    mma_16816<BF16>(s2[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
-                else
-                    mma_16816<BF16>(s[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
-            }
-        }
-
-        // ---- S5: scale (fp32), mask t >= L, online softmax per head column
-        uint32_t pb[NT][2];      // P as PV B fragments (hi part for bf16)
-        uint32_t pb_lo[NT][2];   // bf16 residual part
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) s[nt][r] = (s[nt][r] + s2[nt][r]) * p.scale_log2;
-            if (valid < kBlockSize) {
-                if (r0 >= valid) s[nt][0] = s[nt][1] = -INFINITY;
-                if (r0 + 8 >= valid) s[nt][2] = s[nt][3] = -INFINITY;
-            }
-            float pr[4];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                float mx = fmaxf(s[nt][c], s[nt][c + 2]);
-                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
-                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
-                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
-                const float m_new = fmaxf(m_run[nt][c], mx);
-                const float alpha = ex2(m_run[nt][c] - m_new);
-                m_run[nt][c] = m_new;
-                pr[c] = ex2(s[nt][c] - m_new);
-                pr[c + 2] = ex2(s[nt][c + 2] - m_new);
-                l_run[nt][c] = l_run[nt][c] * alpha + pr[c] + pr[c + 2];
-#pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                    acc[i][nt][c] *= alpha;
-                    acc[i][nt][c + 2] *= alpha;
-                }
-            }
-            // [t][h] 8x8 fragments -> transpose -> B[k = t][n = h]
-            const uint32_t w0 = pack2<BF16>(pr[0], pr[1]);
-            const uint32_t w1 = pack2<BF16>(pr[2], pr[3]);
-            pb[nt][0] = movmatrix_trans(w0);
-            pb[nt][1] = movmatrix_trans(w1);
-            if constexpr (BF16) {
-                // bf16 P keeps only 8 mantissa bits: carry the residual in a
-                // second bf16 term so P enters PV with ~16 bits (R19).
-                const float2 h0 = unpack2<true>(w0), h1 = unpack2<true>(w1);
-                pb_lo[nt][0] = movmatrix_trans(pack2<true>(pr[0] - h0.x, pr[1] - h0.y));
-                pb_lo[nt][1] = movmatrix_trans(pack2<true>(pr[2] - h1.x, pr[3] - h1.y));
-            }
-        }
-
-        // ---- S6: O^T[d][h] += sum_t V^T[d][t] P[t][h]
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            uint32_t a[4];
-            ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
-            if (valid < kBlockSize) {  // zero V rows t >= L (0 * NaN would poison)
-                const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
-                const uint32_t m1 =
-                    (t0 + 8 < valid ? 0xffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
-                a[0] &= m0;
-                a[1] &= m0;
-                a[2] &= m1;
-                a[3] &= m1;
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                mma_16816<BF16>(acc[i][nt], a, pb[nt][0], pb[nt][1]);
-                if constexpr (BF16) mma_16816<BF16>(acc[i][nt], a, pb_lo[nt][0], pb_lo[nt][1]);
-            }
-        }
+        bm.block(kbase, kbase + G::kSlab, valid, p.scale_log2, lane);
         mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
     }
 
     // ---- S7: merge the consumer warps of this unit
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            float l = l_run[nt][c];
-            l += __shfl_xor_sync(kFull, l, 4);
-            l += __shfl_xor_sync(kFull, l, 8);
-            l += __shfl_xor_sync(kFull, l, 16);
-            l_run[nt][c] = l;
-        }
+    bm.reduce_l();
+    const int r0 = lane >> 2;
+    const int t0 = 2 * (lane & 3);
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring reads done
     if (lane < 4) {
 #pragma unroll
@@ -344,8 +195,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int h = nt * 8 + 2 * lane + c;
-                merge_m[warp * NH + h] = m_run[nt][c];
-                merge_l[warp * NH + h] = l_run[nt][c];
+                merge_m[warp * NH + h] = bm.m_run[nt][c];
+                merge_l[warp * NH + h] = bm.l_run[nt][c];
             }
     }
 #pragma unroll
@@ -356,7 +207,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             for (int r = 0; r < 4; ++r) {
                 const int dd = i * 16 + r0 + 8 * (r >> 1);
                 const int h = nt * 8 + t0 + (r & 1);
-                merge_acc[(warp * NH + h) * (D + 4) + dd] = acc[i][nt][r];
+                merge_acc[(warp * NH + h) * (D + 4) + dd] = bm.acc[i][nt][r];
             }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 

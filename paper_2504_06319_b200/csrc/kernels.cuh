@@ -46,6 +46,25 @@ struct PaperParams {
     float scale_log2;
 };
 
+struct StreamParams {
+    const uint16_t* q;
+    const uint16_t* k;
+    const uint16_t* v;
+    const int32_t* bt;
+    const int32_t* lens;
+    void* out;
+    float* ws_o;        // [NS][2][NH][D]  partial outputs of a stream's first/last segment
+    float* ws_lse;      // [NS][2][NH]
+    uint32_t* tickets;  // [B * Hkv] self-resetting arrival counters (zero before first use)
+    int32_t* trace;
+    int B, Hq, Hkv, g, max_blocks;
+    int out_dtype;
+    int pf_mode, pf_dist;
+    int trace_rec_len;
+    int NS;  // streams launched (grid * warps per CTA)
+    float scale_log2;
+};
+
 struct CombineParams {
     const float* ws_o;
     const float* ws_lse;
@@ -61,6 +80,12 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
                           dim3 grid, cudaStream_t stream);
 size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages);
 int splitk_threads();
+
+cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,
+                          bool bf16, int head_dim, int n_tiles, int stages, int warps, bool trace,
+                          int grid, cudaStream_t stream);
+size_t stream_smem_bytes(int head_dim, int stages, int warps);
+bool stream_config_supported(int stages, int warps);
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
 

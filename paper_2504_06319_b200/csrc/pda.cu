@@ -12,6 +12,10 @@
 namespace {
 
 constexpr int kDefaultStages = 8;
+constexpr int kDefaultStreamStages = 6;
+constexpr int kDefaultStreamWarps = 2;
+constexpr size_t kSmemPerSm = 233472;  // 228 KB per SM on B200
+constexpr size_t kSmemReservedPerCta = 1024;
 constexpr int kDefaultSms = 148;  // B200
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -37,10 +41,17 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     if (o->prefetch != PDA_PF_OFF && (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
         return PDA_ERR_SHAPE;
     if (o->partition_tokens < 0 || o->partition_tokens % s->block_size != 0) return PDA_ERR_SHAPE;
-    if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 && o->smem_stages != 12)
+    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_STREAM) return PDA_ERR_SHAPE;
+    if (o->num_sms < 0 || o->stream_warps < 0 || o->reserved != 0) return PDA_ERR_SHAPE;
+    if (o->kernel == PDA_KERNEL_STREAM) {
+        const int st = o->smem_stages ? o->smem_stages : kDefaultStreamStages;
+        const int w = o->stream_warps ? o->stream_warps : kDefaultStreamWarps;
+        if (!pda::stream_config_supported(st, w)) return PDA_ERR_UNSUPPORTED;
+        if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
+    } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&
+               o->smem_stages != 12) {
         return PDA_ERR_UNSUPPORTED;
-    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_SPLITK) return PDA_ERR_SHAPE;
-    if (o->num_sms < 0) return PDA_ERR_SHAPE;
+    }
     return PDA_OK;
 }
 
@@ -64,6 +75,32 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         pl->trace_rec_len = 4 + 2 * R;
         pl->trace_records = B * Hq * pda::kPaperWarps;
         pl->workspace_bytes = 0;
+        return PDA_OK;
+    }
+    if (o->kernel == PDA_KERNEL_STREAM) {
+        // Persistent grid: as many CTAs as fit on the chip at once; NS streams
+        // share all KV blocks of the step equally (S0 happens on the device).
+        const int st = o->smem_stages ? o->smem_stages : kDefaultStreamStages;
+        const int w = o->stream_warps ? o->stream_warps : kDefaultStreamWarps;
+        const int sms = o->num_sms ? o->num_sms : kDefaultSms;
+        const size_t smem = pda::stream_smem_bytes(D, st, w);
+        int per_sm = (int)(kSmemPerSm / (smem + kSmemReservedPerCta));
+        per_sm = per_sm < 2048 / (w * 32) ? per_sm : 2048 / (w * 32);
+        per_sm = per_sm < 32 ? per_sm : 32;
+        const int nh = (Hq / Hkv) <= 8 ? 8 : 16;
+        pl->kernel = PDA_KERNEL_STREAM;
+        pl->partition_tokens = (int32_t)max_tokens;
+        pl->p_max = 1;
+        pl->smem_stages = st;
+        pl->grid_x = sms * per_sm;
+        pl->grid_y = 1;
+        pl->grid_z = 1;
+        pl->threads = w * 32;
+        pl->trace_rec_len = 4 + 2 * s->max_blocks_per_seq;
+        pl->trace_records = B * Hkv;
+        const size_t ns = (size_t)pl->grid_x * w;
+        pl->workspace_bytes = align256(ns * 2 * nh * D * 4) + align256(ns * 2 * nh * 4) +
+                              align256((size_t)B * Hkv * 4);
         return PDA_OK;
     }
     // S0: split-K plan.  Units (partition, kv head, seq) are independent; pick
@@ -193,6 +230,38 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     CUtensorMap tmK, tmV;
     if (!encode_cache_map(&tmK, k_cache, s) || !encode_cache_map(&tmV, v_cache, s))
         return PDA_ERR_CUDA;
+    if (pl.kernel == PDA_KERNEL_STREAM) {
+        const int w = pl.threads / 32;
+        const size_t ns = (size_t)pl.grid_x * w;
+        const int nh = (s->num_q_heads / s->num_kv_heads) <= 8 ? 8 : 16;
+        pda::StreamParams sp{};
+        sp.q = static_cast<const uint16_t*>(q);
+        sp.k = static_cast<const uint16_t*>(k_cache);
+        sp.v = static_cast<const uint16_t*>(v_cache);
+        sp.bt = bt;
+        sp.lens = lens;
+        sp.out = out;
+        char* wsc = static_cast<char*>(ws);
+        sp.ws_o = reinterpret_cast<float*>(wsc);
+        sp.ws_lse = reinterpret_cast<float*>(wsc + align256(ns * 2 * nh * s->head_dim * 4));
+        sp.tickets = reinterpret_cast<uint32_t*>(wsc + align256(ns * 2 * nh * s->head_dim * 4) +
+                                                 align256(ns * 2 * nh * 4));
+        sp.trace = trace;
+        sp.B = s->num_seqs;
+        sp.Hq = s->num_q_heads;
+        sp.Hkv = s->num_kv_heads;
+        sp.g = s->num_q_heads / s->num_kv_heads;
+        sp.max_blocks = s->max_blocks_per_seq;
+        sp.out_dtype = s->out_dtype;
+        sp.pf_mode = prefetch_mode;
+        sp.pf_dist = pf_dist;
+        sp.trace_rec_len = pl.trace_rec_len;
+        sp.NS = (int)ns;
+        sp.scale_log2 = scale_log2;
+        err = pda::launch_stream(tmK, tmV, sp, s->dtype == PDA_BF16, s->head_dim, sp.g <= 8 ? 1 : 2,
+                                 pl.smem_stages, w, trace != nullptr, pl.grid_x, stream);
+        return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
+    }
     pda::SplitKParams p{};
     p.q = static_cast<const uint16_t*>(q);
     p.k = static_cast<const uint16_t*>(k_cache);
@@ -336,6 +405,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 1; }
+int32_t pda_abi_version(void) { return 2; }
 
 }  // extern "C"

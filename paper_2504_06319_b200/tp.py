@@ -58,10 +58,10 @@ class TPDecodeAttention:
                                 torch.empty((num_seqs, max_blocks), dtype=torch.int32, device="meta"))
         opt = _lib.make_options(**{k: v for k, v in opts.items()
                                    if k in ("prefetch", "prefetch_distance", "partition_tokens",
-                                            "smem_stages", "kernel")})
+                                            "smem_stages", "kernel", "stream_warps")})
         self.plan = _lib.plan(shape, opt)
         wsb = self.plan["workspace_bytes"]
-        self.ws = torch.empty(max(1, wsb), dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)  # stream tickets start at 0
 
     def launches_per_step(self) -> int:
         return 1 + (1 if self.plan["p_max"] > 1 else 0)

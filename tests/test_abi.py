@@ -48,7 +48,8 @@ def shape(**kw):
 
 
 def opts(**kw):
-    d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0)
+    d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0,
+             stream_warps=0, reserved=0)
     d.update(kw)
     return _lib.Options(**d)
 
@@ -77,6 +78,12 @@ def test_check_args_shape(kw, status):
     (dict(partition_tokens=32), 0),
     (dict(smem_stages=6), 3),
     (dict(kernel=7), 2),
+    (dict(kernel=3), 0),
+    (dict(kernel=3, smem_stages=6, stream_warps=2), 0),
+    (dict(kernel=3, smem_stages=12), 3),
+    (dict(kernel=3, prefetch_distance=33), 3),
+    (dict(kernel=3, prefetch_distance=32), 0),
+    (dict(reserved=1), 2),
 ])
 def test_check_args_options(kw, status):
     assert pda.check_args(shape(), opts(**kw)) == status
@@ -139,10 +146,23 @@ def test_plan_explicit_partition_and_paper():
     assert pp["trace_rec_len"] == 4 + 2 * 4 and pp["trace_records"] == 2 * 4 * 4
 
 
+def test_plan_stream_persistent_grid():
+    # D=128, 6 stages x 2 warps x 8 KiB = 96 KiB (+1 KiB align) -> 2 CTAs per SM on 148 SMs
+    s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
+              max_blocks_per_seq=256)
+    p = pda.plan(s, opts(kernel=3))
+    assert p["kernel"] == 3 and p["grid_x"] == 296 and p["threads"] == 64 and p["smem_stages"] == 6
+    ns, nh, D = 296 * 2, 8, 128
+    assert p["workspace_bytes"] == ns * 2 * nh * D * 4 + ns * 2 * nh * 4 + 64 * 32 * 4
+    assert p["trace_rec_len"] == 4 + 2 * 256 and p["trace_records"] == 64 * 32
+    p1 = pda.plan(s, opts(kernel=3, smem_stages=8, stream_warps=1))
+    assert p1["grid_x"] == 148 * 3 and p1["threads"] == 32
+
+
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 1
+    assert pda.lib().pda_abi_version() == 2
 
 
 def test_product_never_imports_oracle():

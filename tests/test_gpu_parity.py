@@ -62,7 +62,10 @@ SHAPES = [
 ]
 KERNELS = [dict(kernel="splitk"), dict(kernel="splitk", partition_tokens=16),
            dict(kernel="splitk", partition_tokens=64), dict(kernel="splitk", smem_stages=4),
-           dict(kernel="splitk", smem_stages=12, partition_tokens=256), dict(kernel="paper")]
+           dict(kernel="splitk", smem_stages=12, partition_tokens=256), dict(kernel="paper"),
+           dict(kernel="stream"), dict(kernel="stream", smem_stages=8, stream_warps=1),
+           dict(kernel="stream", smem_stages=4, stream_warps=2),
+           dict(kernel="stream", smem_stages=4, stream_warps=4)]
 
 
 @pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: c.name)
@@ -79,18 +82,18 @@ def test_parity_vs_oracle(pda, oracle_mod, cfg, kw):
 
 
 @pytest.mark.parametrize("cfg", SHAPES[:4], ids=lambda c: c.name)
-@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
 def test_prefetch_is_bitwise_invisible(pda, cfg, kernel):
     """Prefetch changes where data is found, not what is computed."""
     dev = to_dev(synth.make_inputs(cfg, seed=3))
     base = gpu(pda, dev, kernel=kernel, prefetch="off")
     for mode in ("bulk", "line"):
-        for d in (1, 2, 4, 7, 64):
+        for d in (1, 2, 4, 7, 32 if kernel == "stream" else 64):
             o = gpu(pda, dev, kernel=kernel, prefetch=mode, prefetch_distance=d)
             assert torch.equal(o, base), (mode, d)
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
 def test_placement_invariance_bitwise(pda, kernel):
     inp = synth.make_inputs(SHAPES[2], seed=5)
     a = gpu(pda, to_dev(inp), kernel=kernel)
@@ -98,7 +101,7 @@ def test_placement_invariance_bitwise(pda, kernel):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
 def test_run_to_run_bitwise(pda, kernel):
     dev = to_dev(synth.make_inputs(SHAPES[3], seed=8))
     a = gpu(pda, dev, kernel=kernel, partition_tokens=0 if kernel == "paper" else 128)
@@ -108,7 +111,7 @@ def test_run_to_run_bitwise(pda, kernel):
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
-@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
 def test_context_len_one_returns_v_row_exactly(pda, dtype, kernel):
     cfg = synth.Config("l1", 3, 8, 2, 128, (1, 1, 1), dtype, poison_blocks=4)
     inp = synth.make_inputs(cfg, seed=2)
@@ -120,7 +123,7 @@ def test_context_len_one_returns_v_row_exactly(pda, dtype, kernel):
             assert torch.equal(out[b, h].cpu(), inp["v_cache"][blk, h // 4, 0])
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
 def test_needle_every_position(pda, kernel):
     cfg = synth.Config("needle", 1, 2, 1, 64, (37,), "fp16", poison_blocks=2)
     base = synth.make_inputs(cfg, seed=9)
@@ -133,7 +136,7 @@ def test_needle_every_position(pda, kernel):
             inp["k_cache"][int(bt[t // 16]), 0, t % 16, 0] = 40.0 if t == t_star else 0.0
         inp["scale"] = 1.0
         out = gpu(pda, to_dev(inp), kernel=kernel, out_dtype=torch.float32, partition_tokens=0
-                  if kernel == "paper" else 16)
+                  if kernel != "splitk" else 16)
         v = inp["v_cache"][int(bt[t_star // 16]), 0, t_star % 16].float()
         assert torch.allclose(out[0, 0].cpu(), v, atol=1e-5, rtol=0), t_star
 
@@ -184,6 +187,36 @@ def test_trace_paper_matches_alg1(pda, oracle_mod):
             assert (got[1, :, :, 3] == 1).all()
 
 
+def test_trace_stream_matches_oracle_plan(pda, oracle_mod):
+    cfg = synth.Config("trace_s", 4, 8, 2, 128, (37, 700, 0, 260), "bf16", poison_blocks=3)
+    dev = to_dev(synth.make_inputs(cfg, seed=4))
+    for st, w in ((6, 2), (8, 1), (4, 4)):
+        for mode, d in (("off", 0), ("bulk", 1), ("line", 4), ("bulk", 32)):
+            _, tr, info = gpu(pda, dev, kernel="stream", smem_stages=st, stream_warps=w, prefetch=mode,
+                              prefetch_distance=d or None, trace=True)
+            ns = info["grid_x"] * info["threads"] // 32
+            ref = oracle_mod.plan_stream(dev["block_tables"], dev["context_lens"], cfg.num_kv_heads, 16,
+                                         ns, d)
+            got = tr.cpu().numpy().reshape(ref.shape)
+            assert np.array_equal(got, ref), (st, w, mode, d)
+
+
+@pytest.mark.parametrize("ns_cap", [1, 3, 17])
+def test_stream_few_streams_split_rows(pda, oracle_mod, ns_cap):
+    """Force many rows to be split across streams (num_sms small => few streams)
+    so the in-kernel ticket/merge path runs for most rows."""
+    cfg = synth.Config("split_rows", 5, 16, 4, 128, (333, 17, 1, 901, 64), "bf16", poison_blocks=2)
+    inp = synth.make_inputs(cfg, seed=6)
+    ref = oracle_out(oracle_mod, inp)
+    dev = to_dev(inp)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    for rep in range(3):  # tickets must self-reset between calls
+        out = pda.paged_decode_attention(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                         dev["context_lens"], dev["scale"], kernel="stream",
+                                         workspace=ws, out_dtype=torch.float32, num_sms=ns_cap)
+        assert max_err(out, ref) <= 5e-4
+
+
 def test_host_e2e_step_matches_device_path(pda):
     cfg = synth.Config("e2e", 4, 8, 2, 128, (300, 64, 1, 999), "bf16")
     inp = synth.make_inputs(cfg, seed=21)
@@ -203,6 +236,12 @@ def test_nan_poison_never_leaks(pda):
     dev = to_dev(synth.make_inputs(cfg, seed=3))
     for kw in KERNELS:
         assert torch.isfinite(gpu(pda, dev, **kw)).all()
+
+
+@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
+def test_full_size_sampled_stream(pda, oracle_mod, cfg):
+    B = cfg.num_seqs
+    sampled_check(pda, oracle_mod, cfg, [0, B // 3, B - 1], kernel="stream")
 
 
 def test_rejects_cpu_tensors(pda):

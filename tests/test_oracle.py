@@ -296,3 +296,46 @@ def test_plan_splitk_prefetch_off(oracle_mod):
     recs = oracle_mod.plan_splitk(bt, np.array([128], np.int32), 1, 16, 128, 1, 0)
     assert recs[0, 0, 0, 2] == 8 and recs[0, 0, 0, 3] == 0
     assert list(recs[0, 0, 0, 4:12]) == list(range(8))
+
+
+def test_plan_stream_hand_example(oracle_mod):
+    """T = 4 items (row 0: 3 blocks, row 1: 1 block), 2 streams: ranges [0,2), [2,4).
+    Row 0 is split after its second block; with d = 1 only block 0 (item 0 -> 1
+    inside [0,2)) is prefetched-for."""
+    bt = np.array([[10, 11, 12], [20, -1, -1]], dtype=np.int32)
+    lens = np.array([40, 16], dtype=np.int32)
+    r = oracle_mod.plan_stream(bt, lens, 1, 16, 2, 1)
+    R = 3
+    row0, row1 = r[0, 0], r[1, 0]
+    assert list(row0[:4]) == [0, 40, 3, 1]
+    assert list(row0[4:4 + R]) == [10, 11, 12] and list(row0[4 + R:]) == [11, -1, -1]
+    assert list(row1[:4]) == [0, 16, 1, 0] and list(row1[4:4 + R]) == [20, -1, -1]
+    # more streams than items: every item alone, nothing can be prefetched
+    r = oracle_mod.plan_stream(bt, lens, 1, 16, 64, 1)
+    assert r[0, 0, 3] == 0 and r[1, 0, 3] == 0
+    # one stream: a whole row is one segment -> prefetches = n - d per row
+    r = oracle_mod.plan_stream(bt, lens, 1, 16, 1, 1)
+    assert r[0, 0, 3] == 2 and list(r[0, 0, 4 + R:]) == [11, 12, -1]
+
+
+def test_plan_stream_covers_every_block_once(oracle_mod):
+    rng = np.random.default_rng(0)
+    B, Hkv, mb = 5, 3, 9
+    bt = rng.permutation(B * mb).reshape(B, mb).astype(np.int32)
+    lens = np.array([0, 1, 144, 17, 70], dtype=np.int32)
+    for ns in (1, 2, 7, 40, 1000):
+        r = oracle_mod.plan_stream(bt, lens, Hkv, 16, ns, 3)
+        for b in range(B):
+            n = -(-int(lens[b]) // 16)
+            for h in range(Hkv):
+                if n == 0:
+                    assert (r[b, h] == -1).all()
+                    continue
+                assert r[b, h, 2] == n and list(r[b, h, 4:4 + n]) == list(bt[b, :n])
+                assert (r[b, h, 4 + n:4 + mb] == -1).all()
+                # a prefetch target is always the block d ahead in the same row
+                pf = r[b, h, 4 + mb:]
+                for j in range(mb):
+                    if pf[j] != -1:
+                        assert j + 3 < n and pf[j] == bt[b, j + 3]
+                assert r[b, h, 3] == (pf != -1).sum()

@@ -27,6 +27,11 @@ def variants(quick):
         for d in dists:
             vs.append(dict(kernel="splitk", smem_stages=s, prefetch="bulk", prefetch_distance=d))
         vs.append(dict(kernel="splitk", smem_stages=s, prefetch="line", prefetch_distance=4))
+    for st, w in ((6, 2), (8, 1), (4, 2), (4, 4)):
+        vs.append(dict(kernel="stream", smem_stages=st, stream_warps=w, prefetch="off"))
+        vs.append(dict(kernel="stream", smem_stages=st, stream_warps=w, prefetch="line", prefetch_distance=4))
+        if not quick:
+            vs.append(dict(kernel="stream", smem_stages=st, stream_warps=w, prefetch="bulk", prefetch_distance=4))
     vs.append(dict(kernel="paper", prefetch="off"))
     for d in ([4] if quick else [1, 2, 4, 8, 16]):
         vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=d))
@@ -52,6 +57,8 @@ def main():
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--cells", default="", help="comma list of cell names to keep")
+    ap.add_argument("--kernels", default="", help="comma list of kernels to keep")
+    ap.add_argument("--no-graphs", action="store_true", help="time direct calls instead of CUDA-graph replays")
     a = ap.parse_args()
 
     import torch
@@ -69,42 +76,59 @@ def main():
         kvb = cfg.kv_bytes()
         total = kvb + cfg.other_bytes()
         vs = variants(a.quick)
+        if a.kernels:
+            ks = set(a.kernels.split(","))
+            vs = [v for v in vs if v["kernel"] in ks]
         times = {i: [] for i in range(len(vs))}
         outs = {}
-        ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        # separate zeroed workspaces: the stream kernel's arrival tickets must start at 0
+        wss = {"splitk": torch.zeros(1 << 30, dtype=torch.uint8, device="cuda"),
+               "stream": torch.zeros(256 << 20, dtype=torch.uint8, device="cuda"), "paper": None}
+        graphs = {}
         for rnd in range(a.rounds):
             for i, v in enumerate(vs):
-                def run():
+
+                def run(v=v, i=i):
                     return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"],
                                                       inp["block_tables"], inp["context_lens"],
-                                                      inp["scale"], workspace=ws, **v)
+                                                      inp["scale"], out=outs.get(i),
+                                                      workspace=wss[v["kernel"]], **v)
                 if rnd == 0:
-                    o = run()
-                    outs[i] = o
+                    outs[i] = run()
+                    if not a.no_graphs:
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                            run()
+                        graphs[i] = g
                 for _ in range(a.reps):
                     flush.zero_()
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    run()
+                    if a.no_graphs:
+                        run()
+                    else:
+                        graphs[i].replay()
                     e1.record()
                     e1.synchronize()
                     times[i].append(e0.elapsed_time(e1) * 1e3)
         # bitwise invariance of prefetch within each kernel/stages family
         for i, v in enumerate(vs):
             base = next(j for j, w in enumerate(vs) if w["kernel"] == v["kernel"]
-                        and w.get("smem_stages") == v.get("smem_stages") and w["prefetch"] == "off")
+                        and w.get("smem_stages") == v.get("smem_stages")
+                        and w.get("stream_warps") == v.get("stream_warps") and w["prefetch"] == "off")
             us = statistics.median(times[i])
             rec = dict(cell=cfg.name, batch=cfg.num_seqs, ctx=max(cfg.context_lens),
                        q_heads=cfg.num_q_heads, kv_heads=cfg.num_kv_heads, dtype=cfg.dtype,
                        kv_bytes=kvb, **v, us_median=us, us_p10=sorted(times[i])[len(times[i]) // 10],
                        us_p90=sorted(times[i])[(9 * len(times[i])) // 10], gbs=total / (us * 1e-6) / 1e9,
                        speedup_vs_off=statistics.median(times[base]) / us,
-                       bitwise_equal_to_off=bool(torch.equal(outs[i], outs[base])))
+                       bitwise_equal_to_off=bool(torch.equal(outs[i], outs[base])),
+                       timing="cuda_graph_replay" if not a.no_graphs else "direct_call")
             f.write(json.dumps(rec) + "\n")
             f.flush()
             print(json.dumps(rec), flush=True)
-        del inp, ws, outs
+        del inp, wss, outs, graphs
         torch.cuda.empty_cache()
 
 
