@@ -68,14 +68,17 @@ typedef enum {
 } pda_prefetch;
 
 typedef enum {
-    PDA_KERNEL_AUTO = 0,   /* = PDA_KERNEL_SPLITK */
+    PDA_KERNEL_AUTO = 0,   /* = PDA_KERNEL_BALANCED */
     PDA_KERNEL_PAPER = 1,  /* the paper's structure: grid [Hq, B], 4 warps, warp-per-block,
                               K/V loaded to registers (Section 3.1) */
     PDA_KERNEL_SPLITK = 2, /* B200 kernel: split-K over context partitions, TMA ring in
                               shared memory, mma.sync, GQA group per CTA, combine kernel */
-    PDA_KERNEL_STREAM = 3  /* B200 persistent kernel: every warp a self-pipelined stream over an
+    PDA_KERNEL_STREAM = 3, /* B200 persistent kernel: every warp a self-pipelined stream over an
                               equal share of all KV blocks of the step (load-balanced for any
                               length mix), partial rows merged in-kernel; one launch */
+    PDA_KERNEL_BALANCED = 4 /* B200 persistent split-K kernel: one wave of CTAs (producer warp +
+                              4 consumer warps each), CTA c owns an equal share of all KV blocks
+                              of the step, rows merged in-kernel (ticket); one launch */
 } pda_kernel;
 
 typedef struct {
@@ -94,11 +97,12 @@ typedef struct {
     int32_t prefetch;          /* pda_prefetch */
     int32_t prefetch_distance; /* blocks ahead of the block being issued; >= 1 when prefetch on.
                                   Paper kernel: d = 4 (= warps) reproduces Alg. 1 exactly;
-                                  stream kernel: d <= 32 */
+                                  stream / balanced kernels: d <= 32 */
     int32_t partition_tokens;  /* split-K partition size P in tokens; 0 = planner's choice;
                                   otherwise a positive multiple of block_size */
     int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = default.
                                   split-K: 4, 8 (default), 12 (per CTA);
+                                  balanced: 4, 6 (default), 8 (per CTA);
                                   stream: per warp, with stream_warps: (8,1), (4,2), (6,2) default, (4,4) */
     int32_t kernel;            /* pda_kernel */
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
@@ -128,9 +132,9 @@ pda_status pda_plan(const pda_shape* shape, const pda_options* opt, pda_plan_inf
 /* Bytes of device workspace paged_decode_attention needs: the split-K
  * partials (o_p fp32 [B, Hq, P_max, D] and lse_p fp32 [B, Hq, P_max]);
  * 0 when P_max == 1 or for the paper kernel.  Stream kernel: partials of
- * the streams' first/last segments (fp32 [NS, 2, 8*ceil(g/8), D + 1]) and one
+ * the streams' (balanced: CTAs') first/last segments (fp32 [NS, 2, 8*ceil(g/8), D + 1]) and one
  * uint32 arrival ticket per (seq, kv head) at the end of the buffer: the
- * whole workspace must be ZERO before its first use with the stream kernel
+ * whole workspace must be ZERO before its first use with the stream/balanced kernels
  * (every completed call leaves the tickets zero again).
  * Returns 0 on invalid args. */
 size_t pda_workspace_bytes(const pda_shape* shape, const pda_options* opt);
@@ -159,7 +163,7 @@ pda_status paged_decode_attention(const void* q, const void* k_cache, const void
  *            rec[0..1] = token range [s, e) (s = e = min(p*P, L) when empty)
  *   paper:   one record per (b, h, warp) u = (b * Hq + h) * 4 + warp;
  *            rec[0] = first block index (= warp), rec[1] = e = ceil(L / bs)
- *   stream:  one record per row u = b * Hkv + kvh, R = max_blocks_per_seq;
+ *   stream / balanced: one record per row u = b * Hkv + kvh, R = max_blocks_per_seq;
  *            rec[0] = 0, rec[1] = L; visited[j] and prefetch target[j] are
  *            indexed by the block j that issued them (not issue order);
  *            rows with L = 0 stay all -1
@@ -198,7 +202,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 2: pda_options gained stream_warps, reserved */
+int32_t pda_abi_version(void);  /* 3: PDA_KERNEL_BALANCED (the AUTO choice); 2: stream_warps */
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
 PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
-KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3}
+KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4}
 
 # Product default from the round-1 sweep: line-granular L2 prefetch
 # (prefetch.global.L2) 4 blocks ahead; neutral-to-positive for the TMA kernel, while

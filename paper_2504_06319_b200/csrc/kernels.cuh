@@ -65,6 +65,24 @@ struct StreamParams {
     float scale_log2;
 };
 
+struct BalancedParams {
+    const uint16_t* q;
+    const uint16_t* k;
+    const uint16_t* v;
+    const int32_t* bt;
+    const int32_t* lens;
+    void* out;
+    float* ws_o;        // [G][2][NH][D]  partials of a CTA's first/last segment
+    float* ws_lse;      // [G][2][NH]
+    uint32_t* tickets;  // [B * Hkv] self-resetting arrival counters (zero before first use)
+    int32_t* trace;
+    int B, Hq, Hkv, g, max_blocks;
+    int out_dtype;
+    int pf_mode, pf_dist;
+    int trace_rec_len;
+    float scale_log2;
+};
+
 struct CombineParams {
     const float* ws_o;
     const float* ws_lse;
@@ -86,6 +104,11 @@ cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
                           int grid, cudaStream_t stream);
 size_t stream_smem_bytes(int head_dim, int stages, int warps);
 bool stream_config_supported(int stages, int warps);
+
+cudaError_t launch_balanced(const CUtensorMap& tmK, const CUtensorMap& tmV, const BalancedParams& p,
+                            bool bf16, int head_dim, int n_tiles, int stages, bool trace, int grid,
+                            cudaStream_t stream);
+size_t balanced_smem_bytes(int head_dim, int n_tiles, int stages);
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
 

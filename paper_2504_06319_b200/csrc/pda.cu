@@ -14,6 +14,7 @@ namespace {
 constexpr int kDefaultStages = 8;
 constexpr int kDefaultStreamStages = 6;
 constexpr int kDefaultStreamWarps = 2;
+constexpr int kDefaultBalancedStages = 6;
 constexpr size_t kSmemPerSm = 233472;  // 228 KB per SM on B200
 constexpr size_t kSmemReservedPerCta = 1024;
 constexpr int kDefaultSms = 148;  // B200
@@ -41,12 +42,16 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     if (o->prefetch != PDA_PF_OFF && (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
         return PDA_ERR_SHAPE;
     if (o->partition_tokens < 0 || o->partition_tokens % s->block_size != 0) return PDA_ERR_SHAPE;
-    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_STREAM) return PDA_ERR_SHAPE;
+    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_BALANCED) return PDA_ERR_SHAPE;
     if (o->num_sms < 0 || o->stream_warps < 0 || o->reserved != 0) return PDA_ERR_SHAPE;
     if (o->kernel == PDA_KERNEL_STREAM) {
         const int st = o->smem_stages ? o->smem_stages : kDefaultStreamStages;
         const int w = o->stream_warps ? o->stream_warps : kDefaultStreamWarps;
         if (!pda::stream_config_supported(st, w)) return PDA_ERR_UNSUPPORTED;
+        if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
+    } else if (o->kernel == PDA_KERNEL_BALANCED || o->kernel == PDA_KERNEL_AUTO) {
+        if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 6 && o->smem_stages != 8)
+            return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&
                o->smem_stages != 12) {
@@ -100,6 +105,33 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         pl->trace_records = B * Hkv;
         const size_t ns = (size_t)pl->grid_x * w;
         pl->workspace_bytes = align256(ns * 2 * nh * D * 4) + align256(ns * 2 * nh * 4) +
+                              align256((size_t)B * Hkv * 4);
+        return PDA_OK;
+    }
+    if (o->kernel == PDA_KERNEL_BALANCED || o->kernel == PDA_KERNEL_AUTO) {
+        // One persistent wave: as many CTAs as fit (smem, and the register budget
+        // of __launch_bounds__: 3 per SM for g <= 8, 2 for g <= 16).  The
+        // device splits the step's T blocks into G equal ranges (S0).
+        const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
+        const int st = o->smem_stages ? o->smem_stages : kDefaultBalancedStages;
+        const int sms = o->num_sms ? o->num_sms : kDefaultSms;
+        const size_t smem = pda::balanced_smem_bytes(D, n_tiles, st);
+        int per_sm = (int)(kSmemPerSm / (smem + kSmemReservedPerCta));
+        const int reg_cap = n_tiles == 1 ? 3 : 2;
+        per_sm = per_sm < reg_cap ? per_sm : reg_cap;
+        const int nh = 8 * n_tiles;
+        pl->kernel = PDA_KERNEL_BALANCED;
+        pl->partition_tokens = (int32_t)max_tokens;
+        pl->p_max = 1;
+        pl->smem_stages = st;
+        pl->grid_x = sms * per_sm;
+        pl->grid_y = 1;
+        pl->grid_z = 1;
+        pl->threads = pda::splitk_threads();
+        pl->trace_rec_len = 4 + 2 * s->max_blocks_per_seq;
+        pl->trace_records = B * Hkv;
+        const size_t gx = (size_t)pl->grid_x;
+        pl->workspace_bytes = align256(gx * 2 * nh * D * 4) + align256(gx * 2 * nh * 4) +
                               align256((size_t)B * Hkv * 4);
         return PDA_OK;
     }
@@ -230,6 +262,37 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     CUtensorMap tmK, tmV;
     if (!encode_cache_map(&tmK, k_cache, s) || !encode_cache_map(&tmV, v_cache, s))
         return PDA_ERR_CUDA;
+    if (pl.kernel == PDA_KERNEL_BALANCED) {
+        const size_t gx = (size_t)pl.grid_x;
+        const int n_tiles = (s->num_q_heads / s->num_kv_heads) <= 8 ? 1 : 2;
+        const int nh = 8 * n_tiles;
+        pda::BalancedParams bp{};
+        bp.q = static_cast<const uint16_t*>(q);
+        bp.k = static_cast<const uint16_t*>(k_cache);
+        bp.v = static_cast<const uint16_t*>(v_cache);
+        bp.bt = bt;
+        bp.lens = lens;
+        bp.out = out;
+        char* wsc = static_cast<char*>(ws);
+        bp.ws_o = reinterpret_cast<float*>(wsc);
+        bp.ws_lse = reinterpret_cast<float*>(wsc + align256(gx * 2 * nh * s->head_dim * 4));
+        bp.tickets = reinterpret_cast<uint32_t*>(wsc + align256(gx * 2 * nh * s->head_dim * 4) +
+                                                 align256(gx * 2 * nh * 4));
+        bp.trace = trace;
+        bp.B = s->num_seqs;
+        bp.Hq = s->num_q_heads;
+        bp.Hkv = s->num_kv_heads;
+        bp.g = s->num_q_heads / s->num_kv_heads;
+        bp.max_blocks = s->max_blocks_per_seq;
+        bp.out_dtype = s->out_dtype;
+        bp.pf_mode = prefetch_mode;
+        bp.pf_dist = pf_dist;
+        bp.trace_rec_len = pl.trace_rec_len;
+        bp.scale_log2 = scale_log2;
+        err = pda::launch_balanced(tmK, tmV, bp, s->dtype == PDA_BF16, s->head_dim, n_tiles,
+                                   pl.smem_stages, trace != nullptr, pl.grid_x, stream);
+        return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
+    }
     if (pl.kernel == PDA_KERNEL_STREAM) {
         const int w = pl.threads / 32;
         const size_t ns = (size_t)pl.grid_x * w;
@@ -405,6 +468,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 2; }
+int32_t pda_abi_version(void) { return 3; }
 
 }  // extern "C"

@@ -76,8 +76,13 @@ def test_check_args_shape(kw, status):
     (dict(prefetch=3), 2),
     (dict(partition_tokens=24), 2),
     (dict(partition_tokens=32), 0),
-    (dict(smem_stages=6), 3),
+    (dict(kernel=2, smem_stages=6), 3),
+    (dict(smem_stages=6), 0),
+    (dict(smem_stages=12), 3),
+    (dict(kernel=4, prefetch_distance=33), 3),
+    (dict(kernel=5), 2),
     (dict(kernel=7), 2),
+    (dict(kernel=2, prefetch_distance=400), 0),
     (dict(kernel=3), 0),
     (dict(kernel=3, smem_stages=6, stream_warps=2), 0),
     (dict(kernel=3, smem_stages=12), 3),
@@ -121,7 +126,7 @@ def test_plan_no_split_llama2():
     # C2: B=64, 32 kv heads, ctx 4096: 2048 units already fill >= 4 waves -> one partition
     s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
               max_blocks_per_seq=256)
-    p = pda.plan(s, opts())
+    p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 1 and p["partition_tokens"] == 4096 and p["workspace_bytes"] == 0
     assert (p["grid_x"], p["grid_y"], p["grid_z"]) == (1, 32, 64) and p["threads"] == 160
     assert p["trace_rec_len"] == 4 + 2 * 256 and p["trace_records"] == 64 * 32
@@ -131,7 +136,7 @@ def test_plan_split_llama3_8b():
     # C3: 1024 units < 4 waves of 444 -> split 2 -> P = 4096
     s = shape(num_seqs=128, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=65537,
               max_blocks_per_seq=512, dtype=1, out_dtype=1)
-    p = pda.plan(s, opts())
+    p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 2 and p["partition_tokens"] == 4096
     B, Hq, P, D = 128, 32, 2, 128
     assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
@@ -139,7 +144,7 @@ def test_plan_split_llama3_8b():
 
 def test_plan_explicit_partition_and_paper():
     s = shape()
-    p = pda.plan(s, opts(partition_tokens=48))
+    p = pda.plan(s, opts(kernel=2, partition_tokens=48))
     assert p["partition_tokens"] == 48 and p["p_max"] == 6 and p["trace_rec_len"] == 4 + 2 * 3
     pp = pda.plan(s, opts(kernel=1))
     assert pp["kernel"] == 1 and (pp["grid_x"], pp["grid_y"]) == (4, 2) and pp["threads"] == 128
@@ -159,10 +164,24 @@ def test_plan_stream_persistent_grid():
     assert p1["grid_x"] == 148 * 3 and p1["threads"] == 32
 
 
+def test_plan_balanced_is_auto():
+    # D=128, g=1: ring 6 x 8 KiB + merge 16.5 KiB (+align) = 66 KiB -> 3 CTAs/SM -> 444 CTAs
+    s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
+              max_blocks_per_seq=256)
+    p = pda.plan(s, opts())
+    assert p["kernel"] == 4 and p["grid_x"] == 444 and p["threads"] == 160 and p["smem_stages"] == 6
+    G, nh, D = 444, 8, 128
+    assert p["workspace_bytes"] == G * 2 * nh * D * 4 + G * 2 * nh * 4 + 64 * 32 * 4
+    # g = 16 needs two head tiles: register budget caps it at 2 CTAs/SM
+    s16 = shape(num_seqs=8, num_q_heads=32, num_kv_heads=2, head_dim=128, num_blocks=600,
+                max_blocks_per_seq=64)
+    assert pda.plan(s16, opts())["grid_x"] == 296
+
+
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 2
+    assert pda.lib().pda_abi_version() == 3
 
 
 def test_product_never_imports_oracle():

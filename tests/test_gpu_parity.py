@@ -65,7 +65,9 @@ KERNELS = [dict(kernel="splitk"), dict(kernel="splitk", partition_tokens=16),
            dict(kernel="splitk", smem_stages=12, partition_tokens=256), dict(kernel="paper"),
            dict(kernel="stream"), dict(kernel="stream", smem_stages=8, stream_warps=1),
            dict(kernel="stream", smem_stages=4, stream_warps=2),
-           dict(kernel="stream", smem_stages=4, stream_warps=4)]
+           dict(kernel="stream", smem_stages=4, stream_warps=4),
+           dict(kernel="balanced"), dict(kernel="balanced", smem_stages=4),
+           dict(kernel="balanced", smem_stages=8), dict(kernel="balanced", num_sms=3)]
 
 
 @pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: c.name)
@@ -82,18 +84,18 @@ def test_parity_vs_oracle(pda, oracle_mod, cfg, kw):
 
 
 @pytest.mark.parametrize("cfg", SHAPES[:4], ids=lambda c: c.name)
-@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_prefetch_is_bitwise_invisible(pda, cfg, kernel):
     """Prefetch changes where data is found, not what is computed."""
     dev = to_dev(synth.make_inputs(cfg, seed=3))
     base = gpu(pda, dev, kernel=kernel, prefetch="off")
     for mode in ("bulk", "line"):
-        for d in (1, 2, 4, 7, 32 if kernel == "stream" else 64):
+        for d in (1, 2, 4, 7, 32 if kernel in ("stream", "balanced") else 64):
             o = gpu(pda, dev, kernel=kernel, prefetch=mode, prefetch_distance=d)
             assert torch.equal(o, base), (mode, d)
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_placement_invariance_bitwise(pda, kernel):
     inp = synth.make_inputs(SHAPES[2], seed=5)
     a = gpu(pda, to_dev(inp), kernel=kernel)
@@ -101,7 +103,7 @@ def test_placement_invariance_bitwise(pda, kernel):
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_run_to_run_bitwise(pda, kernel):
     dev = to_dev(synth.make_inputs(SHAPES[3], seed=8))
     a = gpu(pda, dev, kernel=kernel, partition_tokens=0 if kernel == "paper" else 128)
@@ -111,7 +113,7 @@ def test_run_to_run_bitwise(pda, kernel):
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
-@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_context_len_one_returns_v_row_exactly(pda, dtype, kernel):
     cfg = synth.Config("l1", 3, 8, 2, 128, (1, 1, 1), dtype, poison_blocks=4)
     inp = synth.make_inputs(cfg, seed=2)
@@ -123,7 +125,7 @@ def test_context_len_one_returns_v_row_exactly(pda, dtype, kernel):
             assert torch.equal(out[b, h].cpu(), inp["v_cache"][blk, h // 4, 0])
 
 
-@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream"])
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_needle_every_position(pda, kernel):
     cfg = synth.Config("needle", 1, 2, 1, 64, (37,), "fp16", poison_blocks=2)
     base = synth.make_inputs(cfg, seed=9)
@@ -187,6 +189,34 @@ def test_trace_paper_matches_alg1(pda, oracle_mod):
             assert (got[1, :, :, 3] == 1).all()
 
 
+def test_trace_balanced_matches_oracle_plan(pda, oracle_mod):
+    cfg = synth.Config("trace_b", 5, 8, 2, 128, (37, 700, 0, 260, 16), "fp16", poison_blocks=3)
+    dev = to_dev(synth.make_inputs(cfg, seed=4))
+    for st, sms in ((6, 0), (4, 2), (8, 1), (6, 5)):
+        for mode, d in (("off", 0), ("bulk", 1), ("line", 4), ("bulk", 32)):
+            _, tr, info = gpu(pda, dev, kernel="balanced", smem_stages=st, num_sms=sms, prefetch=mode,
+                              prefetch_distance=d or None, trace=True)
+            ref = oracle_mod.plan_stream(dev["block_tables"], dev["context_lens"], cfg.num_kv_heads, 16,
+                                         info["grid_x"], d)
+            got = tr.cpu().numpy().reshape(ref.shape)
+            assert np.array_equal(got, ref), (st, sms, mode, d)
+
+
+@pytest.mark.parametrize("sms", [1, 2, 5])
+def test_balanced_split_rows_tickets_reset(pda, oracle_mod, sms):
+    cfg = synth.Config("bsplit", 6, 16, 4, 128, (333, 17, 1, 901, 64, 0), "bf16", poison_blocks=2)
+    inp = synth.make_inputs(cfg, seed=8)
+    ref = oracle_out(oracle_mod, inp)
+    dev = to_dev(inp)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    outs = []
+    for rep in range(3):
+        out = gpu(pda, dev, kernel="balanced", workspace=ws, out_dtype=torch.float32, num_sms=sms)
+        assert max_err(out, ref) <= 5e-4
+        outs.append(out.clone())
+    assert all(torch.equal(o, outs[0]) for o in outs)
+
+
 def test_trace_stream_matches_oracle_plan(pda, oracle_mod):
     cfg = synth.Config("trace_s", 4, 8, 2, 128, (37, 700, 0, 260), "bf16", poison_blocks=3)
     dev = to_dev(synth.make_inputs(cfg, seed=4))
@@ -242,6 +272,7 @@ def test_nan_poison_never_leaks(pda):
 def test_full_size_sampled_stream(pda, oracle_mod, cfg):
     B = cfg.num_seqs
     sampled_check(pda, oracle_mod, cfg, [0, B // 3, B - 1], kernel="stream")
+    sampled_check(pda, oracle_mod, cfg, [1, B // 2, B - 2], kernel="splitk")
 
 
 def test_rejects_cpu_tensors(pda):

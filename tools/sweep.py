@@ -27,6 +27,10 @@ def variants(quick):
         for d in dists:
             vs.append(dict(kernel="splitk", smem_stages=s, prefetch="bulk", prefetch_distance=d))
         vs.append(dict(kernel="splitk", smem_stages=s, prefetch="line", prefetch_distance=4))
+    for st in (6, 4, 8):
+        vs.append(dict(kernel="balanced", smem_stages=st, prefetch="off"))
+        vs.append(dict(kernel="balanced", smem_stages=st, prefetch="line", prefetch_distance=4))
+        vs.append(dict(kernel="balanced", smem_stages=st, prefetch="bulk", prefetch_distance=4))
     for st, w in ((6, 2), (8, 1), (4, 2), (4, 4)):
         vs.append(dict(kernel="stream", smem_stages=st, stream_warps=w, prefetch="off"))
         vs.append(dict(kernel="stream", smem_stages=st, stream_warps=w, prefetch="line", prefetch_distance=4))
@@ -83,7 +87,8 @@ def main():
         outs = {}
         # separate zeroed workspaces: the stream kernel's arrival tickets must start at 0
         wss = {"splitk": torch.zeros(1 << 30, dtype=torch.uint8, device="cuda"),
-               "stream": torch.zeros(256 << 20, dtype=torch.uint8, device="cuda"), "paper": None}
+               "stream": torch.zeros(256 << 20, dtype=torch.uint8, device="cuda"),
+               "balanced": torch.zeros(256 << 20, dtype=torch.uint8, device="cuda"), "paper": None}
         graphs = {}
         for rnd in range(a.rounds):
             for i, v in enumerate(vs):
