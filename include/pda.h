@@ -102,7 +102,7 @@ typedef struct {
                                   otherwise a positive multiple of block_size */
     int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = default.
                                   split-K: 4, 8 (default), 12 (per CTA);
-                                  balanced: 4, 6 (default), 8 (per CTA);
+                                  balanced: 4, 8 (default), 12 (per CTA; multiples of the 4 consumer warps);
                                   stream: per warp, with stream_warps: (8,1), (4,2), (6,2) default, (4,4) */
     int32_t kernel;            /* pda_kernel */
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */

@@ -64,7 +64,9 @@ template <int D, int NT, int S>
 struct BLayout {
     static constexpr int NH = 8 * NT;
     static constexpr int kRing = S * BGeom<D>::kStage;
-    static constexpr int kMergeAcc = kConsumerWarps * NH * (D + 4) * 4;
+    static constexpr int kPasses = 2;              // merge in column halves
+    static constexpr int kDH = D / kPasses;
+    static constexpr int kMergeAcc = kConsumerWarps * NH * (kDH + 4) * 4;
     static constexpr int kMergeML = 2 * kConsumerWarps * NH * 4;
     static constexpr int kBars = 2 * S * 8;
     static constexpr int kMisc = 128;  // T, range, start cursor, ticket broadcast
@@ -292,49 +294,56 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             bm.block(kbase, kbase + G::kSlab, valid, p.scale_log2, lane);
             mbar_arrive(&empty[stage]);
         }
-        // ---- S7: merge the four warps' states of this segment
+        // ---- S7: merge the four warps' states of this segment, in kPasses
+        // column slices so the merge buffer stays small (3 CTAs/SM at S = 8)
         bm.reduce_l();
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreadsC) : "memory");  // merge buffer free
-        if (lane < 4) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int cc2 = 0; cc2 < 2; ++cc2) {
-                    const int h = nt * 8 + 2 * lane + cc2;
-                    merge_m[warp * NH + h] = bm.m_run[nt][cc2];
-                    merge_l[warp * NH + h] = bm.l_run[nt][cc2];
-                }
-        }
-#pragma unroll
-        for (int mi = 0; mi < D / 16; ++mi)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int dd = mi * 16 + r0 + 8 * (r >> 1);
-                    const int h = nt * 8 + t0 + (r & 1);
-                    merge_acc[(warp * NH + h) * (D + 4) + dd] = bm.acc[mi][nt][r];
-                }
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreadsC) : "memory");
         const bool full_row = (j0 == 0 && seg_len == cc.n);
         const int slot = seg_first ? 0 : 1;
-        for (int idx = tid; idx < g * D; idx += kThreadsC) {
-            const int h = idx / D, dd = idx % D;
-            float M = -INFINITY;
 #pragma unroll
-            for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, merge_m[w * NH + h]);
-            float num = 0.f, den = 0.f;
+        for (int pass = 0; pass < Lay::kPasses; ++pass) {
+            asm volatile("bar.sync 1, %0;" ::"n"(kThreadsC) : "memory");  // merge buffer free
+            if (pass == 0 && lane < 4) {
 #pragma unroll
-            for (int w = 0; w < kConsumerWarps; ++w) {
-                const float sc = ex2(merge_m[w * NH + h] - M);
-                den += sc * merge_l[w * NH + h];
-                num += sc * merge_acc[(w * NH + h) * (D + 4) + dd];
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int cc2 = 0; cc2 < 2; ++cc2) {
+                        const int h = nt * 8 + 2 * lane + cc2;
+                        merge_m[warp * NH + h] = bm.m_run[nt][cc2];
+                        merge_l[warp * NH + h] = bm.l_run[nt][cc2];
+                    }
             }
-            if (full_row) {
-                store_out(p.out, (qrow0 + h) * D + dd, num / den, p.out_dtype);
-            } else {
-                p.ws_o[(((size_t)c * 2 + slot) * NH + h) * D + dd] = num / den;
-                if (dd == 0) p.ws_lse[((size_t)c * 2 + slot) * NH + h] = M + __log2f(den);
+#pragma unroll
+            for (int mi = 0; mi < D / 16; ++mi) {
+                if (mi / (D / 16 / Lay::kPasses) != pass) continue;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int dd = mi * 16 + r0 + 8 * (r >> 1) - pass * Lay::kDH;
+                        const int h = nt * 8 + t0 + (r & 1);
+                        merge_acc[(warp * NH + h) * (Lay::kDH + 4) + dd] = bm.acc[mi][nt][r];
+                    }
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kThreadsC) : "memory");
+            for (int idx = tid; idx < g * Lay::kDH; idx += kThreadsC) {
+                const int h = idx / Lay::kDH, dl = idx % Lay::kDH;
+                const int dd = pass * Lay::kDH + dl;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, merge_m[w * NH + h]);
+                float num = 0.f, den = 0.f;
+#pragma unroll
+                for (int w = 0; w < kConsumerWarps; ++w) {
+                    const float sc = ex2(merge_m[w * NH + h] - M);
+                    den += sc * merge_l[w * NH + h];
+                    num += sc * merge_acc[(w * NH + h) * (Lay::kDH + 4) + dl];
+                }
+                if (full_row) {
+                    store_out(p.out, (qrow0 + h) * D + dd, num / den, p.out_dtype);
+                } else {
+                    p.ws_o[(((size_t)c * 2 + slot) * NH + h) * D + dd] = num / den;
+                    if (dd == 0) p.ws_lse[((size_t)c * 2 + slot) * NH + h] = M + __log2f(den);
+                }
             }
         }
         if (!full_row) {
@@ -395,9 +404,13 @@ template <bool BF16, int D, int NT, bool TRACE>
 cudaError_t dispatch_b(const CUtensorMap& tmK, const CUtensorMap& tmV, const BalancedParams& p,
                        int stages, int grid, cudaStream_t s) {
     switch (stages) {
+        // S must be a multiple of the 4 consumer warps: each ring stage then
+        // always belongs to the same warp, which consumed its previous fill, so
+        // the full-barrier parity wait cannot see a stale phase (TMA fills
+        // complete out of order).
         case 4: return launch_b_one<BF16, D, NT, 4, TRACE>(tmK, tmV, p, grid, s);
-        case 6: return launch_b_one<BF16, D, NT, 6, TRACE>(tmK, tmV, p, grid, s);
         case 8: return launch_b_one<BF16, D, NT, 8, TRACE>(tmK, tmV, p, grid, s);
+        case 12: return launch_b_one<BF16, D, NT, 12, TRACE>(tmK, tmV, p, grid, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -407,9 +420,9 @@ cudaError_t dispatch_b(const CUtensorMap& tmK, const CUtensorMap& tmV, const Bal
 size_t balanced_smem_bytes(int head_dim, int n_tiles, int stages) {
 #define PDA_BS(DD, NN, SS) \
     if (head_dim == DD && n_tiles == NN && stages == SS) return BLayout<DD, NN, SS>::kBytes;
-    PDA_BS(64, 1, 4) PDA_BS(64, 1, 6) PDA_BS(64, 1, 8) PDA_BS(64, 2, 4) PDA_BS(64, 2, 6) PDA_BS(64, 2, 8)
-    PDA_BS(128, 1, 4) PDA_BS(128, 1, 6) PDA_BS(128, 1, 8) PDA_BS(128, 2, 4) PDA_BS(128, 2, 6)
-    PDA_BS(128, 2, 8)
+    PDA_BS(64, 1, 4) PDA_BS(64, 1, 8) PDA_BS(64, 1, 12) PDA_BS(64, 2, 4) PDA_BS(64, 2, 8)
+    PDA_BS(64, 2, 12) PDA_BS(128, 1, 4) PDA_BS(128, 1, 8) PDA_BS(128, 1, 12) PDA_BS(128, 2, 4)
+    PDA_BS(128, 2, 8) PDA_BS(128, 2, 12)
 #undef PDA_BS
     return 0;
 }

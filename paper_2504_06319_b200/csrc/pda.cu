@@ -14,7 +14,7 @@ namespace {
 constexpr int kDefaultStages = 8;
 constexpr int kDefaultStreamStages = 6;
 constexpr int kDefaultStreamWarps = 2;
-constexpr int kDefaultBalancedStages = 6;
+constexpr int kDefaultBalancedStages = 8;
 constexpr size_t kSmemPerSm = 233472;  // 228 KB per SM on B200
 constexpr size_t kSmemReservedPerCta = 1024;
 constexpr int kDefaultSms = 148;  // B200
@@ -50,7 +50,7 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         if (!pda::stream_config_supported(st, w)) return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (o->kernel == PDA_KERNEL_BALANCED || o->kernel == PDA_KERNEL_AUTO) {
-        if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 6 && o->smem_stages != 8)
+        if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 && o->smem_stages != 12)
             return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&

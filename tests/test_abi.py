@@ -77,8 +77,8 @@ def test_check_args_shape(kw, status):
     (dict(partition_tokens=24), 2),
     (dict(partition_tokens=32), 0),
     (dict(kernel=2, smem_stages=6), 3),
-    (dict(smem_stages=6), 0),
-    (dict(smem_stages=12), 3),
+    (dict(smem_stages=6), 3),
+    (dict(smem_stages=12), 0),
     (dict(kernel=4, prefetch_distance=33), 3),
     (dict(kernel=5), 2),
     (dict(kernel=7), 2),
@@ -165,11 +165,11 @@ def test_plan_stream_persistent_grid():
 
 
 def test_plan_balanced_is_auto():
-    # D=128, g=1: ring 6 x 8 KiB + merge 16.5 KiB (+align) = 66 KiB -> 3 CTAs/SM -> 444 CTAs
+    # D=128, g=1: ring 8 x 8 KiB + half-width merge 8.5 KiB (+align) = 74 KiB -> 3 CTAs/SM
     s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
               max_blocks_per_seq=256)
     p = pda.plan(s, opts())
-    assert p["kernel"] == 4 and p["grid_x"] == 444 and p["threads"] == 160 and p["smem_stages"] == 6
+    assert p["kernel"] == 4 and p["grid_x"] == 444 and p["threads"] == 160 and p["smem_stages"] == 8
     G, nh, D = 444, 8, 128
     assert p["workspace_bytes"] == G * 2 * nh * D * 4 + G * 2 * nh * 4 + 64 * 32 * 4
     # g = 16 needs two head tiles: register budget caps it at 2 CTAs/SM

@@ -67,7 +67,7 @@ KERNELS = [dict(kernel="splitk"), dict(kernel="splitk", partition_tokens=16),
            dict(kernel="stream", smem_stages=4, stream_warps=2),
            dict(kernel="stream", smem_stages=4, stream_warps=4),
            dict(kernel="balanced"), dict(kernel="balanced", smem_stages=4),
-           dict(kernel="balanced", smem_stages=8), dict(kernel="balanced", num_sms=3)]
+           dict(kernel="balanced", smem_stages=12), dict(kernel="balanced", num_sms=3)]
 
 
 @pytest.mark.parametrize("cfg", SHAPES, ids=lambda c: c.name)
@@ -192,7 +192,7 @@ def test_trace_paper_matches_alg1(pda, oracle_mod):
 def test_trace_balanced_matches_oracle_plan(pda, oracle_mod):
     cfg = synth.Config("trace_b", 5, 8, 2, 128, (37, 700, 0, 260, 16), "fp16", poison_blocks=3)
     dev = to_dev(synth.make_inputs(cfg, seed=4))
-    for st, sms in ((6, 0), (4, 2), (8, 1), (6, 5)):
+    for st, sms in ((8, 0), (4, 2), (12, 1), (8, 5)):
         for mode, d in (("off", 0), ("bulk", 1), ("line", 4), ("bulk", 32)):
             _, tr, info = gpu(pda, dev, kernel="balanced", smem_stages=st, num_sms=sms, prefetch=mode,
                               prefetch_distance=d or None, trace=True)

@@ -27,7 +27,7 @@ def variants(quick):
         for d in dists:
             vs.append(dict(kernel="splitk", smem_stages=s, prefetch="bulk", prefetch_distance=d))
         vs.append(dict(kernel="splitk", smem_stages=s, prefetch="line", prefetch_distance=4))
-    for st in (6, 4, 8):
+    for st in (8, 4, 12):
         vs.append(dict(kernel="balanced", smem_stages=st, prefetch="off"))
         vs.append(dict(kernel="balanced", smem_stages=st, prefetch="line", prefetch_distance=4))
         vs.append(dict(kernel="balanced", smem_stages=st, prefetch="bulk", prefetch_distance=4))
