@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attention us/step & achieved HBM GB/s (prefetch on/off); tokens/s at 1-8 GPU"
+KERNEL_NAMES = {1: "paper_kernel", 2: "splitk_kernel", 3: "stream_kernel", 4: "balanced_kernel"}
 
 
 def parse():
@@ -45,6 +46,7 @@ def parse():
     ap.add_argument("--distance", type=int, default=None)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--partition", type=int, default=0)
+    ap.add_argument("--kernel", default=None, help="auto|splitk|balanced|stream|paper")
     ap.add_argument("--no-extras", action="store_true", help="skip ablation arms / e2e / cpu baseline")
     ap.add_argument("--sweep", action="store_true", help="prefetch-distance x stages sweep (extra JSON lines on stderr)")
     return ap.parse_args()
@@ -241,6 +243,8 @@ def main():
         opt_kw["smem_stages"] = args.stages
     if args.partition:
         opt_kw["partition_tokens"] = args.partition
+    if args.kernel:
+        opt_kw["kernel"] = args.kernel
 
     def make_step(**kw):
         return TPDecodeAttention(inp["k_cache"], inp["v_cache"], local_cfg.num_seqs,
@@ -295,8 +299,8 @@ def main():
                 p_on.append(time_steps(paper_on, max(5, args.steps // 10), 2))
                 p_off.append(time_steps(paper_off, max(5, args.steps // 10), 2))
             extras = {
-                "splitk_prefetch_on_us": statistics.median(on_ms) * 1e3,
-                "splitk_prefetch_off_us": statistics.median(off_ms) * 1e3,
+                "prefetch_on_us": statistics.median(on_ms) * 1e3,
+                "prefetch_off_us": statistics.median(off_ms) * 1e3,
                 "prefetch_speedup": statistics.median(off_ms) / statistics.median(on_ms),
                 "paper_kernel": {
                     "prefetch_on_us": statistics.median(p_on) * 1e3,
@@ -370,7 +374,8 @@ def main():
             "workload": cfg.name, "batch": cfg.num_seqs, "q_heads": cfg.num_q_heads,
             "kv_heads": cfg.num_kv_heads, "head_dim": cfg.head_dim,
             "ctx": max(cfg.context_lens), "block_size": cfg.block_size, "tp": world,
-            "kernel": "splitk", "prefetch": opt_kw.get("prefetch", pda._lib.DEFAULT_PREFETCH),
+            "kernel": KERNEL_NAMES[pl["kernel"]],
+            "prefetch": opt_kw.get("prefetch", pda._lib.DEFAULT_PREFETCH),
             "prefetch_distance": opt_kw.get("prefetch_distance", pda._lib.DEFAULT_DISTANCE),
             "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
             "p_max": pl["p_max"],
@@ -380,7 +385,7 @@ def main():
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": load_traffic(cfg.name),
-            "kernel": "splitk_kernel" + (" + combine_kernel" if pl["p_max"] > 1 else ""),
+            "kernel": KERNEL_NAMES[pl["kernel"]],
             "launch_us": attn_ms * 1e3, "algorithmic_bytes_per_launch": local_bytes,
             "peak_source": peak_src,
         },

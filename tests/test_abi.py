@@ -79,6 +79,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=2, smem_stages=6), 3),
     (dict(smem_stages=6), 3),
     (dict(smem_stages=12), 0),
+    (dict(kernel=4, smem_stages=6), 3),
+    (dict(kernel=4, smem_stages=12), 0),
     (dict(kernel=4, prefetch_distance=33), 3),
     (dict(kernel=5), 2),
     (dict(kernel=7), 2),
@@ -138,8 +140,8 @@ def test_plan_split_llama3_8b():
               max_blocks_per_seq=512, dtype=1, out_dtype=1)
     p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 2 and p["partition_tokens"] == 4096
-    B, Hq, P, D = 128, 32, 2, 128
-    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
+    B, Hq, Hkv, P, D = 128, 32, 8, 2, 128
+    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4 + B * Hkv * 4
 
 
 def test_plan_explicit_partition_and_paper():
@@ -164,18 +166,19 @@ def test_plan_stream_persistent_grid():
     assert p1["grid_x"] == 148 * 3 and p1["threads"] == 32
 
 
-def test_plan_balanced_is_auto():
+def test_plan_balanced_persistent_wave():
     # D=128, g=1: ring 8 x 8 KiB + half-width merge 8.5 KiB (+align) = 74 KiB -> 3 CTAs/SM
     s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
               max_blocks_per_seq=256)
-    p = pda.plan(s, opts())
+    assert pda.plan(s, opts())["kernel"] == 2  # AUTO = split-K
+    p = pda.plan(s, opts(kernel=4))
     assert p["kernel"] == 4 and p["grid_x"] == 444 and p["threads"] == 160 and p["smem_stages"] == 8
     G, nh, D = 444, 8, 128
     assert p["workspace_bytes"] == G * 2 * nh * D * 4 + G * 2 * nh * 4 + 64 * 32 * 4
     # g = 16 needs two head tiles: register budget caps it at 2 CTAs/SM
     s16 = shape(num_seqs=8, num_q_heads=32, num_kv_heads=2, head_dim=128, num_blocks=600,
                 max_blocks_per_seq=64)
-    assert pda.plan(s16, opts())["grid_x"] == 296
+    assert pda.plan(s16, opts(kernel=4))["grid_x"] == 296
 
 
 def test_status_strings():
