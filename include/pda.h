@@ -72,8 +72,8 @@ typedef enum {
     PDA_KERNEL_PAPER = 1,  /* the paper's structure: grid [Hq, B], 4 warps, warp-per-block,
                               K/V loaded to registers (Section 3.1) */
     PDA_KERNEL_SPLITK = 2, /* B200 kernel: split-K over context partitions, TMA ring in
-                              shared memory, mma.sync, GQA group per CTA, partitions merged
-                              in-kernel by the last CTA (ticket); one launch */
+                              shared memory, mma.sync, GQA group per CTA; a small combine
+                              kernel merges partitions when P_max > 1 */
     PDA_KERNEL_STREAM = 3, /* B200 persistent kernel: every warp a self-pipelined stream over an
                               equal share of all KV blocks of the step (load-balanced for any
                               length mix), partial rows merged in-kernel; one launch */
@@ -131,13 +131,12 @@ pda_status pda_check_args(const pda_shape* shape, const pda_options* opt);
 pda_status pda_plan(const pda_shape* shape, const pda_options* opt, pda_plan_info* plan);
 
 /* Bytes of device workspace paged_decode_attention needs: the split-K
- * partials (o_p fp32 [B, Hq, P_max, D] and lse_p fp32 [B, Hq, P_max]) and
- * one uint32 arrival ticket per (seq, kv head); 0 when P_max == 1 or for the
- * paper kernel.  Stream kernel: partials of
+ * partials (o_p fp32 [B, Hq, P_max, D] and lse_p fp32 [B, Hq, P_max]);
+ * 0 when P_max == 1 or for the paper kernel.  Stream kernel: partials of
  * the streams' (balanced: CTAs') first/last segments (fp32 [NS, 2, 8*ceil(g/8), D + 1]) and one
  * uint32 arrival ticket per (seq, kv head) at the end of the buffer: the
  * whole workspace must be ZERO before its first use (every completed call
- * leaves the tickets zero again; applies to split-K, stream and balanced).
+ * leaves the tickets zero again; applies to the stream and balanced kernels).
  * Returns 0 on invalid args. */
 size_t pda_workspace_bytes(const pda_shape* shape, const pda_options* opt);
 
@@ -204,7 +203,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 3: PDA_KERNEL_BALANCED, fused split-K merge; 2: stream_warps */
+int32_t pda_abi_version(void);  /* 3: PDA_KERNEL_BALANCED; 2: stream_warps */
 
 #ifdef __cplusplus
 }

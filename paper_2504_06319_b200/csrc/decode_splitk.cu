@@ -1,5 +1,5 @@
 // decode_splitk.cu -- the B200 decode paged-attention kernel (split-K over
-// context partitions) with the partition merge fused in (last CTA per row).
+// context partitions) and its combine kernel.
 //
 // One CTA per unit (partition p, kv head, sequence b); grid (P_max, Hkv, B).
 //  * Producer warp (warp 4): walks the unit's block-table slice (S1, Alg. 1
@@ -17,8 +17,7 @@
 //  * Epilogue (S7): the 4 warps' (m, l, acc) are merged through shared
 //    memory; a sequence with a single partition writes `out` directly,
 //    otherwise the normalised partial and its log2-sum-exp go to the
-//    workspace and the last partition CTA of the (seq, kv head) to finish
-//    (atomic ticket) merges the partitions in fixed order (S8).
+//    workspace and combine_kernel (S8) merges partitions in fixed order.
 #include "block_math.cuh"
 
 namespace pda {
@@ -234,50 +233,50 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             if (dd == 0) p.ws_lse[row * p.p_max + part] = M + __log2f(den);
         }
     }
-    if (direct) return;
+}
 
-    // ---- S8 fused: the last of the sequence's partition CTAs to finish (a
-    // self-resetting atomic ticket per (b, kv head)) merges the partials in
-    // fixed partition order -- no second kernel launch, deterministic.
-    __threadfence();
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    volatile unsigned* s_ticket = reinterpret_cast<volatile unsigned*>(merge_l + kConsumerWarps * NH);
-    if (threadIdx.x == 0)
-        *s_ticket = atomicInc(p.tickets + (size_t)b * p.Hkv + kvh, (unsigned)(n_parts - 1));
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    if (*s_ticket != (unsigned)(n_parts - 1)) return;
-    __threadfence();
-    for (int idx = threadIdx.x; idx < g * D; idx += kConsumerWarps * 32) {
-        const int h = idx / D, dd = idx % D;
-        const size_t row = (size_t)b * p.Hq + kvh * g + h;
-        const float* lse = p.ws_lse + row * p.p_max;
-        const float* op = p.ws_o + row * p.p_max * D + dd;
-        float M = -INFINITY;
-        for (int q0 = 0; q0 < n_parts; q0 += 4) {  // 4 independent loads in flight
-            float x[4];
+// S8: out = sum_p 2^(lse_p - M) o_p / sum_p 2^(lse_p - M), partitions in fixed order.
+template <int D>
+__global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
+    constexpr int PER = D / 32;
+    const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= p.B * p.Hq) return;
+    const int b = row / p.Hq;
+    int L = p.lens[b];
+    L = L < p.max_tokens ? L : p.max_tokens;
+    const int n_parts = (L + p.part_tokens - 1) / p.part_tokens;
+    if (n_parts <= 1) return;  // written by the main kernel
+    const float* lse = p.ws_lse + (size_t)row * p.p_max;
+    float M = -INFINITY;
+    for (int i = lane; i < n_parts; i += 32) M = fmaxf(M, lse[i]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = q0 + u < n_parts ? __ldcg(lse + q0 + u) : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+    float accv[PER];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) M = fmaxf(M, x[u]);
+    for (int e = 0; e < PER; ++e) accv[e] = 0.f;
+    float den = 0.f;
+    const float* o_base = p.ws_o + (size_t)row * p.p_max * D + lane * PER;
+    for (int part = 0; part < n_parts; ++part) {
+        const float w = ex2(lse[part] - M);
+        den += w;
+        const float* op = o_base + (size_t)part * D;
+        if constexpr (PER == 4) {
+            const float4 x = *reinterpret_cast<const float4*>(op);
+            accv[0] += w * x.x;
+            accv[1] += w * x.y;
+            accv[2] += w * x.z;
+            accv[3] += w * x.w;
+        } else {
+            const float2 x = *reinterpret_cast<const float2*>(op);
+            accv[0] += w * x.x;
+            accv[1] += w * x.y;
         }
-        float num = 0.f, den = 0.f;
-        for (int q0 = 0; q0 < n_parts; q0 += 4) {
-            float l4[4], o4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const bool in = q0 + u < n_parts;
-                l4[u] = in ? __ldcg(lse + q0 + u) : -INFINITY;
-                o4[u] = in ? __ldcg(op + (size_t)(q0 + u) * D) : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float w = ex2(l4[u] - M);
-                den += w;
-                num += w * o4[u];
-            }
-        }
-        store_out(p.out, row * D + dd, num / den, p.out_dtype);
     }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int e = 0; e < PER; ++e)
+        store_out(p.out, (size_t)row * D + lane * PER + e, accv[e] * inv, p.out_dtype);
 }
 
 template <int D, int NT, int STAGES>
@@ -285,7 +284,7 @@ constexpr size_t smem_bytes_for() {
     constexpr int ring = STAGES * Geometry<D>::kStage;
     constexpr int merge = kConsumerWarps * 8 * NT * (D + 4) * 4;
     constexpr int big = ring > merge ? ring : merge;
-    return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4 + 16;
+    return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
 }
 
 template <bool BF16, int D, int NT, int STAGES, bool TRACE>
@@ -354,6 +353,16 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
     }
     return trace ? dispatch_d<false, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
                  : dispatch_d<false, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);
+}
+
+cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream) {
+    const int rows = p.B * p.Hq;
+    const dim3 grid((rows + 3) / 4);
+    if (head_dim == 64)
+        combine_kernel<64><<<grid, 128, 0, stream>>>(p);
+    else
+        combine_kernel<128><<<grid, 128, 0, stream>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace pda

@@ -23,7 +23,6 @@ struct SplitKParams {
     void* out;            // [B, Hq, D]
     float* ws_o;          // [B, Hq, P_max, D]   split-K partial outputs (normalised)
     float* ws_lse;        // [B, Hq, P_max]      log2-sum-exp of each partition
-    uint32_t* tickets;    // [B * Hkv] self-resetting arrival counters (zero before first use)
     int32_t* trace;       // debug trace (TRACE instantiation only)
     int B, Hq, Hkv, g, max_blocks, part_tokens, p_max;
     int out_dtype;
@@ -84,6 +83,14 @@ struct BalancedParams {
     float scale_log2;
 };
 
+struct CombineParams {
+    const float* ws_o;
+    const float* ws_lse;
+    const int32_t* lens;
+    void* out;
+    int B, Hq, p_max, part_tokens, max_tokens;
+    int out_dtype;
+};
 
 // Host launchers (return the launch's cudaError_t).
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
@@ -102,6 +109,8 @@ cudaError_t launch_balanced(const CUtensorMap& tmK, const CUtensorMap& tmV, cons
                             bool bf16, int head_dim, int n_tiles, int stages, bool trace, int grid,
                             cudaStream_t stream);
 size_t balanced_smem_bytes(int head_dim, int n_tiles, int stages);
+
+cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
 
 cudaError_t launch_paper(const PaperParams& p, bool bf16, int head_dim, bool trace, dim3 grid,
                          cudaStream_t stream);

@@ -162,10 +162,8 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->threads = pda::splitk_threads();
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
-    pl->workspace_bytes = p_max > 1 ? align256((size_t)B * Hq * p_max * D * 4) +
-                                          align256((size_t)B * Hq * p_max * 4) +
-                                          align256((size_t)B * Hkv * 4)
-                                    : 0;
+    pl->workspace_bytes =
+        p_max > 1 ? align256((size_t)B * Hq * p_max * D * 4) + align256((size_t)B * Hq * p_max * 4) : 0;
     return PDA_OK;
 }
 
@@ -337,10 +335,6 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     const size_t o_bytes = align256((size_t)s->num_seqs * s->num_q_heads * pl.p_max * s->head_dim * 4);
     p.ws_o = pl.p_max > 1 ? static_cast<float*>(ws) : nullptr;
     p.ws_lse = pl.p_max > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
-    p.tickets = pl.p_max > 1 ? reinterpret_cast<uint32_t*>(
-                                   static_cast<char*>(ws) + o_bytes +
-                                   align256((size_t)s->num_seqs * s->num_q_heads * pl.p_max * 4))
-                             : nullptr;
     p.trace = trace;
     p.B = s->num_seqs;
     p.Hq = s->num_q_heads;
@@ -359,6 +353,24 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
                              pl.smem_stages, trace != nullptr,
                              dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream);
     if (err != cudaSuccess) return PDA_ERR_CUDA;
+    if (pl.p_max > 1) {
+        // S8 as its own small kernel: measured faster than merging in the last
+        // partition CTA (the fused epilogue's fence + ticket cost every CTA a
+        // few microseconds)
+        pda::CombineParams c{};
+        c.ws_o = p.ws_o;
+        c.ws_lse = p.ws_lse;
+        c.lens = lens;
+        c.out = out;
+        c.B = p.B;
+        c.Hq = p.Hq;
+        c.p_max = p.p_max;
+        c.part_tokens = p.part_tokens;
+        c.max_tokens = s->max_blocks_per_seq * s->block_size;
+        c.out_dtype = s->out_dtype;
+        err = pda::launch_combine(c, s->head_dim, stream);
+        if (err != cudaSuccess) return PDA_ERR_CUDA;
+    }
     return PDA_OK;
 }
 

@@ -64,7 +64,8 @@ class TPDecodeAttention:
         self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)  # stream tickets start at 0
 
     def launches_per_step(self) -> int:
-        return 1  # every kernel variant is one launch (partition merge fused in)
+        # split-K launches its combine kernel when sequences are split
+        return 1 + (1 if self.plan["kernel"] == 2 and self.plan["p_max"] > 1 else 0)
 
     def __call__(self, q_local, block_tables, context_lens, scale):
         _lib.paged_decode_attention(q_local, self.k, self.v, block_tables, context_lens, scale,

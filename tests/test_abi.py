@@ -140,8 +140,8 @@ def test_plan_split_llama3_8b():
               max_blocks_per_seq=512, dtype=1, out_dtype=1)
     p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 2 and p["partition_tokens"] == 4096
-    B, Hq, Hkv, P, D = 128, 32, 8, 2, 128
-    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4 + B * Hkv * 4
+    B, Hq, P, D = 128, 32, 2, 128
+    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
 
 
 def test_plan_explicit_partition_and_paper():
