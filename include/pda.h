@@ -67,6 +67,17 @@ typedef enum {
     PDA_PF_LINE_L2 = 2  /* prefetch.global.L2 of every 128-byte line of each slab */
 } pda_prefetch;
 
+/* L2 eviction priority of the KV traffic ("adjusting the cache eviction
+ * priority of prefetched data").  Bit 0: demand K/V loads are marked
+ * evict_first (each block is read once per step, "can be safely
+ * evicted"); bit 1: prefetched lines are marked evict_last. */
+typedef enum {
+    PDA_EV_NORMAL = 0,
+    PDA_EV_DEMAND_FIRST = 1,
+    PDA_EV_PREFETCH_LAST = 2,
+    PDA_EV_BOTH = 3
+} pda_eviction;
+
 typedef enum {
     PDA_KERNEL_AUTO = 0,   /* = PDA_KERNEL_SPLITK (fastest measured on B200) */
     PDA_KERNEL_PAPER = 1,  /* the paper's structure: grid [Hq, B], 4 warps, warp-per-block,
@@ -108,7 +119,7 @@ typedef struct {
     int32_t kernel;            /* pda_kernel */
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
     int32_t stream_warps;      /* stream kernel: warps (streams) per CTA; 0 = default (2) */
-    int32_t reserved;          /* must be 0 */
+    int32_t eviction;          /* pda_eviction (0 = normal) */
 } pda_options;
 
 /* Result of the (host-only, deterministic) split-K planner. */
@@ -203,7 +214,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 3: PDA_KERNEL_BALANCED; 2: stream_warps */
+int32_t pda_abi_version(void);  /* 4: eviction; 3: PDA_KERNEL_BALANCED; 2: stream_warps */
 
 #ifdef __cplusplus
 }

@@ -33,6 +33,56 @@ __device__ __forceinline__ void store_out(void* out, size_t idx, float x, int ou
     }
 }
 
+// S3: TMA loads of one block's K and V slabs (D/64 boxes each) into a ring
+// stage, completion counted on `bar`; demand loads optionally evict_first
+// (the block's lines are not needed again this step).
+template <int D>
+__device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                               int row, uint64_t* bar, int eviction, uint64_t pol_first) {
+    constexpr int kSlab = kBlockSize * D * 2;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+        if (eviction & 1) {
+            tma_load_2d_hint(dst + ch * 2048, tmK, ch * 64, row, bar, pol_first);
+            tma_load_2d_hint(dst + kSlab + ch * 2048, tmV, ch * 64, row, bar, pol_first);
+        } else {
+            tma_load_2d(dst + ch * 2048, tmK, ch * 64, row, bar);
+            tma_load_2d(dst + kSlab + ch * 2048, tmV, ch * 64, row, bar);
+        }
+    }
+}
+
+// S2: L2 prefetch of the K and V slabs starting at element offset `off`
+// (the paper's cp.async.bulk.prefetch.L2, or per-line prefetch.global.L2),
+// optionally evict_last.  Warp-wide call; bulk uses lane 0 only.
+template <int D>
+__device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint16_t* v, size_t off,
+                                                  int pf_mode, int lane, int eviction, uint64_t pol_last) {
+    constexpr int kSlab = kBlockSize * D * 2;
+    if (pf_mode == kPfBulk) {
+        if (lane == 0) {
+            if (eviction & 2) {
+                bulk_prefetch_l2_hint(k + off, kSlab, pol_last);
+                bulk_prefetch_l2_hint(v + off, kSlab, pol_last);
+            } else {
+                bulk_prefetch_l2(k + off, kSlab);
+                bulk_prefetch_l2(v + off, kSlab);
+            }
+        }
+    } else {
+        constexpr int kLines = kSlab / 128;
+        if (lane < kLines) {
+            if (eviction & 2) {
+                prefetch_line_l2_evict_last(k + off + lane * 64);
+                prefetch_line_l2_evict_last(v + off + lane * 64);
+            } else {
+                prefetch_line_l2(k + off + lane * 64);
+                prefetch_line_l2(v + off + lane * 64);
+            }
+        }
+    }
+}
+
 template <bool BF16, int D, int NT>
 struct BlockMath {
     static constexpr int KSTEPS = D / 16;

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
         int win_b = -1, win_base = 0, w0 = 0, w1 = 0;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
         const size_t slab_elems = (size_t)kBlockSize * D;
+        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
         for (long long i = 0; i < total; ++i) {
             // block-id window: ids [win_base, win_base + 64) of row pc.b, 2 per lane
             if (pc.b != win_b || pc.j < win_base) {
@@ -220,12 +221,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
                 if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
                 mbar_arrive_expect_tx(&full[stage], G::kStage);
                 const int rowc = (phys * p.Hkv + pc.kvh) * kBlockSize;
-                uint8_t* dst = ring + stage * G::kStage;
-#pragma unroll
-                for (int ch = 0; ch < G::kChunks; ++ch) tma_load_2d(dst + ch * 2048, &tmK, ch * 64, rowc, &full[stage]);
-#pragma unroll
-                for (int ch = 0; ch < G::kChunks; ++ch)
-                    tma_load_2d(dst + G::kSlab + ch * 2048, &tmV, ch * 64, rowc, &full[stage]);
+                issue_kv_slabs<D>(ring + stage * G::kStage, &tmK, &tmV, rowc, &full[stage], p.eviction,
+                                  pol_first);
                 if constexpr (TRACE) {
                     rec[4 + pc.j] = phys;
                     atomicAdd(rec + 2, pc.j == 0 ? 2 : 1);  // block 0 cancels the -1 fill
@@ -244,18 +241,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
                 const int ta = __shfl_sync(kFullMask, w0, ot & 31), tb = __shfl_sync(kFullMask, w1, ot & 31);
                 const int tgt = ot < 32 ? ta : tb;
                 const size_t off = ((size_t)tgt * p.Hkv + pc.kvh) * slab_elems;
-                if (p.pf_mode == kPfBulk) {
-                    if (lane == 0) {
-                        bulk_prefetch_l2(p.k + off, G::kSlab);
-                        bulk_prefetch_l2(p.v + off, G::kSlab);
-                    }
-                } else {
-                    constexpr int kLines = G::kSlab / 128;
-                    if (lane < kLines) {
-                        prefetch_line_l2(p.k + off + lane * 64);
-                        prefetch_line_l2(p.v + off + lane * 64);
-                    }
-                }
+                prefetch_kv_slabs<D>(p.k, p.v, off, p.pf_mode, lane, p.eviction, pol_last);
                 if constexpr (TRACE) {
                     if (lane == 0) {
                         rec[4 + (p.trace_rec_len - 4) / 2 + pc.j] = tgt;

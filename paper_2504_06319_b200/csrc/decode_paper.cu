@@ -13,24 +13,13 @@
 //    resident Q (line 8) -> online softmax -> P.V.
 //  * The warps' (m, l, acc) are merged through shared memory and the CTA
 //    writes its output row directly (no split-K: the paper has none).
-#include "kernels.cuh"
-#include "ptx.cuh"
+#include "block_math.cuh"
 
 namespace pda {
 
 namespace {
 
-constexpr uint32_t kFull = 0xffffffffu;
-
-__device__ __forceinline__ void store_out(void* out, size_t idx, float x, int out_dtype) {
-    if (out_dtype == 2) {
-        static_cast<float*>(out)[idx] = x;
-    } else if (out_dtype == 1) {
-        static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(x);
-    } else {
-        static_cast<__half*>(out)[idx] = __float2half_rn(x);
-    }
-}
+constexpr uint32_t kFull = kFullMask;
 
 template <bool BF16>
 __device__ __forceinline__ void unpack8(const uint4& w, float (&f)[8]) {
@@ -48,7 +37,6 @@ __global__ void __launch_bounds__(kPaperWarps * 32) paper_kernel(const PaperPara
     constexpr int CH = D / 8;          // 16-byte chunks per token row
     constexpr int TPI = 32 / CH;       // tokens covered by one warp-wide load
     constexpr int NI = kBlockSize / TPI;
-    constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1
 
     __shared__ float sm_m[kPaperWarps], sm_l[kPaperWarps];
     __shared__ float sm_acc[kPaperWarps][D];
@@ -63,6 +51,7 @@ __global__ void __launch_bounds__(kPaperWarps * 32) paper_kernel(const PaperPara
     const int e = (L + kBlockSize - 1) / kBlockSize;
     const int32_t* btrow = p.bt + (size_t)b * p.max_blocks;
     const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
     float qv[8];
     {
@@ -83,15 +72,22 @@ __global__ void __launch_bounds__(kPaperWarps * 32) paper_kernel(const PaperPara
         const int phys = btrow[idx];  // Alg. 1 line 3
         const size_t base = ((size_t)phys * p.Hkv + kvh) * kBlockSize * D;
         uint4 kr[NI], vr[NI];
+        if (p.eviction & 1) {  // demand loads evict_first
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {  // Alg. 1 line 4: K block -> registers
-            const int t = i * TPI + tg;
-            kr[i] = ld_nc_v4(p.k + base + (size_t)t * D + c * 8);
-        }
+            for (int i = 0; i < NI; ++i) kr[i] = ld_nc_v4_hint(p.k + base + (size_t)(i * TPI + tg) * D + c * 8, pol_first);
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            const int t = i * TPI + tg;
-            vr[i] = ld_nc_v4(p.v + base + (size_t)t * D + c * 8);
+            for (int i = 0; i < NI; ++i) vr[i] = ld_nc_v4_hint(p.v + base + (size_t)(i * TPI + tg) * D + c * 8, pol_first);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {  // Alg. 1 line 4: K block -> registers
+                const int t = i * TPI + tg;
+                kr[i] = ld_nc_v4(p.k + base + (size_t)t * D + c * 8);
+            }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int t = i * TPI + tg;
+                vr[i] = ld_nc_v4(p.v + base + (size_t)t * D + c * 8);
+            }
         }
         if constexpr (TRACE) {
             if (lane == 0) rec[4 + nv] = phys;
@@ -100,18 +96,7 @@ __global__ void __launch_bounds__(kPaperWarps * 32) paper_kernel(const PaperPara
         if (d > 0 && idx + d < e) {  // Alg. 1 lines 5-7: prefetch the next block to L2
             const int nphys = btrow[idx + d];
             const size_t nb = ((size_t)nphys * p.Hkv + kvh) * kBlockSize * D;
-            if (p.pf_mode == kPfBulk) {
-                if (lane == 0) {
-                    bulk_prefetch_l2(p.k + nb, kSlab);
-                    bulk_prefetch_l2(p.v + nb, kSlab);
-                }
-            } else {
-                constexpr int kLines = kSlab / 128;
-                if (lane < kLines) {
-                    prefetch_line_l2(p.k + nb + lane * 64);
-                    prefetch_line_l2(p.v + nb + lane * 64);
-                }
-            }
+            prefetch_kv_slabs<D>(p.k, p.v, nb, p.pf_mode, lane, p.eviction, pol_last);
             if constexpr (TRACE) {
                 if (lane == 0) rec[4 + R + npf] = nphys;
             }

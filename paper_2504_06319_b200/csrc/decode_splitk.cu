@@ -107,6 +107,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
         }
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
+        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
         // block ids for 32 blocks at a time, the next chunk loaded one chunk ahead
         int cur = lane < n ? btrow[lane] : 0;
         int pfv = (d > 0 && lane + d < n) ? btrow[lane + d] : -1;
@@ -126,30 +127,14 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
                     if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
                     mbar_arrive_expect_tx(&full[stage], G::kStage);
                     const int row = (phys * p.Hkv + kvh) * kBlockSize;
-                    uint8_t* dst = ring + stage * G::kStage;
-#pragma unroll
-                    for (int ch = 0; ch < G::kChunks; ++ch)
-                        tma_load_2d(dst + ch * 2048, &tmK, ch * 64, row, &full[stage]);
-#pragma unroll
-                    for (int ch = 0; ch < G::kChunks; ++ch)
-                        tma_load_2d(dst + G::kSlab + ch * 2048, &tmV, ch * 64, row, &full[stage]);
+                    issue_kv_slabs<D>(ring + stage * G::kStage, &tmK, &tmV, row, &full[stage], p.eviction,
+                                      pol_first);
                     if constexpr (TRACE) rec[4 + j] = phys;
                 }
                 __syncwarp();
                 if (pf >= 0) {  // warp-uniform: j + d < e (Alg. 1 guard)
                     const size_t off = ((size_t)pf * p.Hkv + kvh) * slab_elems;
-                    if (p.pf_mode == kPfBulk) {
-                        if (lane == 0) {
-                            bulk_prefetch_l2(p.k + off, G::kSlab);
-                            bulk_prefetch_l2(p.v + off, G::kSlab);
-                        }
-                    } else {
-                        constexpr int kLines = G::kSlab / 128;
-                        if (lane < kLines) {
-                            prefetch_line_l2(p.k + off + lane * 64);
-                            prefetch_line_l2(p.v + off + lane * 64);
-                        }
-                    }
+                    prefetch_kv_slabs<D>(p.k, p.v, off, p.pf_mode, lane, p.eviction, pol_last);
                     if constexpr (TRACE) {
                         if (lane == 0) rec[4 + (p.trace_rec_len - 4) / 2 + npf] = pf;
                     }

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(W * 32) stream_kernel(const __grid_constant__ 
     int win_b = -1, win_base = 0, w0 = 0, w1 = 0;
     const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
     const size_t slab_elems = (size_t)kBlockSize * D;
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
     auto window_load = [&](int b, int base) {
         const int32_t* row = p.bt + (size_t)b * p.max_blocks;
@@ -180,12 +181,7 @@ __global__ void __launch_bounds__(W * 32) stream_kernel(const __grid_constant__ 
         if (lane == 0) {
             mbar_arrive_expect_tx(&full[slot], G::kStage);
             const int row = (phys * p.Hkv + pc.kvh) * kBlockSize;
-            uint8_t* dst = ring + slot * G::kStage;
-#pragma unroll
-            for (int ch = 0; ch < G::kChunks; ++ch) tma_load_2d(dst + ch * 2048, &tmK, ch * 64, row, &full[slot]);
-#pragma unroll
-            for (int ch = 0; ch < G::kChunks; ++ch)
-                tma_load_2d(dst + G::kSlab + ch * 2048, &tmV, ch * 64, row, &full[slot]);
+            issue_kv_slabs<D>(ring + slot * G::kStage, &tmK, &tmV, row, &full[slot], p.eviction, pol_first);
         }
         int32_t* rec = nullptr;
         if constexpr (TRACE) {
@@ -205,18 +201,7 @@ __global__ void __launch_bounds__(W * 32) stream_kernel(const __grid_constant__ 
         if (d > 0 && pc.j + d < seg_end) {
             const int tgt = id_at(pc.j + d);
             const size_t off = ((size_t)tgt * p.Hkv + pc.kvh) * slab_elems;
-            if (p.pf_mode == kPfBulk) {
-                if (lane == 0) {
-                    bulk_prefetch_l2(p.k + off, G::kSlab);
-                    bulk_prefetch_l2(p.v + off, G::kSlab);
-                }
-            } else {
-                constexpr int kLines = G::kSlab / 128;
-                if (lane < kLines) {
-                    prefetch_line_l2(p.k + off + lane * 64);
-                    prefetch_line_l2(p.v + off + lane * 64);
-                }
-            }
+            prefetch_kv_slabs<D>(p.k, p.v, off, p.pf_mode, lane, p.eviction, pol_last);
             if constexpr (TRACE) {
                 if (lane == 0) {
                     rec[4 + (p.trace_rec_len - 4) / 2 + pc.j] = tgt;

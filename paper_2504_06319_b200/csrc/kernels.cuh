@@ -27,6 +27,7 @@ struct SplitKParams {
     int B, Hq, Hkv, g, max_blocks, part_tokens, p_max;
     int out_dtype;
     int pf_mode, pf_dist;
+    int eviction;  // pda_eviction bits
     int trace_rec_len;
     float scale_log2;  // scale * log2(e), fp32
 };
@@ -42,6 +43,7 @@ struct PaperParams {
     int B, Hq, Hkv, g, max_blocks;
     int out_dtype;
     int pf_mode, pf_dist;
+    int eviction;  // pda_eviction bits
     int trace_rec_len;
     float scale_log2;
 };
@@ -60,6 +62,7 @@ struct StreamParams {
     int B, Hq, Hkv, g, max_blocks;
     int out_dtype;
     int pf_mode, pf_dist;
+    int eviction;  // pda_eviction bits
     int trace_rec_len;
     int NS;  // streams launched (grid * warps per CTA)
     float scale_log2;
@@ -79,6 +82,7 @@ struct BalancedParams {
     int B, Hq, Hkv, g, max_blocks;
     int out_dtype;
     int pf_mode, pf_dist;
+    int eviction;  // pda_eviction bits
     int trace_rec_len;
     float scale_log2;
 };

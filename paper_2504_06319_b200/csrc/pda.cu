@@ -43,7 +43,7 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         return PDA_ERR_SHAPE;
     if (o->partition_tokens < 0 || o->partition_tokens % s->block_size != 0) return PDA_ERR_SHAPE;
     if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_BALANCED) return PDA_ERR_SHAPE;
-    if (o->num_sms < 0 || o->stream_warps < 0 || o->reserved != 0) return PDA_ERR_SHAPE;
+    if (o->num_sms < 0 || o->stream_warps < 0 || o->eviction < 0 || o->eviction > 3) return PDA_ERR_SHAPE;
     if (o->kernel == PDA_KERNEL_STREAM) {
         const int st = o->smem_stages ? o->smem_stages : kDefaultStreamStages;
         const int w = o->stream_warps ? o->stream_warps : kDefaultStreamWarps;
@@ -252,6 +252,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         p.out_dtype = s->out_dtype;
         p.pf_mode = prefetch_mode;
         p.pf_dist = pf_dist;
+        p.eviction = o->eviction;
         p.trace_rec_len = pl.trace_rec_len;
         p.scale_log2 = scale_log2;
         err = pda::launch_paper(p, s->dtype == PDA_BF16, s->head_dim, trace != nullptr,
@@ -287,6 +288,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         bp.out_dtype = s->out_dtype;
         bp.pf_mode = prefetch_mode;
         bp.pf_dist = pf_dist;
+        bp.eviction = o->eviction;
         bp.trace_rec_len = pl.trace_rec_len;
         bp.scale_log2 = scale_log2;
         err = pda::launch_balanced(tmK, tmV, bp, s->dtype == PDA_BF16, s->head_dim, n_tiles,
@@ -318,6 +320,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         sp.out_dtype = s->out_dtype;
         sp.pf_mode = prefetch_mode;
         sp.pf_dist = pf_dist;
+        sp.eviction = o->eviction;
         sp.trace_rec_len = pl.trace_rec_len;
         sp.NS = (int)ns;
         sp.scale_log2 = scale_log2;
@@ -346,6 +349,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.out_dtype = s->out_dtype;
     p.pf_mode = prefetch_mode;
     p.pf_dist = pf_dist;
+    p.eviction = o->eviction;
     p.trace_rec_len = pl.trace_rec_len;
     p.scale_log2 = scale_log2;
     const int n_tiles = p.g <= 8 ? 1 : 2;
@@ -471,6 +475,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 3; }
+int32_t pda_abi_version(void) { return 4; }
 
 }  // extern "C"

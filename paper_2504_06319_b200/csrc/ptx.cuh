@@ -90,6 +90,30 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* gptr, uint32_t byte
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
 }
 
+// With an L2 cache-policy operand (createpolicy), e.g. evict_last.
+__device__ __forceinline__ void bulk_prefetch_l2_hint(const void* gptr, uint32_t bytes, uint64_t policy) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(gptr), "r"(bytes),
+                 "l"(policy)
+                 : "memory");
+}
+
+// prefetch.global.L2::evict_last of one line -> CCTL.E.PML2.
+__device__ __forceinline__ void prefetch_line_l2_evict_last(const void* gptr) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(gptr));
+}
+
+// L2 cache policies (createpolicy, fraction 1.0).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // prefetch.global.L2 of one line -> CCTL.E.PF2.
 __device__ __forceinline__ void prefetch_line_l2(const void* gptr) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(gptr));
@@ -101,6 +125,14 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4_hint(const void* p, uint64_t policy) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(policy));
     return r;
 }
 

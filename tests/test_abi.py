@@ -49,7 +49,7 @@ def shape(**kw):
 
 def opts(**kw):
     d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0,
-             stream_warps=0, reserved=0)
+             stream_warps=0, eviction=0)
     d.update(kw)
     return _lib.Options(**d)
 
@@ -90,7 +90,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=3, smem_stages=12), 3),
     (dict(kernel=3, prefetch_distance=33), 3),
     (dict(kernel=3, prefetch_distance=32), 0),
-    (dict(reserved=1), 2),
+    (dict(eviction=4), 2),
+    (dict(eviction=3), 0),
 ])
 def test_check_args_options(kw, status):
     assert pda.check_args(shape(), opts(**kw)) == status
@@ -184,7 +185,7 @@ def test_plan_balanced_persistent_wave():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 3
+    assert pda.lib().pda_abi_version() == 4
 
 
 def test_product_never_imports_oracle():

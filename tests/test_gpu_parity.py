@@ -96,6 +96,17 @@ def test_prefetch_is_bitwise_invisible(pda, cfg, kernel):
 
 
 @pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
+def test_eviction_hints_are_bitwise_invisible(pda, kernel):
+    """Eviction priority changes cache residency only."""
+    dev = to_dev(synth.make_inputs(SHAPES[2], seed=13))
+    base = gpu(pda, dev, kernel=kernel, prefetch="off")
+    for ev in (1, 2, 3):
+        for mode in ("bulk", "line"):
+            o = gpu(pda, dev, kernel=kernel, prefetch=mode, prefetch_distance=4, eviction=ev)
+            assert torch.equal(o, base), (ev, mode)
+
+
+@pytest.mark.parametrize("kernel", ["splitk", "paper", "stream", "balanced"])
 def test_placement_invariance_bitwise(pda, kernel):
     inp = synth.make_inputs(SHAPES[2], seed=5)
     a = gpu(pda, to_dev(inp), kernel=kernel)

@@ -40,6 +40,13 @@ def variants(quick):
     for d in ([4] if quick else [1, 2, 4, 8, 16]):
         vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=d))
     vs.append(dict(kernel="paper", prefetch="line", prefetch_distance=4))
+    # eviction priority: demand evict_first / prefetch evict_last / both
+    for ev in (1, 2, 3):
+        vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=4, eviction=ev))
+        vs.append(dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4, eviction=ev))
+        vs.append(dict(kernel="splitk", smem_stages=4, prefetch="line", prefetch_distance=4, eviction=ev))
+    vs.append(dict(kernel="paper", prefetch="off", eviction=1))
+    vs.append(dict(kernel="splitk", smem_stages=8, prefetch="off", eviction=1))
     return vs
 
 
@@ -121,7 +128,8 @@ def main():
         for i, v in enumerate(vs):
             base = next(j for j, w in enumerate(vs) if w["kernel"] == v["kernel"]
                         and w.get("smem_stages") == v.get("smem_stages")
-                        and w.get("stream_warps") == v.get("stream_warps") and w["prefetch"] == "off")
+                        and w.get("stream_warps") == v.get("stream_warps") and w["prefetch"] == "off"
+                        and not w.get("eviction"))
             us = statistics.median(times[i])
             rec = dict(cell=cfg.name, batch=cfg.num_seqs, ctx=max(cfg.context_lens),
                        q_heads=cfg.num_q_heads, kv_heads=cfg.num_kv_heads, dtype=cfg.dtype,
