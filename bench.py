@@ -378,6 +378,7 @@ def main():
             "prefetch": opt_kw.get("prefetch", pda._lib.DEFAULT_PREFETCH),
             "prefetch_distance": opt_kw.get("prefetch_distance", pda._lib.DEFAULT_DISTANCE),
             "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
+            "eviction": ["normal", "demand_first", "prefetch_last", "both"][pl["eviction"]],
             "p_max": pl["p_max"],
             "l2": f"no flush: inputs larger than L2 ({cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)",
             "bytes_per_step": total_bytes,

@@ -75,7 +75,10 @@ typedef enum {
     PDA_EV_NORMAL = 0,
     PDA_EV_DEMAND_FIRST = 1,
     PDA_EV_PREFETCH_LAST = 2,
-    PDA_EV_BOTH = 3
+    PDA_EV_BOTH = 3,
+    PDA_EV_AUTO = 4 /* planner: DEMAND_FIRST when the step's KV bytes (upper bound
+                       B * max_blocks * Hkv * M_block * 2) are <= 2 GiB, else NORMAL
+                       (measured on B200) */
 } pda_eviction;
 
 typedef enum {
@@ -132,6 +135,7 @@ typedef struct {
     int32_t threads;          /* main kernel block size */
     int32_t trace_rec_len;    /* int32 words per trace record (see paged_decode_attention_trace) */
     int32_t trace_records;    /* number of trace records */
+    int32_t eviction;         /* resolved pda_eviction (never PDA_EV_AUTO) */
     size_t workspace_bytes;   /* == pda_workspace_bytes() */
 } pda_plan_info;
 
@@ -214,7 +218,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 4: eviction; 3: PDA_KERNEL_BALANCED; 2: stream_warps */
+int32_t pda_abi_version(void);  /* 5: PDA_EV_AUTO, plan.eviction; 4: eviction; 3: balanced */
 
 #ifdef __cplusplus
 }

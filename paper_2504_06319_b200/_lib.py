@@ -18,7 +18,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
 PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
-EVICTION = {"normal": 0, "demand_first": 1, "prefetch_last": 2, "both": 3}
+EVICTION = {"normal": 0, "demand_first": 1, "prefetch_last": 2, "both": 3, "auto": 4}
+DEFAULT_EVICTION = "auto"
 KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4}
 
 # Product default from the round-1 sweep: line-granular L2 prefetch
@@ -49,7 +50,7 @@ class Options(ctypes.Structure):
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "kernel", "partition_tokens", "p_max", "smem_stages", "grid_x", "grid_y", "grid_z",
-        "threads", "trace_rec_len", "trace_records")] + [("workspace_bytes", ctypes.c_size_t)]
+        "threads", "trace_rec_len", "trace_records", "eviction")] + [("workspace_bytes", ctypes.c_size_t)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -128,7 +129,8 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
 
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
-                 smem_stages=0, kernel="auto", num_sms=0, stream_warps=0, eviction=0) -> Options:
+                 smem_stages=0, kernel="auto", num_sms=0, stream_warps=0,
+                 eviction=DEFAULT_EVICTION) -> Options:
     mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
     if prefetch_distance is None:
         prefetch_distance = DEFAULT_DISTANCE if mode else 0
@@ -169,7 +171,8 @@ def _stream_handle(stream):
 def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scale=None, out=None, *,
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
-                           num_sms=0, eviction=0, workspace=None, stream=None, trace=False):
+                           num_sms=0, eviction=DEFAULT_EVICTION, workspace=None, stream=None,
+                           trace=False):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16),

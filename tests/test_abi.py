@@ -90,7 +90,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=3, smem_stages=12), 3),
     (dict(kernel=3, prefetch_distance=33), 3),
     (dict(kernel=3, prefetch_distance=32), 0),
-    (dict(eviction=4), 2),
+    (dict(eviction=5), 2),
+    (dict(eviction=4), 0),
     (dict(eviction=3), 0),
 ])
 def test_check_args_options(kw, status):
@@ -182,10 +183,20 @@ def test_plan_balanced_persistent_wave():
     assert pda.plan(s16, opts(kernel=4))["grid_x"] == 296
 
 
+def test_eviction_auto_resolution():
+    small = shape(num_seqs=16, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=5000,
+                  max_blocks_per_seq=256)   # 16 x 4096 tokens x 8 heads x 512 B = 0.27 GB
+    big = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
+                max_blocks_per_seq=256)     # 4.3 GB
+    assert pda.plan(small, opts(eviction=4))["eviction"] == 1
+    assert pda.plan(big, opts(eviction=4))["eviction"] == 0
+    assert pda.plan(big, opts(eviction=2))["eviction"] == 2
+
+
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 4
+    assert pda.lib().pda_abi_version() == 5
 
 
 def test_product_never_imports_oracle():
