@@ -286,28 +286,39 @@ def main():
         ms = time_steps(step_main, args.steps, args.warmup)
         extras = {}
         if not args.no_extras:
-            # prefetch ablation arms on the same inputs (ABAB-interleaved)
-            off = make_step(**{**opt_kw, "prefetch": "off"})
-            on_ms, off_ms = [], []
-            for _ in range(3):
-                on_ms.append(time_steps(step_main, max(10, args.steps // 3), 2))
-                off_ms.append(time_steps(off, max(10, args.steps // 3), 2))
-            paper_on = make_step(kernel="paper", prefetch="bulk", prefetch_distance=4)
-            paper_off = make_step(kernel="paper", prefetch="off")
-            p_on, p_off = [], []
-            for _ in range(2):
-                p_on.append(time_steps(paper_on, max(5, args.steps // 10), 2))
-                p_off.append(time_steps(paper_off, max(5, args.steps // 10), 2))
+            # prefetch ablation arms on the same inputs, interleaved step by step
+            # (A B A B ...) with per-step CUDA events, medians per arm
+            arms = {
+                "on": step_main,
+                "off": make_step(**{**opt_kw, "prefetch": "off"}),
+                "paper_on": make_step(kernel="paper", prefetch="bulk", prefetch_distance=4),
+                "paper_off": make_step(kernel="paper", prefetch="off"),
+            }
+            per = {k: [] for k in arms}
+            for k, fn in arms.items():  # warm each arm
+                fn(q, bt, lens, scale)
+            torch.cuda.synchronize()
+            n_rep = max(10, args.steps // 4)
+            for _ in range(n_rep):
+                for k, fn in arms.items():
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn(q, bt, lens, scale)
+                    e1.record(stream)
+                    per[k].append((e0, e1))
+            torch.cuda.synchronize()
+            med = {k: statistics.median(a.elapsed_time(b) for a, b in v) * 1e3 for k, v in per.items()}
             extras = {
-                "prefetch_on_us": statistics.median(on_ms) * 1e3,
-                "prefetch_off_us": statistics.median(off_ms) * 1e3,
-                "prefetch_speedup": statistics.median(off_ms) / statistics.median(on_ms),
+                "prefetch_on_us": med["on"],
+                "prefetch_off_us": med["off"],
+                "prefetch_speedup": med["off"] / med["on"],
                 "paper_kernel": {
-                    "prefetch_on_us": statistics.median(p_on) * 1e3,
-                    "prefetch_off_us": statistics.median(p_off) * 1e3,
-                    "prefetch_speedup": statistics.median(p_off) / statistics.median(p_on),
-                    "desc": "paper structure: grid [Hq,B], 4 warps, warp-per-block LDG, Alg. 1 d=4",
+                    "prefetch_on_us": med["paper_on"],
+                    "prefetch_off_us": med["paper_off"],
+                    "prefetch_speedup": med["paper_off"] / med["paper_on"],
+                    "desc": "paper structure: grid [Hq,B], 4 warps, warp-per-block LDG, Alg. 1 bulk d=4",
                 },
+                "arms_timing": f"{n_rep} interleaved steps per arm, per-step CUDA events, median",
             }
             # in-run read roofline (read-only stream over a 4 GiB buffer)
             buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")

@@ -79,7 +79,7 @@ def main():
     ap.add_argument("--workload", required=True)
     ap.add_argument("--algo-bytes", type=float, required=True)
     ap.add_argument("--tag", required=True)
-    ap.add_argument("--kernel-filter", default="pda::")
+    ap.add_argument("--kernel-filter", default="unnamed>::")
     a = ap.parse_args()
 
     ks = raw(a.rep)
@@ -101,7 +101,7 @@ def main():
             traffic = rd + wr
             md += ["", f"DRAM traffic per launch = {traffic:.4e} B; algorithmic bytes = {a.algo_bytes:.4e} B; "
                    f"ratio = {traffic / a.algo_bytes:.4f}", ""]
-            if a.kernel_filter in name and "splitk_kernel" in name:
+            if "splitk_kernel" in name or "balanced_kernel" in name:
                 summary[a.workload] = {"dram_bytes_per_launch": traffic, "kernel": name[:120],
                                        "algorithmic_bytes": a.algo_bytes, "tag": a.tag}
     if a.launches:
