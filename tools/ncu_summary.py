@@ -79,7 +79,7 @@ def main():
     ap.add_argument("--workload", required=True)
     ap.add_argument("--algo-bytes", type=float, required=True)
     ap.add_argument("--tag", required=True)
-    ap.add_argument("--kernel-filter", default="unnamed>::")
+    ap.add_argument("--kernel-filter", default="pda::")
     a = ap.parse_args()
 
     ks = raw(a.rep)
