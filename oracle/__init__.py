@@ -60,6 +60,11 @@ def lib():
             L.oracle_plan_paper.restype = i32
             L.oracle_plan_stream.argtypes = [p, p, i32, i32, i32, i32, i32, i32, p]
             L.oracle_plan_stream.restype = i32
+            L.oracle_e4m3_to_f64.argtypes = [ctypes.c_uint8]
+            L.oracle_e4m3_to_f64.restype = f64
+            L.oracle_paged_attention_kv8.argtypes = [p, i32, p, p, f64, f64, p, p, i32, i32, i32, i32,
+                                                     i32, i32, f64, p, p, i64, i32]
+            L.oracle_paged_attention_kv8.restype = i32
             L.oracle_eq1_block_bytes.argtypes = [i64, i64, i64]
             L.oracle_eq1_block_bytes.restype = i64
             L.oracle_eq2_total_bytes.argtypes = [i64, i64, i64, i64]
@@ -170,6 +175,37 @@ def plan_stream(block_tables, context_lens, num_kv_heads: int, block_size: int, 
     if rc != 0:
         raise ValueError("oracle_plan_stream: invalid arguments")
     return recs
+
+
+def _u8(a) -> np.ndarray:
+    if hasattr(a, "detach"):
+        import torch
+        a = a.detach().cpu().contiguous().view(torch.uint8).numpy()
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def paged_attention_kv8(q, k_cache, v_cache, k_scale: float, v_scale: float, block_tables,
+                        context_lens, scale: float, q_dtype: str, rows=None, nthreads: int = 0):
+    """fp64 paged decode attention over an e4m3 KV cache with per-tensor scales."""
+    qa, ka, va = _u16(q), _u8(k_cache), _u8(v_cache)
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    B, Hq, D = qa.shape
+    _, Hkv, bs, D2 = ka.shape
+    assert D2 == D and va.shape == ka.shape
+    out = np.full((B, Hq, D), np.nan, dtype=np.float64)
+    rows_a = np.ascontiguousarray(rows, dtype=np.int64) if rows is not None else None
+    rc = lib().oracle_paged_attention_kv8(
+        _ptr(qa), DTYPES[q_dtype], _ptr(ka), _ptr(va), float(k_scale), float(v_scale), _ptr(bt),
+        _ptr(lens), B, Hq, Hkv, D, bs, bt.shape[1], float(scale), _ptr(out),
+        _ptr(rows_a) if rows_a is not None else None, rows_a.size if rows_a is not None else 0,
+        int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_paged_attention_kv8: invalid arguments")
+    return out
+
+
+def e4m3_to_f64(code: int) -> float:
+    return lib().oracle_e4m3_to_f64(code)
 
 
 def fp16_to_f64(bits: int) -> float:

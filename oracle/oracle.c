@@ -21,6 +21,9 @@
  *                            needle, sum of weights = 1.
  *   oracle_attention_weights pinned: sums to 1, matches numpy softmax.
  *   oracle_fp16/bf16_to_f64  pinned: numpy float16 / torch bfloat16 decode.
+ *   oracle_e4m3_to_f64       pinned: torch float8_e4m3fn decode, all 256 codes.
+ *   oracle_paged_attention_kv8 pinned: numpy softmax attention on the
+ *                            dequantised contiguous gather, closed forms.
  *   oracle_plan_splitk       pinned: hand-computed ranges, Alg. 1 guard
  *                            counts, brute-force plan.
  *   oracle_plan_paper        pinned: Alg. 1 guard counts, hand examples.
@@ -67,6 +70,24 @@ double oracle_bf16_to_f64(uint16_t h) {
         v = frac ? NAN : INFINITY;
     } else {
         v = ldexp((double)(frac + 128), exp - 134); /* (1 + f/128) * 2^(e-127) */
+    }
+    return sign ? -v : v;
+}
+
+/* OCP FP8 E4M3 (the "e4m3fn" encoding) -> double, from the format definition:
+ * 1 sign bit, 4 exponent bits with bias 7, 3 fraction bits; no infinities,
+ * S.1111.111 is NaN; max finite 448. */
+double oracle_e4m3_to_f64(uint8_t x) {
+    int sign = (x >> 7) & 1;
+    int exp = (x >> 3) & 0xf;
+    int frac = x & 0x7;
+    double v;
+    if (exp == 15 && frac == 7) {
+        v = NAN;
+    } else if (exp == 0) {
+        v = ldexp((double)frac, -9); /* subnormal: frac/8 * 2^-6 */
+    } else {
+        v = ldexp((double)(frac + 8), exp - 10); /* (1 + f/8) * 2^(e-7) */
     }
     return sign ? -v : v;
 }
@@ -167,6 +188,63 @@ int oracle_paged_attention(const uint16_t* q, const uint16_t* k, const uint16_t*
             int b = (int)(r / Hq), h = (int)(r % Hq);
             attend_row(q, k, v, dtype, bt, lens, b, h, Hq, Hkv, D, bs, max_blocks, scale, w,
                        out + (size_t)r * D);
+        }
+        free(w);
+    }
+    return 0;
+}
+
+/* FP8 KV cache variant: K and V stored as e4m3 codes with
+ * per-tensor scales, k_t = k_scale * e4m3(K[...]), v_t = v_scale * e4m3(V[...]);
+ * q in fp16/bf16 (q_dtype).  Same plain definition as oracle_paged_attention
+ * on the dequantised values:
+ *   s_t = scale * sum_d q[b,h,d] * k_t[d];  out = sum_t softmax(s)_t * v_t. */
+int oracle_paged_attention_kv8(const uint16_t* q, int q_dtype, const uint8_t* k, const uint8_t* v,
+                               double k_scale, double v_scale, const int32_t* bt,
+                               const int32_t* lens, int B, int Hq, int Hkv, int D, int bs,
+                               int max_blocks, double scale, double* out, const int64_t* rows,
+                               int64_t n_rows, int nthreads) {
+    if (B < 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || D <= 0 || bs <= 0 || max_blocks < 0) return -1;
+    int64_t total = rows ? n_rows : (int64_t)B * Hq;
+    int Lmax = max_blocks * bs;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+    {
+        double* w = (double*)malloc(sizeof(double) * (Lmax > 0 ? Lmax : 1));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t i = 0; i < total; ++i) {
+            int64_t r = rows ? rows[i] : i;
+            int b = (int)(r / Hq), h = (int)(r % Hq);
+            int kvh = h / (Hq / Hkv);
+            int L = lens[b];
+            double* o = out + (size_t)r * D;
+            for (int d = 0; d < D; ++d) o[d] = 0.0;
+            if (L <= 0) continue;
+            double m = -INFINITY;
+            for (int t = 0; t < L; ++t) {
+                int64_t phys = bt[(size_t)b * max_blocks + t / bs];
+                double acc = 0.0;
+                for (int d = 0; d < D; ++d)
+                    acc += decode(q[((size_t)b * Hq + h) * D + d], q_dtype) *
+                           (k_scale * oracle_e4m3_to_f64(k[kv_offset(phys, kvh, t % bs, d, Hkv, bs, D)]));
+                w[t] = scale * acc;
+                if (w[t] > m) m = w[t];
+            }
+            double Z = 0.0;
+            for (int t = 0; t < L; ++t) {
+                w[t] = exp(w[t] - m);
+                Z += w[t];
+            }
+            for (int t = 0; t < L; ++t) {
+                int64_t phys = bt[(size_t)b * max_blocks + t / bs];
+                for (int d = 0; d < D; ++d)
+                    o[d] += (w[t] / Z) *
+                            (v_scale * oracle_e4m3_to_f64(v[kv_offset(phys, kvh, t % bs, d, Hkv, bs, D)]));
+            }
         }
         free(w);
     }

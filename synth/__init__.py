@@ -173,6 +173,21 @@ def make_inputs(cfg: Config, seed: int = 0, device="cpu", poison: bool = True,
                 scale=1.0 / math.sqrt(D), cfg=cfg)
 
 
+def quantize_kv_e4m3(inputs: dict, k_scale: float = 1.0 / 224, v_scale: float = 1.0 / 224) -> dict:
+    """FP8 KV-cache variant of `inputs`: K and V stored as
+    OCP e4m3 codes (uint8) of x / scale with per-tensor scales, NaN poison kept
+    as the e4m3 NaN code 0x7F.  The dequantised cache is scale * e4m3(code)."""
+    out = dict(inputs)
+    for name, sc in (("k_cache", k_scale), ("v_cache", v_scale)):
+        x = inputs[name].float()
+        nan = torch.isnan(x)
+        codes = (x / sc).nan_to_num(0.0).to(torch.float8_e4m3fn).view(torch.uint8)
+        codes[nan] = 0x7F
+        out[name] = codes
+    out.update(k_scale=k_scale, v_scale=v_scale, kv_dtype="e4m3")
+    return out
+
+
 def permute_placement(inputs: dict, seed: int) -> dict:
     """Re-place every physical block at a new random position and rewrite the
     block tables consistently (same logical cache, different placement)."""

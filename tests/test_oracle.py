@@ -339,3 +339,41 @@ def test_plan_stream_covers_every_block_once(oracle_mod):
                     if pf[j] != -1:
                         assert j + 3 < n and pf[j] == bt[b, j + 3]
                 assert r[b, h, 3] == (pf != -1).sum()
+
+
+# ---- FP8 (e4m3) KV cache variant -------------------------
+
+def test_e4m3_decode_all_codes(oracle_mod):
+    ref = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).double().numpy()
+    got = np.array([oracle_mod.e4m3_to_f64(c) for c in range(256)])
+    nan = np.isnan(ref)
+    assert (np.isnan(got) == nan).all() and nan.sum() == 2
+    assert (got[~nan] == ref[~nan]).all()
+    assert np.nanmax(got) == 448.0
+
+
+@pytest.mark.parametrize("qdt", ["fp16", "bf16"])
+def test_kv8_oracle_vs_dequantised_numpy(oracle_mod, qdt):
+    cfg = synth.Config("kv8", 3, 8, 2, 128, (37, 1, 90), qdt, poison_blocks=2)
+    inp = synth.quantize_kv_e4m3(synth.make_inputs(cfg, seed=4), k_scale=1 / 200, v_scale=1 / 300)
+    out = oracle_mod.paged_attention_kv8(inp["q"], inp["k_cache"], inp["v_cache"], inp["k_scale"],
+                                         inp["v_scale"], inp["block_tables"], inp["context_lens"],
+                                         inp["scale"], qdt)
+    assert np.isfinite(out).all()
+    deq = dict(inp)
+    deq["k_cache"] = inp["k_cache"].view(torch.float8_e4m3fn).double() * inp["k_scale"]
+    deq["v_cache"] = inp["v_cache"].view(torch.float8_e4m3fn).double() * inp["v_scale"]
+    for b in range(3):
+        for h in range(8):
+            np.testing.assert_allclose(out[b, h], contiguous_reference(deq, b, h), rtol=0, atol=1e-12)
+
+
+def test_kv8_context_one_is_scaled_v_row(oracle_mod):
+    cfg = synth.Config("kv8_l1", 1, 2, 1, 64, (1,), "fp16")
+    inp = synth.quantize_kv_e4m3(synth.make_inputs(cfg, seed=1), v_scale=0.125)
+    out = oracle_mod.paged_attention_kv8(inp["q"], inp["k_cache"], inp["v_cache"], inp["k_scale"],
+                                         inp["v_scale"], inp["block_tables"], inp["context_lens"],
+                                         inp["scale"], "fp16")
+    codes = inp["v_cache"][int(inp["block_tables"][0, 0]), 0, 0]
+    vrow = codes.view(torch.float8_e4m3fn).double().numpy() * 0.125
+    assert np.array_equal(out[0, 0], vrow) and np.array_equal(out[0, 1], vrow)

@@ -1,0 +1,41 @@
+"""Partition-size / ring-depth sweep for one config (CUDA-graph replays, L2 flushed)."""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2504_06319_b200 as pda
+import synth
+from bench import workload_config
+
+cfg = workload_config(sys.argv[1])
+variants = eval(sys.argv[2])
+inp = synth.make_inputs(cfg, seed=0, device="cuda")
+ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+res = {}
+graphs = {}
+outs = {}
+for i, v in enumerate(variants):
+    outs[i] = pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                         inp["context_lens"], inp["scale"], workspace=ws, **v)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="relaxed"):
+        pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                   inp["context_lens"], inp["scale"], out=outs[i], workspace=ws, **v)
+    graphs[i] = g
+    res[i] = []
+for rnd in range(5):
+    for i in graphs:
+        for _ in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); graphs[i].replay(); e1.record(); e1.synchronize()
+            res[i].append(e0.elapsed_time(e1) * 1e3)
+tot = cfg.kv_bytes() + cfg.other_bytes()
+for i, v in enumerate(variants):
+    us = statistics.median(res[i])
+    print(json.dumps(dict(cell=cfg.name, **v, us=round(us, 1), gbs=round(tot / us / 1e3))))
