@@ -58,7 +58,12 @@ typedef enum {
     PDA_ERR_CUDA = 6         /* a CUDA runtime/driver call or launch failed */
 } pda_status;
 
-typedef enum { PDA_F16 = 0, PDA_BF16 = 1, PDA_F32 = 2 /* out_dtype only */ } pda_dtype;
+typedef enum {
+    PDA_F16 = 0,
+    PDA_BF16 = 1,
+    PDA_F32 = 2, /* out_dtype only */
+    PDA_E4M3 = 3 /* kv_dtype only: OCP FP8 E4M3 codes with per-tensor scales */
+} pda_dtype;
 
 /* L2 prefetch of upcoming KV blocks (Section 3.2). */
 typedef enum {
@@ -104,8 +109,11 @@ typedef struct {
     int32_t block_size;         /* tokens per KV block (16) */
     int32_t num_blocks;         /* physical blocks in k_cache / v_cache */
     int32_t max_blocks_per_seq; /* columns of block_tables */
-    int32_t dtype;              /* pda_dtype of q, k_cache, v_cache */
+    int32_t dtype;              /* pda_dtype of q (and of the caches unless kv_dtype says e4m3) */
     int32_t out_dtype;          /* pda_dtype of out */
+    int32_t kv_dtype;           /* pda_dtype of k_cache / v_cache: == dtype, or PDA_E4M3 (1 byte per
+                                   element; value = k_scale|v_scale * e4m3(code); head_dim 128 and the
+                                   split-K kernel only; a bf16 q is converted to fp16 for the MMAs) */
 } pda_shape;
 
 typedef struct {
@@ -123,6 +131,8 @@ typedef struct {
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
     int32_t stream_warps;      /* stream kernel: warps (streams) per CTA; 0 = default (2) */
     int32_t eviction;          /* pda_eviction (0 = normal) */
+    float k_scale;             /* e4m3 cache only: K dequantisation scale (0 = 1.0) */
+    float v_scale;             /* e4m3 cache only: V dequantisation scale (0 = 1.0) */
 } pda_options;
 
 /* Result of the (host-only, deterministic) split-K planner. */
@@ -218,7 +228,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 5: PDA_EV_AUTO, plan.eviction; 4: eviction; 3: balanced */
+int32_t pda_abi_version(void);  /* 6: e4m3 KV (shape.kv_dtype, options.k/v_scale); 5: EV_AUTO */
 
 #ifdef __cplusplus
 }

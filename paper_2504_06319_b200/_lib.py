@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpda.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
-PDA_F16, PDA_BF16, PDA_F32 = 0, 1, 2
+PDA_F16, PDA_BF16, PDA_F32, PDA_E4M3 = 0, 1, 2, 3
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
 EVICTION = {"normal": 0, "demand_first": 1, "prefetch_last": 2, "both": 3, "auto": 4}
 DEFAULT_EVICTION = "auto"
@@ -38,13 +38,13 @@ class PdaError(RuntimeError):
 class Shape(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "num_seqs", "num_q_heads", "num_kv_heads", "head_dim", "block_size", "num_blocks",
-        "max_blocks_per_seq", "dtype", "out_dtype")]
+        "max_blocks_per_seq", "dtype", "out_dtype", "kv_dtype")]
 
 
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms",
-        "stream_warps", "eviction")]
+        "stream_warps", "eviction")] + [("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -116,6 +116,8 @@ def _dtype_code(dt) -> int:
         return PDA_BF16
     if dt == torch.float32:
         return PDA_F32
+    if dt in (torch.uint8, torch.float8_e4m3fn):
+        return PDA_E4M3
     raise TypeError(f"unsupported dtype {dt}")
 
 
@@ -125,18 +127,19 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
     if D2 != D:
         raise ValueError("q and k_cache head_dim differ")
     return Shape(B, Hq, Hkv, D, bs, nb, block_tables.shape[1], _dtype_code(q.dtype),
-                 _dtype_code(out_dtype if out_dtype is not None else q.dtype))
+                 _dtype_code(out_dtype if out_dtype is not None else q.dtype), _dtype_code(k_cache.dtype))
 
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
                  smem_stages=0, kernel="auto", num_sms=0, stream_warps=0,
-                 eviction=DEFAULT_EVICTION) -> Options:
+                 eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0) -> Options:
     mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
     if prefetch_distance is None:
         prefetch_distance = DEFAULT_DISTANCE if mode else 0
     kern = KERNEL[kernel] if not isinstance(kernel, int) else kernel
     return Options(mode, int(prefetch_distance), int(partition_tokens), int(smem_stages), kern,
-                   int(num_sms), int(stream_warps), int(EVICTION.get(eviction, eviction)))
+                   int(num_sms), int(stream_warps), int(EVICTION.get(eviction, eviction)), float(k_scale),
+                   float(v_scale))
 
 
 def plan(shape: Shape, opts: Options) -> dict:
@@ -171,11 +174,12 @@ def _stream_handle(stream):
 def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scale=None, out=None, *,
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
-                           num_sms=0, eviction=DEFAULT_EVICTION, workspace=None, stream=None,
-                           trace=False):
+                           num_sms=0, eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0,
+                           workspace=None, stream=None, trace=False):
     """Decode attention over a paged KV cache (see include/pda.h).
 
-    q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16),
+    q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16 like q, or
+    uint8/float8_e4m3fn e4m3 codes dequantised with k_scale / v_scale),
     block_tables [B, max_blocks] int32, context_lens [B] int32, all CUDA.
     Returns out [B, Hq, D] (and the int32 bookkeeping trace if trace=True).
     """
@@ -185,9 +189,12 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
         raise TypeError("block_tables / context_lens must be int32")
     if out is not None:
         out_dtype = out.dtype
+    if out_dtype is None and k_cache.dtype in (torch.uint8, torch.float8_e4m3fn):
+        out_dtype = q.dtype
     shape = make_shape(q, k_cache, block_tables, out_dtype)
     opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel,
-                        num_sms=num_sms, stream_warps=stream_warps, eviction=eviction)
+                        num_sms=num_sms, stream_warps=stream_warps, eviction=eviction,
+                        k_scale=k_scale, v_scale=v_scale)
     if scale is None:
         scale = q.shape[-1] ** -0.5
     info = plan(shape, opts)

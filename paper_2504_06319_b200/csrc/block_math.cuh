@@ -33,32 +33,36 @@ __device__ __forceinline__ void store_out(void* out, size_t idx, float x, int ou
     }
 }
 
-// S3: TMA loads of one block's K and V slabs (D/64 boxes each) into a ring
-// stage, completion counted on `bar`; demand loads optionally evict_first
-// (the block's lines are not needed again this step).
-template <int D>
+// S3: TMA loads of one block's K and V slabs (kChunks boxes of 16 rows x
+// 128 B each) into a ring stage, completion counted on `bar`; demand loads
+// optionally evict_first (the block is not needed again this step).
+template <int kSlab, int kChunks, int kBoxCols>
 __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                                int row, uint64_t* bar, int eviction, uint64_t pol_first) {
-    constexpr int kSlab = kBlockSize * D * 2;
 #pragma unroll
-    for (int ch = 0; ch < D / 64; ++ch) {
+    for (int ch = 0; ch < kChunks; ++ch) {
         if (eviction & 1) {
-            tma_load_2d_hint(dst + ch * 2048, tmK, ch * 64, row, bar, pol_first);
-            tma_load_2d_hint(dst + kSlab + ch * 2048, tmV, ch * 64, row, bar, pol_first);
+            tma_load_2d_hint(dst + ch * 2048, tmK, ch * kBoxCols, row, bar, pol_first);
+            tma_load_2d_hint(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar, pol_first);
         } else {
-            tma_load_2d(dst + ch * 2048, tmK, ch * 64, row, bar);
-            tma_load_2d(dst + kSlab + ch * 2048, tmV, ch * 64, row, bar);
+            tma_load_2d(dst + ch * 2048, tmK, ch * kBoxCols, row, bar);
+            tma_load_2d(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar);
         }
     }
 }
 
-// S2: L2 prefetch of the K and V slabs starting at element offset `off`
+template <int D>
+__device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                               int row, uint64_t* bar, int eviction, uint64_t pol_first) {
+    issue_kv_slabs<kBlockSize * D * 2, D / 64, 64>(dst, tmK, tmV, row, bar, eviction, pol_first);
+}
+
+// S2: L2 prefetch of the kSlab-byte K and V slabs at byte offset `off`
 // (the paper's cp.async.bulk.prefetch.L2, or per-line prefetch.global.L2),
 // optionally evict_last.  Warp-wide call; bulk uses lane 0 only.
-template <int D>
-__device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint16_t* v, size_t off,
-                                                  int pf_mode, int lane, int eviction, uint64_t pol_last) {
-    constexpr int kSlab = kBlockSize * D * 2;
+template <int kSlab>
+__device__ __forceinline__ void prefetch_kv_bytes(const uint8_t* k, const uint8_t* v, size_t off, int pf_mode,
+                                                  int lane, int eviction, uint64_t pol_last) {
     if (pf_mode == kPfBulk) {
         if (lane == 0) {
             if (eviction & 2) {
@@ -73,14 +77,22 @@ __device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint1
         constexpr int kLines = kSlab / 128;
         if (lane < kLines) {
             if (eviction & 2) {
-                prefetch_line_l2_evict_last(k + off + lane * 64);
-                prefetch_line_l2_evict_last(v + off + lane * 64);
+                prefetch_line_l2_evict_last(k + off + lane * 128);
+                prefetch_line_l2_evict_last(v + off + lane * 128);
             } else {
-                prefetch_line_l2(k + off + lane * 64);
-                prefetch_line_l2(v + off + lane * 64);
+                prefetch_line_l2(k + off + lane * 128);
+                prefetch_line_l2(v + off + lane * 128);
             }
         }
     }
+}
+
+// 16-bit element form (element offset `off`).
+template <int D>
+__device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint16_t* v, size_t off,
+                                                  int pf_mode, int lane, int eviction, uint64_t pol_last) {
+    prefetch_kv_bytes<kBlockSize * D * 2>(reinterpret_cast<const uint8_t*>(k), reinterpret_cast<const uint8_t*>(v),
+                                          off * 2, pf_mode, lane, eviction, pol_last);
 }
 
 template <bool BF16, int D, int NT>
@@ -128,15 +140,17 @@ struct BlockMath {
     // tokens (1..16) are inside the context, the rest are masked.
     __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
                                           int lane) {
+        float s[NT][4], s2[NT][4];
+        qk(kbase, lane, s, s2);
+        uint32_t pb[NT][2], pb_lo[NT][2];
+        softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
+        pv(vbase, valid, lane, pb, pb_lo);
+    }
+
+    // ---- S4: S^T = K Q^T (two independent accumulator chains s, s2)
+    __device__ __forceinline__ void qk(uint32_t kbase, int lane, float (&s)[NT][4], float (&s2)[NT][4]) {
         const int k_t = (lane & 7) + ((lane >> 3) & 1) * 8;
         const int k_c = (lane >> 4) * 8;
-        const int v_t = (lane & 7) + (lane >> 4) * 8;
-        const int v_c = ((lane >> 3) & 1) * 8;
-        const int r0 = lane >> 2;
-        const int t0 = 2 * (lane & 3);
-
-        // ---- S4 (two independent accumulator chains)
-        float s[NT][4], s2[NT][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -153,9 +167,14 @@ struct BlockMath {
                     mma_16816<BF16>(s[nt], a, qf[kk][nt][0], qf[kk][nt][1]);
             }
         }
+    }
 
-        // ---- S5
-        uint32_t pb[NT][2], pb_lo[NT][2];
+    // ---- S5: scale (fp32), mask t >= valid, online softmax per head column;
+    // P leaves as PV B fragments (transposed in registers with movmatrix)
+    __device__ __forceinline__ void softmax(float (&s)[NT][4], const float (&s2)[NT][4], int valid,
+                                            float scale_log2, int lane, uint32_t (&pb)[NT][2],
+                                            uint32_t (&pb_lo)[NT][2]) {
+        const int r0 = lane >> 2;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -195,27 +214,40 @@ struct BlockMath {
                 pb_lo[nt][1] = movmatrix_trans(pack2<true>(pr[2] - h1.x, pr[3] - h1.y));
             }
         }
+    }
 
-        // ---- S6
+    // Zero the V^T fragment elements of tokens >= valid (0 * NaN would poison).
+    static __device__ __forceinline__ void mask_v(uint32_t (&a)[4], int valid, int lane) {
+        const int t0 = 2 * (lane & 3);
+        const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+        const uint32_t m1 = (t0 + 8 < valid ? 0xffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
+        a[0] &= m0;
+        a[1] &= m0;
+        a[2] &= m1;
+        a[3] &= m1;
+    }
+
+    // ---- S6: O^T[d][h] += sum_t V^T[d][t] P[t][h]
+    __device__ __forceinline__ void pv(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2],
+                                       const uint32_t (&pb_lo)[NT][2]) {
+        const int v_t = (lane & 7) + (lane >> 4) * 8;
+        const int v_c = ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
             uint32_t a[4];
             ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
-            if (valid < kBlockSize) {  // zero V rows t >= L (0 * NaN would poison)
-                const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
-                const uint32_t m1 =
-                    (t0 + 8 < valid ? 0xffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
-                a[0] &= m0;
-                a[1] &= m0;
-                a[2] &= m1;
-                a[3] &= m1;
-            }
+            if (valid < kBlockSize) mask_v(a, valid, lane);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 mma_16816<BF16>(acc[i][nt], a, pb[nt][0], pb[nt][1]);
                 if constexpr (BF16) mma_16816<BF16>(acc[i][nt], a, pb_lo[nt][0], pb_lo[nt][1]);
             }
         }
+    }
+
+    // Output column d held by accumulator acc[i][*][r] of this lane.
+    static __device__ __forceinline__ int dcol(int i, int lane, int r) {
+        return i * 16 + (lane >> 2) + 8 * (r >> 1);
     }
 
     // Reduce the per-lane partial row sums across the 8 lanes of each column.
@@ -230,6 +262,110 @@ struct BlockMath {
                 l += __shfl_xor_sync(kFullMask, l, 16);
                 l_run[nt][c] = l;
             }
+    }
+};
+
+// FP8 (e4m3) KV-cache variant, head_dim 128.  K and V
+// slabs are 16 x 128 bytes (one TMA box, SWIZZLE_128B); every e4m3 value is
+// exact in fp16, so the math runs on fp16 MMAs (P in fp16, no hi/lo split).
+//  * QK^T: ldmatrix (b16) over byte rows hands each lane 4 consecutive fp8 of
+//    a token; converted pairwise to f16x2 they fill the A fragment with the
+//    contraction index d permuted within each 16-column k-step -- Q's B
+//    fragment is loaded with the same permutation, so q.k is unchanged.
+//  * PV: V bytes are loaded per token row, converted to f16x2 and transposed
+//    in registers with movmatrix into V^T fragments; the output rows d come
+//    out permuted within each 16-row tile (dcol() gives the mapping).
+// Q_BF16 only selects how q is read (bf16 q is converted to fp16).
+__device__ __forceinline__ void cvt_e4m3x4(uint32_t w, uint32_t& lo, uint32_t& hi) {
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "cvt.rn.f16x2.e4m3x2 %0, l;\n\tcvt.rn.f16x2.e4m3x2 %1, h;\n\t}"
+        : "=r"(lo), "=r"(hi)
+        : "r"(w));
+}
+
+template <bool Q_BF16, int NT>
+struct BlockMathKV8 : BlockMath<false, 128, NT> {
+    using Base = BlockMath<false, 128, NT>;
+    static constexpr int D = 128;
+    static constexpr int MT = D / 16;
+    static constexpr int kSlab = kBlockSize * D;  // 1 byte per element
+
+    // Q B fragments: qf[2j + half][nt] = Q[h][32j + 16 half + 4(lane%4) + {0,1 | 2,3}]
+    __device__ __forceinline__ void load_q(const uint16_t* q, size_t first_row, int g, int lane) {
+        const int h = lane >> 2, t = lane & 3;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int hh = nt * 8 + h;
+            const uint16_t* qrow = q + (first_row + hh) * D;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                uint2 w = make_uint2(0u, 0u);
+                if (hh < g) w = __ldg(reinterpret_cast<const uint2*>(qrow + kk * 16 + 4 * t));
+                if constexpr (Q_BF16) {
+                    const float2 a = unpack2<true>(w.x), b = unpack2<true>(w.y);
+                    w.x = pack2<false>(a.x, a.y);
+                    w.y = pack2<false>(b.x, b.y);
+                }
+                this->qf[kk][nt][0] = w.x;
+                this->qf[kk][nt][1] = w.y;
+            }
+        }
+    }
+
+    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
+                                          int lane) {
+        float s[NT][4], s2[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
+        // ---- S4 on e4m3 K
+        const int kr = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int j = 0; j < D / 32; ++j) {
+            const int unit = 2 * j + (lane >> 4);
+            uint32_t r[4];
+            ldsm_x4(kbase + kr * 128 + ((unit ^ (kr & 7)) << 4), r[0], r[1], r[2], r[3]);
+            uint32_t a[4], c[4];
+            cvt_e4m3x4(r[0], a[0], a[2]);
+            cvt_e4m3x4(r[1], a[1], a[3]);
+            cvt_e4m3x4(r[2], c[0], c[2]);
+            cvt_e4m3x4(r[3], c[1], c[3]);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                mma_16816<false>(s[nt], a, this->qf[2 * j][nt][0], this->qf[2 * j][nt][1]);
+                mma_16816<false>(s2[nt], c, this->qf[2 * j + 1][nt][0], this->qf[2 * j + 1][nt][1]);
+            }
+        }
+        uint32_t pb[NT][2], pb_lo[NT][2];
+        this->softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
+        // ---- S6 on e4m3 V
+        const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int ip = 0; ip < MT / 2; ++ip) {
+            const int unit = 2 * ip + (lane >> 4);
+            uint32_t r[4];
+            ldsm_x4(vbase + vr * 128 + ((unit ^ (vr & 7)) << 4), r[0], r[1], r[2], r[3]);
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
+                uint32_t x0, y0, x1, y1;
+                cvt_e4m3x4(r[2 * c2], x0, y0);      // tokens 0-7
+                cvt_e4m3x4(r[2 * c2 + 1], x1, y1);  // tokens 8-15
+                uint32_t a[4] = {movmatrix_trans(x0), movmatrix_trans(y0), movmatrix_trans(x1),
+                                 movmatrix_trans(y1)};
+                if (valid < kBlockSize) Base::mask_v(a, valid, lane);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    mma_16816<false>(this->acc[2 * ip + c2][nt], a, pb[nt][0], pb[nt][1]);
+            }
+        }
+    }
+
+    // Output column d held by accumulator acc[i][*][r]: rows 0-7 of a tile are
+    // the even-pair columns {0,1,4,5,8,9,12,13}, rows 8-15 the odd pairs.
+    static __device__ __forceinline__ int dcol(int i, int lane, int r) {
+        const int m = lane >> 2;
+        return i * 16 + 4 * (m >> 1) + (m & 1) + 2 * (r >> 1);
     }
 };
 

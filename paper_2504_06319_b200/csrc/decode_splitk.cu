@@ -26,18 +26,30 @@ namespace {
 
 constexpr uint32_t kFull = kFullMask;
 
-template <int D>
+template <int D, bool KV8>
 struct Geometry {
-    static constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1: M_block = b * d_h * T_block
-    static constexpr int kStage = 2 * kSlab;          // K slab + V slab
-    static constexpr int kChunks = D / 64;            // 128-byte column chunks (TMA boxes)
+    static constexpr int kElem = KV8 ? 1 : 2;             // bytes per K/V element (e4m3 | fp16/bf16)
+    static constexpr int kSlab = kBlockSize * D * kElem;  // Eq. 1: M_block = b * d_h * T_block
+    static constexpr int kStage = 2 * kSlab;              // K slab + V slab
+    static constexpr int kBoxCols = 128 / kElem;          // TMA box: 16 rows x 128 bytes
+    static constexpr int kChunks = kSlab / 2048;          // boxes per slab
 };
 
-template <bool BF16, int D, int NT, int STAGES, bool TRACE>
+template <bool BF16, int D, int NT, bool KV8>
+struct MathFor {
+    using type = BlockMath<BF16, D, NT>;
+};
+template <bool BF16, int D, int NT>
+struct MathFor<BF16, D, NT, true> {
+    using type = BlockMathKV8<BF16, NT>;
+};
+
+template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
-    using G = Geometry<D>;
+    using G = Geometry<D, KV8>;
+    using BM = typename MathFor<BF16, D, NT, KV8>::type;
     constexpr int NH = 8 * NT;  // padded heads per CTA
     constexpr int MT = D / 16;  // m-tiles of O^T
 
@@ -112,7 +124,6 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
         int cur = lane < n ? btrow[lane] : 0;
         int pfv = (d > 0 && lane + d < n) ? btrow[lane + d] : -1;
         int npf = 0;
-        const size_t slab_elems = (size_t)kBlockSize * D;
         for (int c = 0; c < n; c += 32) {
             const int nxt = c + 32 + lane < n ? btrow[c + 32 + lane] : 0;
             const int pfn = (d > 0 && c + 32 + lane + d < n) ? btrow[c + 32 + lane + d] : -1;
@@ -127,14 +138,14 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
                     if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
                     mbar_arrive_expect_tx(&full[stage], G::kStage);
                     const int row = (phys * p.Hkv + kvh) * kBlockSize;
-                    issue_kv_slabs<D>(ring + stage * G::kStage, &tmK, &tmV, row, &full[stage], p.eviction,
-                                      pol_first);
+                    issue_kv_slabs<G::kSlab, G::kChunks, G::kBoxCols>(ring + stage * G::kStage, &tmK, &tmV,
+                                                                       row, &full[stage], p.eviction, pol_first);
                     if constexpr (TRACE) rec[4 + j] = phys;
                 }
                 __syncwarp();
                 if (pf >= 0) {  // warp-uniform: j + d < e (Alg. 1 guard)
-                    const size_t off = ((size_t)pf * p.Hkv + kvh) * slab_elems;
-                    prefetch_kv_slabs<D>(p.k, p.v, off, p.pf_mode, lane, p.eviction, pol_last);
+                    const size_t off = ((size_t)pf * p.Hkv + kvh) * G::kSlab;
+                    prefetch_kv_bytes<G::kSlab>(p.k, p.v, off, p.pf_mode, lane, p.eviction, pol_last);
                     if constexpr (TRACE) {
                         if (lane == 0) rec[4 + (p.trace_rec_len - 4) / 2 + npf] = pf;
                     }
@@ -156,7 +167,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     }
 
     // ============================== consumer warps ==============================
-    BlockMath<BF16, D, NT> bm;
+    BM bm;
     bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
     bm.reset();
     for (int j = warp; j < n; j += kConsumerWarps) {
@@ -190,7 +201,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const int dd = i * 16 + r0 + 8 * (r >> 1);
+                const int dd = BM::dcol(i, lane, r);
                 const int h = nt * 8 + t0 + (r & 1);
                 merge_acc[(warp * NH + h) * (D + 4) + dd] = bm.acc[i][nt][r];
             }
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             den += sc * merge_l[w * NH + h];
             num += sc * merge_acc[(w * NH + h) * (D + 4) + dd];
         }
-        const float o = num / den;
+        const float o = num / den * p.out_scale;  // v_scale for the e4m3 cache, else 1
         const size_t row = (size_t)b * p.Hq + kvh * g + h;
         if (direct) {
             store_out(p.out, row * D + dd, o, p.out_dtype);
@@ -265,19 +276,19 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
         store_out(p.out, (size_t)row * D + lane * PER + e, accv[e] * inv, p.out_dtype);
 }
 
-template <int D, int NT, int STAGES>
+template <int D, int NT, int STAGES, bool KV8 = false>
 constexpr size_t smem_bytes_for() {
-    constexpr int ring = STAGES * Geometry<D>::kStage;
+    constexpr int ring = STAGES * Geometry<D, KV8>::kStage;
     constexpr int merge = kConsumerWarps * 8 * NT * (D + 4) * 4;
     constexpr int big = ring > merge ? ring : merge;
     return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
 }
 
-template <bool BF16, int D, int NT, int STAGES, bool TRACE>
+template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8 = false>
 cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                        dim3 grid, cudaStream_t stream) {
-    auto kern = splitk_kernel<BF16, D, NT, STAGES, TRACE>;
-    constexpr size_t smem = smem_bytes_for<D, NT, STAGES>();
+    auto kern = splitk_kernel<BF16, D, NT, STAGES, TRACE, KV8>;
+    constexpr size_t smem = smem_bytes_for<D, NT, STAGES, KV8>();
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -290,15 +301,22 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
     return cudaGetLastError();
 }
 
-template <bool BF16, int D, int NT, bool TRACE>
+template <bool BF16, int D, int NT, bool TRACE, bool KV8 = false>
 cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                             int stages, dim3 grid, cudaStream_t s) {
     switch (stages) {
-        case 4: return launch_one<BF16, D, NT, 4, TRACE>(tmK, tmV, p, grid, s);
-        case 8: return launch_one<BF16, D, NT, 8, TRACE>(tmK, tmV, p, grid, s);
-        case 12: return launch_one<BF16, D, NT, 12, TRACE>(tmK, tmV, p, grid, s);
+        case 4: return launch_one<BF16, D, NT, 4, TRACE, KV8>(tmK, tmV, p, grid, s);
+        case 8: return launch_one<BF16, D, NT, 8, TRACE, KV8>(tmK, tmV, p, grid, s);
+        case 12: return launch_one<BF16, D, NT, 12, TRACE, KV8>(tmK, tmV, p, grid, s);
         default: return cudaErrorInvalidValue;
     }
+}
+
+template <bool BF16, bool TRACE>
+cudaError_t dispatch_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p, int n_tiles,
+                         int stages, dim3 grid, cudaStream_t s) {
+    return n_tiles == 1 ? dispatch_stages<BF16, 128, 1, TRACE, true>(tmK, tmV, p, stages, grid, s)
+                        : dispatch_stages<BF16, 128, 2, TRACE, true>(tmK, tmV, p, stages, grid, s);
 }
 
 template <bool BF16, int D, bool TRACE>
@@ -317,7 +335,15 @@ cudaError_t dispatch_d(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
 
 }  // namespace
 
-size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages) {
+size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8) {
+    if (kv8) {
+        if (head_dim != 128) return 0;
+#define PDA_SMEM8(NN, SS) \
+    if (n_tiles == NN && stages == SS) return smem_bytes_for<128, NN, SS, true>();
+        PDA_SMEM8(1, 4) PDA_SMEM8(1, 8) PDA_SMEM8(1, 12) PDA_SMEM8(2, 4) PDA_SMEM8(2, 8) PDA_SMEM8(2, 12)
+#undef PDA_SMEM8
+        return 0;
+    }
 #define PDA_SMEM_CASE(DD, NN, SS) \
     if (head_dim == DD && n_tiles == NN && stages == SS) return smem_bytes_for<DD, NN, SS>();
     PDA_SMEM_CASE(64, 1, 4) PDA_SMEM_CASE(64, 1, 8) PDA_SMEM_CASE(64, 1, 12)
@@ -332,7 +358,15 @@ int splitk_threads() { return (kConsumerWarps + 1) * 32; }
 
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace, dim3 grid,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, bool kv8) {
+    if (kv8) {
+        if (head_dim != 128) return cudaErrorInvalidValue;
+        if (bf16)
+            return trace ? dispatch_kv8<true, true>(tmK, tmV, p, n_tiles, stages, grid, stream)
+                         : dispatch_kv8<true, false>(tmK, tmV, p, n_tiles, stages, grid, stream);
+        return trace ? dispatch_kv8<false, true>(tmK, tmV, p, n_tiles, stages, grid, stream)
+                     : dispatch_kv8<false, false>(tmK, tmV, p, n_tiles, stages, grid, stream);
+    }
     if (bf16) {
         return trace ? dispatch_d<true, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
                      : dispatch_d<true, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);

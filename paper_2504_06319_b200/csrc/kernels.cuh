@@ -16,8 +16,8 @@ enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };
 
 struct SplitKParams {
     const uint16_t* q;  // [B, Hq, D]
-    const uint16_t* k;  // [num_blocks, Hkv, 16, D] (raw pointer: prefetch addresses)
-    const uint16_t* v;
+    const uint8_t* k;   // [num_blocks, Hkv, 16, D] (bytes: prefetch addresses)
+    const uint8_t* v;
     const int32_t* bt;    // [B, max_blocks]
     const int32_t* lens;  // [B]
     void* out;            // [B, Hq, D]
@@ -29,7 +29,8 @@ struct SplitKParams {
     int pf_mode, pf_dist;
     int eviction;  // pda_eviction bits
     int trace_rec_len;
-    float scale_log2;  // scale * log2(e), fp32
+    float scale_log2;  // scale * log2(e) (* k_scale for an e4m3 cache), fp32
+    float out_scale;   // v_scale for an e4m3 cache, else 1
 };
 
 struct PaperParams {
@@ -99,8 +100,8 @@ struct CombineParams {
 // Host launchers (return the launch's cudaError_t).
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace,
-                          dim3 grid, cudaStream_t stream);
-size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages);
+                          dim3 grid, cudaStream_t stream, bool kv8 = false);
+size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8 = false);
 int splitk_threads();
 
 cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,

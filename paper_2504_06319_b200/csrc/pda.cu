@@ -36,6 +36,11 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     if (s->dtype != PDA_F16 && s->dtype != PDA_BF16) return PDA_ERR_UNSUPPORTED;
     if (s->out_dtype != s->dtype && s->out_dtype != PDA_F32) return PDA_ERR_UNSUPPORTED;
     if (s->head_dim != 64 && s->head_dim != 128) return PDA_ERR_UNSUPPORTED;
+    if (s->kv_dtype != s->dtype && s->kv_dtype != PDA_E4M3) return PDA_ERR_UNSUPPORTED;
+    if (s->kv_dtype == PDA_E4M3 &&
+        (s->head_dim != 128 || (o && o->kernel != PDA_KERNEL_AUTO && o->kernel != PDA_KERNEL_SPLITK)))
+        return PDA_ERR_UNSUPPORTED;
+    if (o && (!(o->k_scale >= 0.f) || !(o->v_scale >= 0.f))) return PDA_ERR_SHAPE;
     if (s->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
     if (s->num_q_heads / s->num_kv_heads > 16) return PDA_ERR_UNSUPPORTED;
     if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_LINE_L2) return PDA_ERR_SHAPE;
@@ -149,6 +154,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
     const int stages = o->smem_stages ? o->smem_stages : kDefaultStages;
     const int sms = o->num_sms ? o->num_sms : kDefaultSms;
+    (void)n_tiles;
     int64_t P;
     if (o->partition_tokens > 0) {
         P = o->partition_tokens;
@@ -194,12 +200,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 bool encode_cache_map(CUtensorMap* m, const void* base, const pda_shape* s) {
     auto enc = get_encode();
     if (!enc) return false;
+    const bool kv8 = s->kv_dtype == PDA_E4M3;
     const cuuint64_t dims[2] = {(cuuint64_t)s->head_dim,
                                 (cuuint64_t)s->num_blocks * s->num_kv_heads * s->block_size};
-    const cuuint64_t strides[1] = {(cuuint64_t)s->head_dim * 2};
-    const cuuint32_t box[2] = {64, (cuuint32_t)s->block_size};
+    const cuuint64_t strides[1] = {(cuuint64_t)s->head_dim * (kv8 ? 1 : 2)};
+    const cuuint32_t box[2] = {kv8 ? 128u : 64u, (cuuint32_t)s->block_size};  // 128-byte rows
     const cuuint32_t estr[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box,
+    return enc(m, kv8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+               const_cast<void*>(base), dims, strides, box,
                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -337,9 +345,11 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
     }
     pda::SplitKParams p{};
+    const bool kv8 = s->kv_dtype == PDA_E4M3;
+    const float k_scale = kv8 && o->k_scale > 0.f ? o->k_scale : 1.f;
     p.q = static_cast<const uint16_t*>(q);
-    p.k = static_cast<const uint16_t*>(k_cache);
-    p.v = static_cast<const uint16_t*>(v_cache);
+    p.k = static_cast<const uint8_t*>(k_cache);
+    p.v = static_cast<const uint8_t*>(v_cache);
     p.bt = bt;
     p.lens = lens;
     p.out = out;
@@ -359,11 +369,12 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.pf_dist = pf_dist;
     p.eviction = pl.eviction;
     p.trace_rec_len = pl.trace_rec_len;
-    p.scale_log2 = scale_log2;
+    p.scale_log2 = (float)((double)scale * k_scale * 1.4426950408889634);
+    p.out_scale = kv8 && o->v_scale > 0.f ? o->v_scale : 1.f;
     const int n_tiles = p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,
-                             dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream);
+                             dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream, kv8);
     if (err != cudaSuccess) return PDA_ERR_CUDA;
     if (pl.p_max > 1) {
         // S8 as its own small kernel: measured faster than merging in the last
@@ -483,6 +494,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 5; }
+int32_t pda_abi_version(void) { return 6; }
 
 }  // extern "C"

@@ -44,12 +44,13 @@ def shape(**kw):
     d = dict(num_seqs=2, num_q_heads=4, num_kv_heads=2, head_dim=64, block_size=16, num_blocks=32,
              max_blocks_per_seq=16, dtype=0, out_dtype=0)
     d.update(kw)
+    d.setdefault("kv_dtype", d["dtype"])
     return _lib.Shape(**d)
 
 
 def opts(**kw):
     d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0,
-             stream_warps=0, eviction=0)
+             stream_warps=0, eviction=0, k_scale=0.0, v_scale=0.0)
     d.update(kw)
     return _lib.Options(**d)
 
@@ -65,6 +66,9 @@ def opts(**kw):
     (dict(out_dtype=2), 0),
     (dict(num_seqs=-1), 2),
     (dict(num_blocks=0), 2),
+    (dict(kv_dtype=3), 3),                 # e4m3 needs head_dim 128
+    (dict(kv_dtype=3, head_dim=128), 0),
+    (dict(kv_dtype=1), 3),                 # bf16 cache with an fp16 q
 ])
 def test_check_args_shape(kw, status):
     assert pda.check_args(shape(**kw), opts()) == status
@@ -91,6 +95,7 @@ def test_check_args_shape(kw, status):
     (dict(kernel=3, prefetch_distance=33), 3),
     (dict(kernel=3, prefetch_distance=32), 0),
     (dict(eviction=5), 2),
+    (dict(k_scale=-1.0), 2),
     (dict(eviction=4), 0),
     (dict(eviction=3), 0),
 ])
@@ -193,10 +198,17 @@ def test_eviction_auto_resolution():
     assert pda.plan(big, opts(eviction=2))["eviction"] == 2
 
 
+def test_e4m3_cache_needs_splitk():
+    s = shape(head_dim=128, kv_dtype=3)
+    assert pda.check_args(s, opts(kernel=2)) == 0
+    for k in (1, 3, 4):
+        assert pda.check_args(s, opts(kernel=k)) == 3
+
+
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 5
+    assert pda.lib().pda_abi_version() == 6
 
 
 def test_product_never_imports_oracle():

@@ -323,3 +323,84 @@ def test_full_size_c5_tp8_shard(pda, oracle_mod):
 def test_sweep_cell_ragged(pda, oracle_mod):
     cfg = synth.sweep_cell(16, 8192, seed=3)
     sampled_check(pda, oracle_mod, cfg, list(range(0, 16, 5)))
+
+
+# ---- FP8 (e4m3) KV cache ---------------------------------
+
+def kv8(inp, ks=1 / 224, vs=1 / 256):
+    return synth.quantize_kv_e4m3(inp, k_scale=ks, v_scale=vs)
+
+
+def oracle_kv8(oracle_mod, inp, rows=None):
+    return oracle_mod.paged_attention_kv8(inp["q"].cpu(), inp["k_cache"].cpu(), inp["v_cache"].cpu(),
+                                          inp["k_scale"], inp["v_scale"], inp["block_tables"].cpu(),
+                                          inp["context_lens"].cpu(), inp["scale"], inp["cfg"].dtype, rows=rows)
+
+
+def gpu_kv8(pda, inp, **kw):
+    return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                      inp["context_lens"], inp["scale"], k_scale=inp["k_scale"],
+                                      v_scale=inp["v_scale"], **kw)
+
+
+KV8_SHAPES = [
+    synth.Config("kv8_mha", 4, 4, 4, 128, (1, 15, 17, 300), "fp16", poison_blocks=5),
+    synth.Config("kv8_gqa4_bf16", 3, 16, 4, 128, (100, 1000, 513), "bf16", poison_blocks=3),
+    synth.Config("kv8_gqa8", 2, 16, 2, 128, (777, 64), "fp16", poison_blocks=2),
+    synth.Config("kv8_gqa16", 2, 32, 2, 128, (95, 250), "bf16", poison_blocks=2),
+    synth.Config("kv8_zero", 3, 4, 2, 128, (0, 5, 0), "fp16", poison_blocks=1),
+]
+
+
+@pytest.mark.parametrize("cfg", KV8_SHAPES, ids=lambda c: c.name)
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=64), dict(smem_stages=4),
+                                dict(smem_stages=12, partition_tokens=256)],
+                         ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
+def test_kv8_parity_vs_oracle(pda, oracle_mod, cfg, kw):
+    inp = kv8(synth.make_inputs(cfg, seed=17))
+    ref = oracle_kv8(oracle_mod, inp)
+    dev = to_dev(inp)
+    assert max_err(gpu_kv8(pda, dev, **kw), ref) <= TOL
+    assert max_err(gpu_kv8(pda, dev, out_dtype=torch.float32, **kw), ref) <= 5e-4
+
+
+def test_kv8_prefetch_eviction_bitwise_invisible(pda):
+    dev = to_dev(kv8(synth.make_inputs(KV8_SHAPES[1], seed=3)))
+    base = gpu_kv8(pda, dev, prefetch="off", eviction="normal")
+    for mode in ("bulk", "line"):
+        for d in (1, 4, 64):
+            for ev in ("normal", "both"):
+                assert torch.equal(gpu_kv8(pda, dev, prefetch=mode, prefetch_distance=d, eviction=ev), base)
+
+
+def test_kv8_context_one_is_scaled_v_row(pda):
+    cfg = synth.Config("kv8_l1", 2, 8, 2, 128, (1, 1), "fp16", poison_blocks=2)
+    inp = kv8(synth.make_inputs(cfg, seed=2), vs=1 / 256)
+    out = gpu_kv8(pda, to_dev(inp), out_dtype=torch.float32)
+    for b in range(2):
+        blk = int(inp["block_tables"][b, 0])
+        for h in range(8):
+            v = inp["v_cache"][blk, h // 4, 0].view(torch.float8_e4m3fn).float() / 256
+            assert torch.equal(out[b, h].cpu(), v)
+
+
+def test_kv8_trace_matches_oracle_plan(pda, oracle_mod):
+    cfg = synth.Config("kv8_trace", 3, 8, 2, 128, (37, 256, 0), "fp16", poison_blocks=3)
+    dev = to_dev(kv8(synth.make_inputs(cfg, seed=1)))
+    for P in (16, 64, 0):
+        _, tr, info = gpu_kv8(pda, dev, partition_tokens=P, prefetch="line", prefetch_distance=3, trace=True)
+        ref = oracle_mod.plan_splitk(dev["block_tables"], dev["context_lens"], 2, 16, info["partition_tokens"],
+                                     info["p_max"], 3)
+        assert np.array_equal(tr.cpu().numpy().reshape(ref.shape), ref)
+
+
+@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
+def test_kv8_full_size_sampled(pda, oracle_mod, cfg):
+    inp = kv8(synth.make_inputs(cfg, seed=0, device="cuda"))
+    out = gpu_kv8(pda, inp)
+    torch.cuda.synchronize()
+    B = cfg.num_seqs
+    sub = synth.sample_rows(inp, [0, B // 2, B - 1])
+    sub.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
+    assert max_err(out[[0, B // 2, B - 1]], oracle_kv8(oracle_mod, sub)) <= TOL
+    assert torch.isfinite(out).all()
