@@ -134,6 +134,9 @@ def workload_config(name: str):
     if name.startswith("c4_"):  # c4_b{B}_ctx{C}
         _, b, c = name.split("_")
         return synth.sweep_cell(int(b[1:]), int(c[3:]))
+    if name.startswith("u_"):  # u_B_Hq_Hkv_D_ctx_dtype: a uniform custom shape
+        _, B, Hq, Hkv, D, ctx, dt = name.split("_")
+        return synth.uniform(name, int(B), int(Hq), int(Hkv), int(D), int(ctx), dt)
     raise SystemExit(f"unknown config {name}")
 
 

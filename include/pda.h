@@ -124,7 +124,8 @@ typedef struct {
     int32_t partition_tokens;  /* split-K partition size P in tokens; 0 = planner's choice;
                                   otherwise a positive multiple of block_size */
     int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = default.
-                                  split-K: 4, 8 (default), 12 (per CTA);
+                                  split-K: 4, 8 (default), 12 (per CTA); e4m3 cache: 8,
+                                  16 (default), 24 (blocks are consumed in pairs);
                                   balanced: 4, 8 (default), 12 (per CTA; multiples of the 4 consumer warps);
                                   stream: per warp, with stream_warps: (8,1), (4,2), (6,2) default, (4,4) */
     int32_t kernel;            /* pda_kernel */

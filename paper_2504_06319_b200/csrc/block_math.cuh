@@ -312,14 +312,12 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         }
     }
 
-    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
-                                          int lane) {
-        float s[NT][4], s2[NT][4];
+    // ---- S4 on e4m3 K (two accumulator chains: even / odd k-steps)
+    __device__ __forceinline__ void qk8(uint32_t kbase, int lane, float (&s)[NT][4], float (&s2)[NT][4]) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
-        // ---- S4 on e4m3 K
         const int kr = (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int j = 0; j < D / 32; ++j) {
@@ -337,9 +335,10 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
                 mma_16816<false>(s2[nt], c, this->qf[2 * j + 1][nt][0], this->qf[2 * j + 1][nt][1]);
             }
         }
-        uint32_t pb[NT][2], pb_lo[NT][2];
-        this->softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
-        // ---- S6 on e4m3 V
+    }
+
+    // ---- S6 on e4m3 V
+    __device__ __forceinline__ void pv8(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2]) {
         const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int ip = 0; ip < MT / 2; ++ip) {
@@ -359,6 +358,70 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
                     mma_16816<false>(this->acc[2 * ip + c2][nt], a, pb[nt][0], pb[nt][1]);
             }
         }
+    }
+
+    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
+                                          int lane) {
+        float s[NT][4], s2[NT][4];
+        qk8(kbase, lane, s, s2);
+        uint32_t pb[NT][2], pb_lo[NT][2];
+        this->softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
+        pv8(vbase, valid, lane, pb);
+    }
+
+    // Two blocks (32 tokens) per step: independent QK chains, ONE online-softmax
+    // update (shared max / rescale), two PV tiles -- halves the per-block
+    // latency chain, which bounds the e4m3 path (half the bytes per block).
+    __device__ __forceinline__ void block2(uint32_t kb0, uint32_t vb0, int valid0, uint32_t kb1, uint32_t vb1,
+                                           int valid1, float scale_log2, int lane) {
+        float sa[NT][4], sa2[NT][4], sb[NT][4], sb2[NT][4];
+        qk8(kb0, lane, sa, sa2);
+        qk8(kb1, lane, sb, sb2);
+        const int r0 = lane >> 2;
+        uint32_t pa[NT][2], pbb[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                sa[nt][r] = (sa[nt][r] + sa2[nt][r]) * scale_log2;
+                sb[nt][r] = (sb[nt][r] + sb2[nt][r]) * scale_log2;
+            }
+            if (valid0 < kBlockSize) {
+                if (r0 >= valid0) sa[nt][0] = sa[nt][1] = -INFINITY;
+                if (r0 + 8 >= valid0) sa[nt][2] = sa[nt][3] = -INFINITY;
+            }
+            if (valid1 < kBlockSize) {
+                if (r0 >= valid1) sb[nt][0] = sb[nt][1] = -INFINITY;
+                if (r0 + 8 >= valid1) sb[nt][2] = sb[nt][3] = -INFINITY;
+            }
+            float pra[4], prb[4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float mx = fmaxf(fmaxf(sa[nt][c], sa[nt][c + 2]), fmaxf(sb[nt][c], sb[nt][c + 2]));
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 4));
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 8));
+                mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 16));
+                const float m_new = fmaxf(this->m_run[nt][c], mx);
+                const float alpha = ex2(this->m_run[nt][c] - m_new);
+                this->m_run[nt][c] = m_new;
+                pra[c] = ex2(sa[nt][c] - m_new);
+                pra[c + 2] = ex2(sa[nt][c + 2] - m_new);
+                prb[c] = ex2(sb[nt][c] - m_new);
+                prb[c + 2] = ex2(sb[nt][c + 2] - m_new);
+                this->l_run[nt][c] = this->l_run[nt][c] * alpha + (pra[c] + pra[c + 2]) + (prb[c] + prb[c + 2]);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    this->acc[i][nt][c] *= alpha;
+                    this->acc[i][nt][c + 2] *= alpha;
+                }
+            }
+            pa[nt][0] = movmatrix_trans(pack2<false>(pra[0], pra[1]));
+            pa[nt][1] = movmatrix_trans(pack2<false>(pra[2], pra[3]));
+            pbb[nt][0] = movmatrix_trans(pack2<false>(prb[0], prb[1]));
+            pbb[nt][1] = movmatrix_trans(pack2<false>(prb[2], prb[3]));
+        }
+        pv8(vb0, valid0, lane, pa);
+        pv8(vb1, valid1, lane, pbb);
     }
 
     // Output column d held by accumulator acc[i][*][r]: rows 0-7 of a tile are

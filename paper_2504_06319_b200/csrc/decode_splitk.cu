@@ -170,14 +170,37 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     BM bm;
     bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
     bm.reset();
-    for (int j = warp; j < n; j += kConsumerWarps) {
-        const int stage = j % STAGES;
-        const uint32_t round = j / STAGES;
-        mbar_wait(&full[stage], round & 1);
-        const uint32_t kbase = smem_u32(ring + stage * G::kStage);
-        const int valid = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
-        bm.block(kbase, kbase + G::kSlab, valid, p.scale_log2, lane);
-        mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
+    if constexpr (KV8) {
+        // e4m3: a warp takes blocks in pairs (2w, 2w+1 mod 8) and runs one softmax
+        // update per pair; with STAGES % 8 == 0 every stage still belongs to one warp
+        static_assert(STAGES % (2 * kConsumerWarps) == 0, "pairs need STAGES % 8 == 0");
+        for (int j = 2 * warp; j < n; j += 2 * kConsumerWarps) {
+            const bool two = j + 1 < n;
+            const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
+            mbar_wait(&full[st0], (j / STAGES) & 1);
+            if (two) mbar_wait(&full[st1], ((j + 1) / STAGES) & 1);
+            const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
+            const int v0 = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
+            if (two) {
+                const int v1 = min(kBlockSize, e_tok - (sb + j + 1) * kBlockSize);
+                bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
+                mbar_arrive(&empty[st0]);
+                mbar_arrive(&empty[st1]);
+            } else {
+                bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                mbar_arrive(&empty[st0]);
+            }
+        }
+    } else {
+        for (int j = warp; j < n; j += kConsumerWarps) {
+            const int stage = j % STAGES;
+            const uint32_t round = j / STAGES;
+            mbar_wait(&full[stage], round & 1);
+            const uint32_t kbase = smem_u32(ring + stage * G::kStage);
+            const int valid = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
+            bm.block(kbase, kbase + G::kSlab, valid, p.scale_log2, lane);
+            mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
+        }
     }
 
     // ---- S7: merge the consumer warps of this unit
@@ -312,11 +335,23 @@ cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, cons
     }
 }
 
+template <bool BF16, int NT, bool TRACE>
+cudaError_t dispatch_stages_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
+                                int stages, dim3 grid, cudaStream_t s) {
+    // 4 KiB stages, consumed in pairs: depth a multiple of 8
+    switch (stages) {
+        case 8: return launch_one<BF16, 128, NT, 8, TRACE, true>(tmK, tmV, p, grid, s);
+        case 16: return launch_one<BF16, 128, NT, 16, TRACE, true>(tmK, tmV, p, grid, s);
+        case 24: return launch_one<BF16, 128, NT, 24, TRACE, true>(tmK, tmV, p, grid, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <bool BF16, bool TRACE>
 cudaError_t dispatch_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p, int n_tiles,
                          int stages, dim3 grid, cudaStream_t s) {
-    return n_tiles == 1 ? dispatch_stages<BF16, 128, 1, TRACE, true>(tmK, tmV, p, stages, grid, s)
-                        : dispatch_stages<BF16, 128, 2, TRACE, true>(tmK, tmV, p, stages, grid, s);
+    return n_tiles == 1 ? dispatch_stages_kv8<BF16, 1, TRACE>(tmK, tmV, p, stages, grid, s)
+                        : dispatch_stages_kv8<BF16, 2, TRACE>(tmK, tmV, p, stages, grid, s);
 }
 
 template <bool BF16, int D, bool TRACE>
@@ -340,7 +375,7 @@ size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8) {
         if (head_dim != 128) return 0;
 #define PDA_SMEM8(NN, SS) \
     if (n_tiles == NN && stages == SS) return smem_bytes_for<128, NN, SS, true>();
-        PDA_SMEM8(1, 4) PDA_SMEM8(1, 8) PDA_SMEM8(1, 12) PDA_SMEM8(2, 4) PDA_SMEM8(2, 8) PDA_SMEM8(2, 12)
+        PDA_SMEM8(1, 8) PDA_SMEM8(1, 16) PDA_SMEM8(1, 24) PDA_SMEM8(2, 8) PDA_SMEM8(2, 16) PDA_SMEM8(2, 24)
 #undef PDA_SMEM8
         return 0;
     }

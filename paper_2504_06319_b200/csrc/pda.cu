@@ -12,6 +12,7 @@
 namespace {
 
 constexpr int kDefaultStages = 8;
+constexpr int kDefaultStagesKV8 = 16;
 constexpr int kDefaultStreamStages = 6;
 constexpr int kDefaultStreamWarps = 2;
 constexpr int kDefaultBalancedStages = 8;
@@ -58,6 +59,9 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 && o->smem_stages != 12)
             return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
+    } else if (s->kv_dtype == PDA_E4M3) {
+        if (o->smem_stages != 0 && o->smem_stages != 8 && o->smem_stages != 16 && o->smem_stages != 24)
+            return PDA_ERR_UNSUPPORTED;
     } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&
                o->smem_stages != 12) {
         return PDA_ERR_UNSUPPORTED;
@@ -152,7 +156,9 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // the partition size so the grid holds >= 4 waves of resident CTAs while a
     // partition keeps >= 512 tokens (32 blocks) to amortise pipeline fill.
     const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
-    const int stages = o->smem_stages ? o->smem_stages : kDefaultStages;
+    // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
+    const int stages = o->smem_stages ? o->smem_stages
+                                      : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
     const int sms = o->num_sms ? o->num_sms : kDefaultSms;
     (void)n_tiles;
     int64_t P;

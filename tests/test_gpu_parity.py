@@ -353,8 +353,9 @@ KV8_SHAPES = [
 
 
 @pytest.mark.parametrize("cfg", KV8_SHAPES, ids=lambda c: c.name)
-@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=64), dict(smem_stages=4),
-                                dict(smem_stages=12, partition_tokens=256)],
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=64), dict(smem_stages=8),
+                                dict(smem_stages=16, partition_tokens=256), dict(smem_stages=24),
+                                dict(partition_tokens=16), dict(partition_tokens=48)],
                          ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
 def test_kv8_parity_vs_oracle(pda, oracle_mod, cfg, kw):
     inp = kv8(synth.make_inputs(cfg, seed=17))

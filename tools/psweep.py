@@ -13,7 +13,11 @@ from bench import workload_config
 
 cfg = workload_config(sys.argv[1])
 variants = eval(sys.argv[2])
+kv8 = len(sys.argv) > 3 and sys.argv[3] == "kv8"
 inp = synth.make_inputs(cfg, seed=0, device="cuda")
+if kv8:
+    inp = synth.quantize_kv_e4m3(inp)
+    variants = [dict(v, k_scale=inp["k_scale"], v_scale=inp["v_scale"]) for v in variants]
 ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 res = {}
@@ -35,7 +39,7 @@ for rnd in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); graphs[i].replay(); e1.record(); e1.synchronize()
             res[i].append(e0.elapsed_time(e1) * 1e3)
-tot = cfg.kv_bytes() + cfg.other_bytes()
+tot = cfg.kv_bytes() // (2 if kv8 else 1) + cfg.other_bytes()
 for i, v in enumerate(variants):
     us = statistics.median(res[i])
-    print(json.dumps(dict(cell=cfg.name, **v, us=round(us, 1), gbs=round(tot / us / 1e3))))
+    print(json.dumps(dict(cell=cfg.name + ("_kv8" if kv8 else ""), **v, us=round(us, 1), gbs=round(tot / us / 1e3))))
