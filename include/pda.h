@@ -120,7 +120,7 @@ typedef struct {
     int32_t prefetch;          /* pda_prefetch */
     int32_t prefetch_distance; /* blocks ahead of the block being issued; >= 1 when prefetch on.
                                   Paper kernel: d = 4 (= warps) reproduces Alg. 1 exactly;
-                                  stream / balanced kernels: d <= 32 */
+                                  stream / balanced kernels and e4m3 caches: d <= 32 */
     int32_t partition_tokens;  /* split-K partition size P in tokens; 0 = planner's choice;
                                   otherwise a positive multiple of block_size */
     int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = default.

@@ -35,6 +35,13 @@ struct Geometry {
     static constexpr int kChunks = kSlab / 2048;          // boxes per slab
 };
 
+// Blocks of a unit with n blocks that consumer warp w handles in pair mode.
+__device__ __forceinline__ int j_count_of(int n, int w) {
+    int c = 0;
+    for (int j = 2 * w; j < n; j += 2 * kConsumerWarps) c += (j + 1 < n) ? 2 : 1;
+    return c;
+}
+
 template <bool BF16, int D, int NT, bool KV8>
 struct MathFor {
     using type = BlockMath<BF16, D, NT>;
@@ -44,8 +51,13 @@ struct MathFor<BF16, D, NT, true> {
     using type = BlockMathKV8<BF16, NT>;
 };
 
+// e4m3 caches: no producer warp -- each consumer warp refills the ring stages it
+// owns (4 issuers instead of 1: the 2 KiB slabs need twice the issue rate).
+template <bool KV8>
+constexpr int splitk_block_threads() { return (kConsumerWarps + (KV8 ? 0 : 1)) * 32; }
+
 template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8>
-__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
+__global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
     using G = Geometry<D, KV8>;
@@ -108,10 +120,14 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
         }
         fence_barrier_init();
+        if constexpr (TRACE && KV8) {
+            rec[2] = 0;
+            rec[3] = 0;
+        }
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
+    if (!KV8 && warp == kConsumerWarps) {
         // ============================ producer warp ============================
         if (lane == 0) {
             prefetch_tmap(&tmK);
@@ -171,9 +187,58 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
     bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
     bm.reset();
     if constexpr (KV8) {
-        // e4m3: a warp takes blocks in pairs (2w, 2w+1 mod 8) and runs one softmax
-        // update per pair; with STAGES % 8 == 0 every stage still belongs to one warp
+        // e4m3: a warp takes blocks in pairs (2w, 2w+1 mod 8), runs one softmax
+        // update per pair, and refills the two stages it just read (it owns
+        // every stage s with (s % 8) / 2 == w, so no empty barriers are needed
+        // and a parity wait always refers to the warp's own previous fill).
         static_assert(STAGES % (2 * kConsumerWarps) == 0, "pairs need STAGES % 8 == 0");
+        const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
+        const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;  // <= 32 (validated)
+        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+        if (lane == 0 && warp == 0) {
+            prefetch_tmap(&tmK);
+            prefetch_tmap(&tmV);
+        }
+        int wbase = 0;  // block-id window [wbase, wbase + 64) of this unit, 2 ids per lane
+        int w0 = lane < n ? btrow[lane] : 0;
+        int w1 = 32 + lane < n ? btrow[32 + lane] : 0;
+        int npf = 0;
+        auto id_at = [&](int pos) {
+            const int o = pos - wbase;
+            const int x = __shfl_sync(kFull, w0, o & 31), y = __shfl_sync(kFull, w1, o & 31);
+            return o < 32 ? x : y;
+        };
+        auto issue = [&](int pos) {  // S1 + S3 (+ S2) for block `pos` of the unit, warp-wide
+            while (pos >= wbase + 32) {
+                w0 = w1;
+                wbase += 32;
+                w1 = wbase + 32 + lane < n ? btrow[wbase + 32 + lane] : 0;
+            }
+            const int phys = id_at(pos);
+            const bool pf = d > 0 && pos + d < n;  // Alg. 1 guard against the unit end
+            const int tgt = pf ? id_at(pos + d) : -1;
+            const int st = pos % STAGES;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&full[st], G::kStage);
+                issue_kv_slabs<G::kSlab, G::kChunks, G::kBoxCols>(ring + st * G::kStage, &tmK, &tmV,
+                                                                   (phys * p.Hkv + kvh) * kBlockSize, &full[st],
+                                                                   p.eviction, pol_first);
+                if constexpr (TRACE) rec[4 + pos] = phys;
+            }
+            if (pf) {
+                prefetch_kv_bytes<G::kSlab>(p.k, p.v, ((size_t)tgt * p.Hkv + kvh) * G::kSlab, p.pf_mode, lane,
+                                            p.eviction, pol_last);
+                if constexpr (TRACE) {
+                    // every block below n - d prefetches, so issue order == block order
+                    if (lane == 0) rec[4 + (p.trace_rec_len - 4) / 2 + pos] = tgt;
+                }
+                ++npf;
+            }
+        };
+        for (int pos = 2 * warp; pos < STAGES && pos < n; pos += 2 * kConsumerWarps) {
+            issue(pos);
+            if (pos + 1 < n) issue(pos + 1);
+        }
         for (int j = 2 * warp; j < n; j += 2 * kConsumerWarps) {
             const bool two = j + 1 < n;
             const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
@@ -184,11 +249,20 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
             if (two) {
                 const int v1 = min(kBlockSize, e_tok - (sb + j + 1) * kBlockSize);
                 bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
-                mbar_arrive(&empty[st0]);
-                mbar_arrive(&empty[st1]);
             } else {
                 bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
-                mbar_arrive(&empty[st0]);
+            }
+            // our ldmatrix reads of the two stages are complete (their registers fed
+            // the MMAs above); order them before the async-proxy refills
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (j + STAGES < n) issue(j + STAGES);
+            if (j + 1 + STAGES < n) issue(j + 1 + STAGES);
+        }
+        if constexpr (TRACE) {
+            if (lane == 0) {
+                atomicAdd(rec + 2, (j_count_of(n, warp)));
+                atomicAdd(rec + 3, npf);
             }
         }
     } else {
@@ -203,6 +277,12 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, NT == 1 ? 3 : 2)
         }
     }
 
+    if constexpr (TRACE && KV8) {
+        if (threadIdx.x == 0) {
+            rec[0] = s_tok;
+            rec[1] = e_tok;
+        }
+    }
     // ---- S7: merge the consumer warps of this unit
     bm.reduce_l();
     const int r0 = lane >> 2;
@@ -320,7 +400,7 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
         if (e != cudaSuccess) return e;
         configured_device = dev;
     }
-    kern<<<grid, (kConsumerWarps + 1) * 32, smem, stream>>>(tmK, tmV, p);
+    kern<<<grid, splitk_block_threads<KV8>(), smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();
 }
 
@@ -389,7 +469,7 @@ size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8) {
     return 0;
 }
 
-int splitk_threads() { return (kConsumerWarps + 1) * 32; }
+int splitk_threads(bool kv8) { return kv8 ? splitk_block_threads<true>() : splitk_block_threads<false>(); }
 
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace, dim3 grid,

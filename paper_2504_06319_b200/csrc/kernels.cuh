@@ -102,7 +102,7 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace,
                           dim3 grid, cudaStream_t stream, bool kv8 = false);
 size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8 = false);
-int splitk_threads();
+int splitk_threads(bool kv8 = false);
 
 cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, int warps, bool trace,

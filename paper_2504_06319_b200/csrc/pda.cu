@@ -62,6 +62,7 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     } else if (s->kv_dtype == PDA_E4M3) {
         if (o->smem_stages != 0 && o->smem_stages != 8 && o->smem_stages != 16 && o->smem_stages != 24)
             return PDA_ERR_UNSUPPORTED;
+        if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&
                o->smem_stages != 12) {
         return PDA_ERR_UNSUPPORTED;
@@ -179,7 +180,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->grid_x = (int32_t)p_max;
     pl->grid_y = Hkv;
     pl->grid_z = B;
-    pl->threads = pda::splitk_threads();
+    pl->threads = pda::splitk_threads(s->kv_dtype == PDA_E4M3);
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
     pl->workspace_bytes =

@@ -369,7 +369,7 @@ def test_kv8_prefetch_eviction_bitwise_invisible(pda):
     dev = to_dev(kv8(synth.make_inputs(KV8_SHAPES[1], seed=3)))
     base = gpu_kv8(pda, dev, prefetch="off", eviction="normal")
     for mode in ("bulk", "line"):
-        for d in (1, 4, 64):
+        for d in (1, 4, 32):
             for ev in ("normal", "both"):
                 assert torch.equal(gpu_kv8(pda, dev, prefetch=mode, prefetch_distance=d, eviction=ev), base)
 
