@@ -132,6 +132,8 @@ typedef struct {
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
     int32_t stream_warps;      /* stream kernel: warps (streams) per CTA; 0 = default (2) */
     int32_t eviction;          /* pda_eviction (0 = normal) */
+    int32_t issue_mode;        /* split-K ring refill: 0 = auto, 1 = a producer warp, 2 = each
+                                  consumer warp refills its own stages (always for e4m3) */
     float k_scale;             /* e4m3 cache only: K dequantisation scale (0 = 1.0) */
     float v_scale;             /* e4m3 cache only: V dequantisation scale (0 = 1.0) */
 } pda_options;
@@ -229,7 +231,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 6: e4m3 KV (shape.kv_dtype, options.k/v_scale); 5: EV_AUTO */
+int32_t pda_abi_version(void);  /* 7: options.issue_mode; 6: e4m3 KV; 5: EV_AUTO */
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ PDA_F16, PDA_BF16, PDA_F32, PDA_E4M3 = 0, 1, 2, 3
 PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
 EVICTION = {"normal": 0, "demand_first": 1, "prefetch_last": 2, "both": 3, "auto": 4}
 DEFAULT_EVICTION = "auto"
+ISSUE = {"auto": 0, "producer": 1, "self": 2}
 KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4}
 
 # Product default from the round-1 sweep: line-granular L2 prefetch
@@ -44,7 +45,8 @@ class Shape(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms",
-        "stream_warps", "eviction")] + [("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
+        "stream_warps", "eviction", "issue_mode")] + [("k_scale", ctypes.c_float),
+                                                      ("v_scale", ctypes.c_float)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -132,14 +134,14 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
                  smem_stages=0, kernel="auto", num_sms=0, stream_warps=0,
-                 eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0) -> Options:
+                 eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0, issue_mode=0) -> Options:
     mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
     if prefetch_distance is None:
         prefetch_distance = DEFAULT_DISTANCE if mode else 0
     kern = KERNEL[kernel] if not isinstance(kernel, int) else kernel
     return Options(mode, int(prefetch_distance), int(partition_tokens), int(smem_stages), kern,
-                   int(num_sms), int(stream_warps), int(EVICTION.get(eviction, eviction)), float(k_scale),
-                   float(v_scale))
+                   int(num_sms), int(stream_warps), int(EVICTION.get(eviction, eviction)),
+                   int(ISSUE.get(issue_mode, issue_mode)), float(k_scale), float(v_scale))
 
 
 def plan(shape: Shape, opts: Options) -> dict:
@@ -175,7 +177,7 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
                            num_sms=0, eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0,
-                           workspace=None, stream=None, trace=False):
+                           issue_mode=0, workspace=None, stream=None, trace=False):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16 like q, or
@@ -194,7 +196,7 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     shape = make_shape(q, k_cache, block_tables, out_dtype)
     opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel,
                         num_sms=num_sms, stream_warps=stream_warps, eviction=eviction,
-                        k_scale=k_scale, v_scale=v_scale)
+                        k_scale=k_scale, v_scale=v_scale, issue_mode=issue_mode)
     if scale is None:
         scale = q.shape[-1] ** -0.5
     info = plan(shape, opts)

@@ -35,13 +35,6 @@ struct Geometry {
     static constexpr int kChunks = kSlab / 2048;          // boxes per slab
 };
 
-// Blocks of a unit with n blocks that consumer warp w handles in pair mode.
-__device__ __forceinline__ int j_count_of(int n, int w) {
-    int c = 0;
-    for (int j = 2 * w; j < n; j += 2 * kConsumerWarps) c += (j + 1 < n) ? 2 : 1;
-    return c;
-}
-
 template <bool BF16, int D, int NT, bool KV8>
 struct MathFor {
     using type = BlockMath<BF16, D, NT>;
@@ -51,13 +44,14 @@ struct MathFor<BF16, D, NT, true> {
     using type = BlockMathKV8<BF16, NT>;
 };
 
-// e4m3 caches: no producer warp -- each consumer warp refills the ring stages it
-// owns (4 issuers instead of 1: the 2 KiB slabs need twice the issue rate).
-template <bool KV8>
-constexpr int splitk_block_threads() { return (kConsumerWarps + (KV8 ? 0 : 1)) * 32; }
+// Self-issue mode (always for e4m3 caches): no producer warp -- each consumer
+// warp refills the ring stages it owns (4 issuers instead of 1; the 2 KiB e4m3
+// slabs need twice the issue rate of the 16-bit path).
+template <bool SELF>
+constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) * 32; }
 
-template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8>
-__global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
+template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8, bool SELF>
+__global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
     using G = Geometry<D, KV8>;
@@ -120,14 +114,14 @@ __global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
             mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
         }
         fence_barrier_init();
-        if constexpr (TRACE && KV8) {
+        if constexpr (TRACE && SELF) {
             rec[2] = 0;
             rec[3] = 0;
         }
     }
     __syncthreads();
 
-    if (!KV8 && warp == kConsumerWarps) {
+    if (!SELF && warp == kConsumerWarps) {
         // ============================ producer warp ============================
         if (lane == 0) {
             prefetch_tmap(&tmK);
@@ -186,12 +180,14 @@ __global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
     BM bm;
     bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
     bm.reset();
-    if constexpr (KV8) {
-        // e4m3: a warp takes blocks in pairs (2w, 2w+1 mod 8), runs one softmax
-        // update per pair, and refills the two stages it just read (it owns
-        // every stage s with (s % 8) / 2 == w, so no empty barriers are needed
-        // and a parity wait always refers to the warp's own previous fill).
-        static_assert(STAGES % (2 * kConsumerWarps) == 0, "pairs need STAGES % 8 == 0");
+    if constexpr (SELF) {
+        // A warp takes blocks in groups of PAIR (e4m3: pairs 2w, 2w+1 mod 8 with
+        // one softmax update per pair; 16-bit: j = w mod 4) and refills the
+        // stages it just read: it owns every stage s with (s / PAIR) % 4 == w, so
+        // no empty barriers are needed and a parity wait always refers to the
+        // warp's own previous fill.
+        constexpr int PAIR = KV8 ? 2 : 1;
+        static_assert(STAGES % (PAIR * kConsumerWarps) == 0, "stages must split evenly over the warps");
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;  // <= 32 (validated)
         const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
@@ -235,33 +231,39 @@ __global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
                 ++npf;
             }
         };
-        for (int pos = 2 * warp; pos < STAGES && pos < n; pos += 2 * kConsumerWarps) {
+        for (int pos = PAIR * warp; pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
             issue(pos);
-            if (pos + 1 < n) issue(pos + 1);
+            if (PAIR == 2 && pos + 1 < n) issue(pos + 1);
         }
-        for (int j = 2 * warp; j < n; j += 2 * kConsumerWarps) {
-            const bool two = j + 1 < n;
+        int mine = 0;
+        for (int j = PAIR * warp; j < n; j += PAIR * kConsumerWarps) {
+            const bool two = PAIR == 2 && j + 1 < n;
             const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
             mbar_wait(&full[st0], (j / STAGES) & 1);
             if (two) mbar_wait(&full[st1], ((j + 1) / STAGES) & 1);
             const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
             const int v0 = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
-            if (two) {
-                const int v1 = min(kBlockSize, e_tok - (sb + j + 1) * kBlockSize);
-                bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
+            if constexpr (PAIR == 2) {
+                if (two) {
+                    const int v1 = min(kBlockSize, e_tok - (sb + j + 1) * kBlockSize);
+                    bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
+                } else {
+                    bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                }
             } else {
                 bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
             }
-            // our ldmatrix reads of the two stages are complete (their registers fed
-            // the MMAs above); order them before the async-proxy refills
+            mine += two ? 2 : 1;
+            // our ldmatrix reads of the stages are complete (their registers fed the
+            // MMAs above); order them before the async-proxy refills
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (j + STAGES < n) issue(j + STAGES);
-            if (j + 1 + STAGES < n) issue(j + 1 + STAGES);
+            if (two && j + 1 + STAGES < n) issue(j + 1 + STAGES);
         }
         if constexpr (TRACE) {
             if (lane == 0) {
-                atomicAdd(rec + 2, (j_count_of(n, warp)));
+                atomicAdd(rec + 2, mine);
                 atomicAdd(rec + 3, npf);
             }
         }
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(splitk_block_threads<KV8>(), NT == 1 ? 3 : 2)
         }
     }
 
-    if constexpr (TRACE && KV8) {
+    if constexpr (TRACE && SELF) {
         if (threadIdx.x == 0) {
             rec[0] = s_tok;
             rec[1] = e_tok;
@@ -387,10 +389,10 @@ constexpr size_t smem_bytes_for() {
     return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
 }
 
-template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8 = false>
+template <bool BF16, int D, int NT, int STAGES, bool TRACE, bool KV8 = false, bool SELF = KV8>
 cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                        dim3 grid, cudaStream_t stream) {
-    auto kern = splitk_kernel<BF16, D, NT, STAGES, TRACE, KV8>;
+    auto kern = splitk_kernel<BF16, D, NT, STAGES, TRACE, KV8, SELF>;
     constexpr size_t smem = smem_bytes_for<D, NT, STAGES, KV8>();
     static int configured_device = -1;
     int dev = 0;
@@ -400,17 +402,17 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
         if (e != cudaSuccess) return e;
         configured_device = dev;
     }
-    kern<<<grid, splitk_block_threads<KV8>(), smem, stream>>>(tmK, tmV, p);
+    kern<<<grid, splitk_block_threads<SELF>(), smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();
 }
 
-template <bool BF16, int D, int NT, bool TRACE, bool KV8 = false>
+template <bool BF16, int D, int NT, bool TRACE, bool SELF>
 cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                             int stages, dim3 grid, cudaStream_t s) {
     switch (stages) {
-        case 4: return launch_one<BF16, D, NT, 4, TRACE, KV8>(tmK, tmV, p, grid, s);
-        case 8: return launch_one<BF16, D, NT, 8, TRACE, KV8>(tmK, tmV, p, grid, s);
-        case 12: return launch_one<BF16, D, NT, 12, TRACE, KV8>(tmK, tmV, p, grid, s);
+        case 4: return launch_one<BF16, D, NT, 4, TRACE, false, SELF>(tmK, tmV, p, grid, s);
+        case 8: return launch_one<BF16, D, NT, 8, TRACE, false, SELF>(tmK, tmV, p, grid, s);
+        case 12: return launch_one<BF16, D, NT, 12, TRACE, false, SELF>(tmK, tmV, p, grid, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -420,9 +422,9 @@ cudaError_t dispatch_stages_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, 
                                 int stages, dim3 grid, cudaStream_t s) {
     // 4 KiB stages, consumed in pairs: depth a multiple of 8
     switch (stages) {
-        case 8: return launch_one<BF16, 128, NT, 8, TRACE, true>(tmK, tmV, p, grid, s);
-        case 16: return launch_one<BF16, 128, NT, 16, TRACE, true>(tmK, tmV, p, grid, s);
-        case 24: return launch_one<BF16, 128, NT, 24, TRACE, true>(tmK, tmV, p, grid, s);
+        case 8: return launch_one<BF16, 128, NT, 8, TRACE, true, true>(tmK, tmV, p, grid, s);
+        case 16: return launch_one<BF16, 128, NT, 16, TRACE, true, true>(tmK, tmV, p, grid, s);
+        case 24: return launch_one<BF16, 128, NT, 24, TRACE, true, true>(tmK, tmV, p, grid, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -436,16 +438,19 @@ cudaError_t dispatch_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const S
 
 template <bool BF16, int D, bool TRACE>
 cudaError_t dispatch_nt(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
-                        int n_tiles, int stages, dim3 grid, cudaStream_t s) {
-    return n_tiles == 1 ? dispatch_stages<BF16, D, 1, TRACE>(tmK, tmV, p, stages, grid, s)
-                        : dispatch_stages<BF16, D, 2, TRACE>(tmK, tmV, p, stages, grid, s);
+                        int n_tiles, int stages, dim3 grid, cudaStream_t s, bool self_issue) {
+    if (self_issue)
+        return n_tiles == 1 ? dispatch_stages<BF16, D, 1, TRACE, true>(tmK, tmV, p, stages, grid, s)
+                            : dispatch_stages<BF16, D, 2, TRACE, true>(tmK, tmV, p, stages, grid, s);
+    return n_tiles == 1 ? dispatch_stages<BF16, D, 1, TRACE, false>(tmK, tmV, p, stages, grid, s)
+                        : dispatch_stages<BF16, D, 2, TRACE, false>(tmK, tmV, p, stages, grid, s);
 }
 
 template <bool BF16, bool TRACE>
 cudaError_t dispatch_d(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
-                       int head_dim, int n_tiles, int stages, dim3 grid, cudaStream_t s) {
-    return head_dim == 64 ? dispatch_nt<BF16, 64, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s)
-                          : dispatch_nt<BF16, 128, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s);
+                       int head_dim, int n_tiles, int stages, dim3 grid, cudaStream_t s, bool self_issue) {
+    return head_dim == 64 ? dispatch_nt<BF16, 64, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s, self_issue)
+                          : dispatch_nt<BF16, 128, TRACE>(tmK, tmV, p, n_tiles, stages, grid, s, self_issue);
 }
 
 }  // namespace
@@ -469,11 +474,13 @@ size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8) {
     return 0;
 }
 
-int splitk_threads(bool kv8) { return kv8 ? splitk_block_threads<true>() : splitk_block_threads<false>(); }
+int splitk_threads(bool self_issue) {
+    return self_issue ? splitk_block_threads<true>() : splitk_block_threads<false>();
+}
 
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace, dim3 grid,
-                          cudaStream_t stream, bool kv8) {
+                          cudaStream_t stream, bool kv8, bool self_issue) {
     if (kv8) {
         if (head_dim != 128) return cudaErrorInvalidValue;
         if (bf16)
@@ -483,11 +490,11 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
                      : dispatch_kv8<false, false>(tmK, tmV, p, n_tiles, stages, grid, stream);
     }
     if (bf16) {
-        return trace ? dispatch_d<true, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
-                     : dispatch_d<true, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);
+        return trace ? dispatch_d<true, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream, self_issue)
+                     : dispatch_d<true, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream, self_issue);
     }
-    return trace ? dispatch_d<false, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream)
-                 : dispatch_d<false, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream);
+    return trace ? dispatch_d<false, true>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream, self_issue)
+                 : dispatch_d<false, false>(tmK, tmV, p, head_dim, n_tiles, stages, grid, stream, self_issue);
 }
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream) {

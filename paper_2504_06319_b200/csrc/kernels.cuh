@@ -100,9 +100,9 @@ struct CombineParams {
 // Host launchers (return the launch's cudaError_t).
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace,
-                          dim3 grid, cudaStream_t stream, bool kv8 = false);
+                          dim3 grid, cudaStream_t stream, bool kv8 = false, bool self_issue = false);
 size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8 = false);
-int splitk_threads(bool kv8 = false);
+int splitk_threads(bool self_issue = false);
 
 cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, int warps, bool trace,

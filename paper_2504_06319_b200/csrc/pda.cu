@@ -42,6 +42,10 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         (s->head_dim != 128 || (o && o->kernel != PDA_KERNEL_AUTO && o->kernel != PDA_KERNEL_SPLITK)))
         return PDA_ERR_UNSUPPORTED;
     if (o && (!(o->k_scale >= 0.f) || !(o->v_scale >= 0.f))) return PDA_ERR_SHAPE;
+    if (o && (o->issue_mode < 0 || o->issue_mode > 2)) return PDA_ERR_SHAPE;
+    if (o && s->kv_dtype == PDA_E4M3 && o->issue_mode == 1) return PDA_ERR_UNSUPPORTED;
+    if (o && o->issue_mode == 2 && o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32)
+        return PDA_ERR_UNSUPPORTED;  // self-issue block-id window reaches 32 blocks ahead
     if (s->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
     if (s->num_q_heads / s->num_kv_heads > 16) return PDA_ERR_UNSUPPORTED;
     if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_LINE_L2) return PDA_ERR_SHAPE;
@@ -68,6 +72,13 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         return PDA_ERR_UNSUPPORTED;
     }
     return PDA_OK;
+}
+
+// Split-K ring refill mode: e4m3 always self-issues; 16-bit follows issue_mode
+// (auto = the producer warp).
+bool self_issue(const pda_shape* s, const pda_options* o) {
+    if (s->kv_dtype == PDA_E4M3) return true;
+    return o->issue_mode == 2;
 }
 
 pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
@@ -180,7 +191,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->grid_x = (int32_t)p_max;
     pl->grid_y = Hkv;
     pl->grid_z = B;
-    pl->threads = pda::splitk_threads(s->kv_dtype == PDA_E4M3);
+    pl->threads = pda::splitk_threads(self_issue(s, o));
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
     pl->workspace_bytes =
@@ -381,7 +392,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     const int n_tiles = p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,
-                             dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream, kv8);
+                             dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream, kv8, self_issue(s, o));
     if (err != cudaSuccess) return PDA_ERR_CUDA;
     if (pl.p_max > 1) {
         // S8 as its own small kernel: measured faster than merging in the last
@@ -501,6 +512,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 6; }
+int32_t pda_abi_version(void) { return 7; }
 
 }  // extern "C"

@@ -58,7 +58,8 @@ class TPDecodeAttention:
                                 torch.empty((num_seqs, max_blocks), dtype=torch.int32, device="meta"))
         opt = _lib.make_options(**{k: v for k, v in opts.items()
                                    if k in ("prefetch", "prefetch_distance", "partition_tokens",
-                                            "smem_stages", "kernel", "stream_warps", "eviction")})
+                                            "smem_stages", "kernel", "stream_warps", "eviction",
+                                            "issue_mode")})
         self.plan = _lib.plan(shape, opt)
         wsb = self.plan["workspace_bytes"]
         self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)  # stream tickets start at 0

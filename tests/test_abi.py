@@ -50,7 +50,7 @@ def shape(**kw):
 
 def opts(**kw):
     d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0,
-             stream_warps=0, eviction=0, k_scale=0.0, v_scale=0.0)
+             stream_warps=0, eviction=0, issue_mode=0, k_scale=0.0, v_scale=0.0)
     d.update(kw)
     return _lib.Options(**d)
 
@@ -96,6 +96,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=3, prefetch_distance=32), 0),
     (dict(eviction=5), 2),
     (dict(k_scale=-1.0), 2),
+    (dict(issue_mode=3), 2),
+    (dict(issue_mode=2), 0),
     (dict(eviction=4), 0),
     (dict(eviction=3), 0),
 ])
@@ -208,7 +210,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 6
+    assert pda.lib().pda_abi_version() == 7
 
 
 def test_product_never_imports_oracle():

@@ -63,6 +63,8 @@ SHAPES = [
 KERNELS = [dict(kernel="splitk"), dict(kernel="splitk", partition_tokens=16),
            dict(kernel="splitk", partition_tokens=64), dict(kernel="splitk", smem_stages=4),
            dict(kernel="splitk", smem_stages=12, partition_tokens=256), dict(kernel="paper"),
+           dict(kernel="splitk", issue_mode="self"), dict(kernel="splitk", issue_mode="self", smem_stages=4,
+                                                          partition_tokens=48),
            dict(kernel="stream"), dict(kernel="stream", smem_stages=8, stream_warps=1),
            dict(kernel="stream", smem_stages=4, stream_warps=2),
            dict(kernel="stream", smem_stages=4, stream_warps=4),
@@ -173,13 +175,14 @@ def test_split_sizes_agree(pda, oracle_mod):
         assert max_err(o, ref) <= 5e-4  # fp32 out: only P / accumulation rounding remains
 
 
-def test_trace_splitk_matches_oracle_plan(pda, oracle_mod):
+@pytest.mark.parametrize("issue", ["producer", "self"])
+def test_trace_splitk_matches_oracle_plan(pda, oracle_mod, issue):
     cfg = synth.Config("trace", 3, 8, 2, 64, (37, 256, 0), "fp16", poison_blocks=3)
     dev = to_dev(synth.make_inputs(cfg, seed=1))
     for P in (16, 64, 128, 0):
-        for mode, d in (("off", 0), ("bulk", 1), ("bulk", 3), ("line", 4), ("bulk", 40)):
+        for mode, d in (("off", 0), ("bulk", 1), ("bulk", 3), ("line", 4), ("bulk", 30 if issue == "self" else 40)):
             _, tr, info = gpu(pda, dev, kernel="splitk", partition_tokens=P, prefetch=mode,
-                              prefetch_distance=d or None, trace=True)
+                              prefetch_distance=d or None, trace=True, issue_mode=issue)
             ref = oracle_mod.plan_splitk(dev["block_tables"], dev["context_lens"], cfg.num_kv_heads, 16,
                                          info["partition_tokens"], info["p_max"], d)
             got = tr.cpu().numpy().reshape(ref.shape)
