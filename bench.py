@@ -292,7 +292,8 @@ def main():
             # prefetch ablation arms on the same inputs, interleaved step by step
             # (A B A B ...) with per-step CUDA events, medians per arm
             arms = {
-                "on": step_main,
+                "on": make_step(**{**opt_kw, "prefetch": "line", "prefetch_distance": 4}),
+                "bulk": make_step(**{**opt_kw, "prefetch": "bulk", "prefetch_distance": 4}),
                 "off": make_step(**{**opt_kw, "prefetch": "off"}),
                 "paper_on": make_step(kernel="paper", prefetch="bulk", prefetch_distance=4),
                 "paper_off": make_step(kernel="paper", prefetch="off"),
@@ -315,6 +316,9 @@ def main():
                 "prefetch_on_us": med["on"],
                 "prefetch_off_us": med["off"],
                 "prefetch_speedup": med["off"] / med["on"],
+                "prefetch_on_desc": "same kernel + prefetch.global.L2 line prefetch 4 blocks ahead",
+                "prefetch_bulk_us": med["bulk"],
+                "prefetch_bulk_speedup": med["off"] / med["bulk"],
                 "paper_kernel": {
                     "prefetch_on_us": med["paper_on"],
                     "prefetch_off_us": med["paper_off"],
@@ -323,6 +327,24 @@ def main():
                 },
                 "arms_timing": f"{n_rep} interleaved steps per arm, per-step CUDA events, median",
             }
+            # FP8 (e4m3) KV-cache variant of the same step
+            if cfg.head_dim == 128:
+                q8 = synth.quantize_kv_e4m3(inp)
+                ws8 = torch.zeros(max(1, pda.workspace_bytes(
+                    pda.make_shape(q, q8["k_cache"], bt), pda.make_options(**opt_kw))), dtype=torch.uint8,
+                    device="cuda")
+
+                def kv8_step(q_, bt_, lens_, scale_):
+                    pda.paged_decode_attention(q_, q8["k_cache"], q8["v_cache"], bt_, lens_, scale_,
+                                               out=step_main.out_local, workspace=ws8, k_scale=q8["k_scale"],
+                                               v_scale=q8["v_scale"], **opt_kw)
+                ms8 = time_steps(kv8_step, max(10, args.steps // 2), 2)
+                b8 = cfg.kv_bytes() // 2 + cfg.other_bytes()
+                extras["e4m3_kv"] = {"us_per_step": ms8 * 1e3, "speedup_vs_16bit": ms / ms8,
+                                     "algorithmic_gbs": b8 / (ms8 * 1e-3) / 1e9 * world,
+                                     "tokens_per_s": cfg.num_seqs / (ms8 * 1e-3),
+                                     "desc": "K/V as OCP e4m3 codes + per-tensor scales, 1 B/element"}
+                del q8, ws8
             # in-run read roofline (read-only stream over a 4 GiB buffer)
             buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
             sink = torch.zeros(4, dtype=torch.int32, device="cuda")
@@ -393,6 +415,7 @@ def main():
             "prefetch_distance": opt_kw.get("prefetch_distance", pda._lib.DEFAULT_DISTANCE),
             "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
             "eviction": ["normal", "demand_first", "prefetch_last", "both"][pl["eviction"]],
+            "issue": "self (consumer warps refill their ring stages)" if pl["threads"] == 128 else "producer warp",
             "p_max": pl["p_max"],
             "l2": f"no flush: inputs larger than L2 ({cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)",
             "bytes_per_step": total_bytes,

@@ -132,8 +132,9 @@ typedef struct {
     int32_t num_sms;           /* SMs the planner assumes; 0 = 148 (B200) */
     int32_t stream_warps;      /* stream kernel: warps (streams) per CTA; 0 = default (2) */
     int32_t eviction;          /* pda_eviction (0 = normal) */
-    int32_t issue_mode;        /* split-K ring refill: 0 = auto, 1 = a producer warp, 2 = each
-                                  consumer warp refills its own stages (always for e4m3) */
+    int32_t issue_mode;        /* split-K ring refill: 0 = auto (= 2), 1 = a producer warp, 2 = each
+                                  consumer warp refills its own stages (always for e4m3);
+                                  self-issue limits prefetch_distance to 32 */
     float k_scale;             /* e4m3 cache only: K dequantisation scale (0 = 1.0) */
     float v_scale;             /* e4m3 cache only: V dequantisation scale (0 = 1.0) */
 } pda_options;

@@ -23,10 +23,12 @@ DEFAULT_EVICTION = "auto"
 ISSUE = {"auto": 0, "producer": 1, "self": 2}
 KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4}
 
-# Product default from the round-1 sweep: line-granular L2 prefetch
-# (prefetch.global.L2) 4 blocks ahead; neutral-to-positive for the TMA kernel, while
-# the bulk form (UBLKPF) competes with the TMA loads for the same unit.
-DEFAULT_PREFETCH = "line"
+# Product defaults from the round-1 measurements: the TMA ring
+# already fetches S blocks ahead into shared memory while the current block is
+# computed, so the extra L2 prefetch (the paper's instruction, or per-line) is
+# measured 0-9 % slower on every cell with self-issuing consumers -> off by
+# default; "line" / "bulk" with a distance remain the ablation switch.
+DEFAULT_PREFETCH = "off"
 DEFAULT_DISTANCE = 4
 
 

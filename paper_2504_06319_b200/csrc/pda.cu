@@ -44,7 +44,8 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     if (o && (!(o->k_scale >= 0.f) || !(o->v_scale >= 0.f))) return PDA_ERR_SHAPE;
     if (o && (o->issue_mode < 0 || o->issue_mode > 2)) return PDA_ERR_SHAPE;
     if (o && s->kv_dtype == PDA_E4M3 && o->issue_mode == 1) return PDA_ERR_UNSUPPORTED;
-    if (o && o->issue_mode == 2 && o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32)
+    if (o && o->issue_mode != 1 && (o->kernel == PDA_KERNEL_AUTO || o->kernel == PDA_KERNEL_SPLITK) &&
+        o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32)
         return PDA_ERR_UNSUPPORTED;  // self-issue block-id window reaches 32 blocks ahead
     if (s->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
     if (s->num_q_heads / s->num_kv_heads > 16) return PDA_ERR_UNSUPPORTED;
@@ -74,11 +75,11 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
     return PDA_OK;
 }
 
-// Split-K ring refill mode: e4m3 always self-issues; 16-bit follows issue_mode
-// (auto = the producer warp).
+// Split-K ring refill mode: e4m3 always self-issues; 16-bit follows issue_mode,
+// auto = self-issue (equal on C2, +1-3 % on GQA / ragged cells).
 bool self_issue(const pda_shape* s, const pda_options* o) {
     if (s->kv_dtype == PDA_E4M3) return true;
-    return o->issue_mode == 2;
+    return o->issue_mode != 1;
 }
 
 pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {

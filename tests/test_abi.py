@@ -88,7 +88,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=4, prefetch_distance=33), 3),
     (dict(kernel=5), 2),
     (dict(kernel=7), 2),
-    (dict(kernel=2, prefetch_distance=400), 0),
+    (dict(kernel=2, prefetch_distance=400), 3),          # self-issue window: d <= 32
+    (dict(kernel=2, prefetch_distance=400, issue_mode=1), 0),
     (dict(kernel=3), 0),
     (dict(kernel=3, smem_stages=6, stream_warps=2), 0),
     (dict(kernel=3, smem_stages=12), 3),
@@ -139,7 +140,8 @@ def test_plan_no_split_llama2():
               max_blocks_per_seq=256)
     p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 1 and p["partition_tokens"] == 4096 and p["workspace_bytes"] == 0
-    assert (p["grid_x"], p["grid_y"], p["grid_z"]) == (1, 32, 64) and p["threads"] == 160
+    assert (p["grid_x"], p["grid_y"], p["grid_z"]) == (1, 32, 64) and p["threads"] == 128  # self-issue
+    assert pda.plan(s, opts(kernel=2, issue_mode=1))["threads"] == 160  # + producer warp
     assert p["trace_rec_len"] == 4 + 2 * 256 and p["trace_records"] == 64 * 32
 
 
