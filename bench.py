@@ -225,9 +225,16 @@ def main():
     import synth
     from paper_2504_06319_b200.tp import TPDecodeAttention
 
-    torch.cuda.set_device(local)
+    # PDA_BENCH_SHARE_GPU=1 (testing only): ranks share the visible GPUs round-robin
+    # and use gloo, so the multi-rank path can be exercised on a 1-GPU box
+    share = os.environ.get("PDA_BENCH_SHARE_GPU") == "1"
+    dev_index = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
     pda.lib()
 
     cfg = workload_config(args.config)
@@ -276,7 +283,7 @@ def main():
         barrier()
         ms = e0.elapsed_time(e1) / steps
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -285,7 +292,7 @@ def main():
     local_bytes = algorithmic_bytes(local_cfg)
     peak, peak_src = load_peaks()
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         ms = time_steps(step_main, args.steps, args.warmup)
         extras = {}
         if not args.no_extras:

@@ -31,7 +31,13 @@ def gather_heads(out_local: torch.Tensor, group=None, gathered: torch.Tensor | N
     B, hl, D = out_local.shape
     if gathered is None:
         gathered = torch.empty((world * B, hl, D), dtype=out_local.dtype, device=out_local.device)
-    dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group)
+    if out_local.is_cuda and dist.get_backend(group) == "gloo":
+        # testing path (several ranks sharing one GPU): gloo gathers host tensors
+        host = torch.empty(gathered.shape, dtype=gathered.dtype)
+        dist.all_gather_into_tensor(host, out_local.cpu(), group=group)
+        gathered.copy_(host)
+    else:
+        dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group)
     return gathered.view(world, B, hl, D).permute(1, 0, 2, 3)
 
 
