@@ -40,6 +40,13 @@ def variants(quick):
     for d in ([4] if quick else [1, 2, 4, 8, 16]):
         vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=d))
     vs.append(dict(kernel="paper", prefetch="line", prefetch_distance=4))
+    # 16-bit split-K with the producer-warp refill (the alternative to self-issue)
+    vs.append(dict(kernel="splitk", smem_stages=8, prefetch="off", issue_mode="producer"))
+    vs.append(dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4, issue_mode="producer"))
+    # e4m3 KV cache (NEXT f3)
+    for st in (8, 16):
+        vs.append(dict(kernel="splitk", smem_stages=st, prefetch="off", kv="e4m3"))
+        vs.append(dict(kernel="splitk", smem_stages=st, prefetch="line", prefetch_distance=4, kv="e4m3"))
     # eviction priority: demand evict_first / prefetch evict_last / both
     for ev in (1, 2, 3):
         vs.append(dict(kernel="paper", prefetch="bulk", prefetch_distance=4, eviction=ev))
@@ -84,6 +91,7 @@ def main():
         if keep and cfg.name not in keep:
             continue
         inp = synth.make_inputs(cfg, seed=5, device="cuda")
+        inp8 = synth.quantize_kv_e4m3(inp)
         kvb = cfg.kv_bytes()
         total = kvb + cfg.other_bytes()
         vs = variants(a.quick)
@@ -101,10 +109,15 @@ def main():
             for i, v in enumerate(vs):
 
                 def run(v=v, i=i):
-                    return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"],
-                                                      inp["block_tables"], inp["context_lens"],
-                                                      inp["scale"], out=outs.get(i),
-                                                      workspace=wss[v["kernel"]], **v)
+                    kw = {k: x for k, x in v.items() if k != "kv"}
+                    src = inp
+                    if v.get("kv") == "e4m3":
+                        src = inp8
+                        kw.update(k_scale=inp8["k_scale"], v_scale=inp8["v_scale"])
+                    return pda.paged_decode_attention(src["q"], src["k_cache"], src["v_cache"],
+                                                      src["block_tables"], src["context_lens"],
+                                                      src["scale"], out=outs.get(i),
+                                                      workspace=wss[v["kernel"]], **kw)
                 if rnd == 0:
                     outs[i] = run()
                     if not a.no_graphs:
@@ -129,19 +142,21 @@ def main():
             base = next(j for j, w in enumerate(vs) if w["kernel"] == v["kernel"]
                         and w.get("smem_stages") == v.get("smem_stages")
                         and w.get("stream_warps") == v.get("stream_warps") and w["prefetch"] == "off"
-                        and not w.get("eviction"))
+                        and not w.get("eviction") and w.get("kv") == v.get("kv")
+                        and w.get("issue_mode") == v.get("issue_mode"))
             us = statistics.median(times[i])
+            tot_v = (kvb // 2 + cfg.other_bytes()) if v.get("kv") == "e4m3" else total
             rec = dict(cell=cfg.name, batch=cfg.num_seqs, ctx=max(cfg.context_lens),
                        q_heads=cfg.num_q_heads, kv_heads=cfg.num_kv_heads, dtype=cfg.dtype,
                        kv_bytes=kvb, **v, us_median=us, us_p10=sorted(times[i])[len(times[i]) // 10],
-                       us_p90=sorted(times[i])[(9 * len(times[i])) // 10], gbs=total / (us * 1e-6) / 1e9,
+                       us_p90=sorted(times[i])[(9 * len(times[i])) // 10], gbs=tot_v / (us * 1e-6) / 1e9,
                        speedup_vs_off=statistics.median(times[base]) / us,
                        bitwise_equal_to_off=bool(torch.equal(outs[i], outs[base])),
                        timing="cuda_graph_replay" if not a.no_graphs else "direct_call")
             f.write(json.dumps(rec) + "\n")
             f.flush()
             print(json.dumps(rec), flush=True)
-        del inp, wss, outs, graphs
+        del inp, inp8, wss, outs, graphs
         torch.cuda.empty_cache()
 
 
