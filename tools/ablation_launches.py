@@ -18,11 +18,13 @@ VARIANTS = [
     dict(kernel="paper", prefetch="off"),
     dict(kernel="paper", prefetch="bulk", prefetch_distance=4),
     dict(kernel="paper", prefetch="line", prefetch_distance=4),
-    dict(kernel="splitk", smem_stages=4, prefetch="off"),
-    dict(kernel="splitk", smem_stages=4, prefetch="line", prefetch_distance=4),
+    dict(kernel="splitk", smem_stages=8, prefetch="off", issue_mode="producer"),
+    dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4, issue_mode="producer"),
     dict(kernel="splitk", smem_stages=8, prefetch="off"),
     dict(kernel="splitk", smem_stages=8, prefetch="bulk", prefetch_distance=4),
     dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4),
+    dict(kernel="splitk", smem_stages=16, prefetch="off", kv="e4m3"),
+    dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4, kv="e4m3"),
 ]
 
 
@@ -38,12 +40,18 @@ def main():
     from bench import workload_config
     cfg = workload_config(a.config)
     inp = synth.make_inputs(cfg, seed=5, device="cuda")
-    ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    inp8 = synth.quantize_kv_e4m3(inp)
+    ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
     order = []
     for v in VARIANTS:
+        kw = {k: x for k, x in v.items() if k != "kv"}
+        src = inp
+        if v.get("kv") == "e4m3":
+            src = inp8
+            kw.update(k_scale=inp8["k_scale"], v_scale=inp8["v_scale"])
         for rep in range(2):
-            pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
-                                       inp["context_lens"], inp["scale"], workspace=ws, **v)
+            pda.paged_decode_attention(src["q"], src["k_cache"], src["v_cache"], src["block_tables"],
+                                       src["context_lens"], src["scale"], workspace=ws, **kw)
             order.append(dict(v, rep=rep))
     torch.cuda.synchronize()
     with open(os.path.join(ROOT, "gpurun_out", f"ablation_order_{a.config}.json"), "w") as f:

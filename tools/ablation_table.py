@@ -30,6 +30,10 @@ def label(v):
     s = v["kernel"]
     if v["kernel"] == "splitk":
         s += f" S{v['smem_stages']}"
+        if v.get("issue_mode"):
+            s += f" {v['issue_mode']}"
+        if v.get("kv"):
+            s += f" {v['kv']}"
     s += " " + v["prefetch"]
     if v["prefetch"] != "off":
         s += f" d{v['prefetch_distance']}"
@@ -88,6 +92,7 @@ def main():
         sp = []
         for (c, m), d in zip(cols, d0):
             fam = c.rsplit(" ", 2)[0] if (" bulk" in c or " line" in c) else c.rsplit(" ", 1)[0]
+            fam = fam.replace(" S16", "").replace(" S8", "")
             if c.endswith(" off"):
                 base[fam] = d
             sp.append(f"{base.get(fam, d) / d:.3f}x")
