@@ -65,6 +65,9 @@ def lib():
             L.oracle_paged_attention_kv8.argtypes = [p, i32, p, p, f64, f64, p, p, i32, i32, i32, i32,
                                                      i32, i32, f64, p, p, i64, i32]
             L.oracle_paged_attention_kv8.restype = i32
+            L.oracle_paged_attention_mq.argtypes = [p, p, p, i32, p, p, i32, i32, i32, i32, i32, i32,
+                                                    i32, f64, p, i32]
+            L.oracle_paged_attention_mq.restype = i32
             L.oracle_eq1_block_bytes.argtypes = [i64, i64, i64]
             L.oracle_eq1_block_bytes.restype = i64
             L.oracle_eq2_total_bytes.argtypes = [i64, i64, i64, i64]
@@ -201,6 +204,22 @@ def paged_attention_kv8(q, k_cache, v_cache, k_scale: float, v_scale: float, blo
         int(nthreads))
     if rc != 0:
         raise ValueError("oracle_paged_attention_kv8: invalid arguments")
+    return out
+
+
+def paged_attention_mq(q, k_cache, v_cache, block_tables, context_lens, scale: float, dtype: str,
+                       nthreads: int = 0) -> np.ndarray:
+    """Multi-token causal decode: q [B, q_len, Hq, D] -> out [B, q_len, Hq, D] fp64."""
+    qa, ka, va = _u16(q), _u16(k_cache), _u16(v_cache)
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    B, q_len, Hq, D = qa.shape
+    _, Hkv, bs, _ = ka.shape
+    out = np.full((B, q_len, Hq, D), np.nan, dtype=np.float64)
+    rc = lib().oracle_paged_attention_mq(_ptr(qa), _ptr(ka), _ptr(va), DTYPES[dtype], _ptr(bt), _ptr(lens), B,
+                                         q_len, Hq, Hkv, D, bs, bt.shape[1], float(scale), _ptr(out),
+                                         int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_paged_attention_mq: invalid arguments")
     return out
 
 

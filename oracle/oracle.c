@@ -24,6 +24,9 @@
  *   oracle_e4m3_to_f64       pinned: torch float8_e4m3fn decode, all 256 codes.
  *   oracle_paged_attention_kv8 pinned: numpy softmax attention on the
  *                            dequantised contiguous gather, closed forms.
+ *   oracle_paged_attention_mq pinned: numpy causal attention on contiguous
+ *                            gathers (explicit causal mask), q_len = 1 ==
+ *                            oracle_paged_attention bitwise.
  *   oracle_plan_splitk       pinned: hand-computed ranges, Alg. 1 guard
  *                            counts, brute-force plan.
  *   oracle_plan_paper        pinned: Alg. 1 guard counts, hand examples.
@@ -249,6 +252,43 @@ int oracle_paged_attention_kv8(const uint16_t* q, int q_dtype, const uint8_t* k,
         free(w);
     }
     return 0;
+}
+
+/* Multi-token (speculative) decode: q_len query tokens per
+ * sequence, q [B, q_len, Hq, D] -> out [B, q_len, Hq, D].  context_lens[b] = L
+ * counts the q_len new tokens, whose K/V are already in the cache; query token
+ * i sits at position L - q_len + i and attends causally to tokens
+ * [0, L - q_len + i], i.e. it is the single-query definition with context
+ * length L_i = L - q_len + i + 1 (L_i <= 0 gives a zero row).  This function
+ * evaluates exactly that: for each (b, i) it calls the single-query
+ * definition on the sequence truncated to L_i. */
+int oracle_paged_attention_mq(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                              const int32_t* bt, const int32_t* lens, int B, int q_len, int Hq,
+                              int Hkv, int D, int bs, int max_blocks, double scale, double* out,
+                              int nthreads) {
+    if (q_len <= 0) return -1;
+    int32_t* li = (int32_t*)malloc(sizeof(int32_t) * (B > 0 ? B : 1));
+    int32_t* bti = (int32_t*)malloc(sizeof(int32_t) * (size_t)(B > 0 ? B : 1) * (max_blocks > 0 ? max_blocks : 1));
+    uint16_t* qi = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(B > 0 ? B : 1) * Hq * D);
+    double* oi = (double*)malloc(sizeof(double) * (size_t)(B > 0 ? B : 1) * Hq * D);
+    int rc = 0;
+    for (int i = 0; i < q_len && rc == 0; ++i) {
+        for (int b = 0; b < B; ++b) {
+            int L = lens[b] - q_len + i + 1;
+            li[b] = L > 0 ? L : 0;
+            for (int j = 0; j < max_blocks; ++j) bti[(size_t)b * max_blocks + j] = bt[(size_t)b * max_blocks + j];
+            memcpy(qi + (size_t)b * Hq * D, q + (((size_t)b * q_len + i) * Hq) * D, sizeof(uint16_t) * Hq * D);
+        }
+        rc = oracle_paged_attention(qi, k, v, dtype, bti, li, B, Hq, Hkv, D, bs, max_blocks, scale, oi,
+                                    NULL, 0, nthreads);
+        for (int b = 0; b < B; ++b)
+            memcpy(out + (((size_t)b * q_len + i) * Hq) * D, oi + (size_t)b * Hq * D, sizeof(double) * Hq * D);
+    }
+    free(li);
+    free(bti);
+    free(qi);
+    free(oi);
+    return rc;
 }
 
 int oracle_max_threads(void) {

@@ -173,6 +173,20 @@ def make_inputs(cfg: Config, seed: int = 0, device="cpu", poison: bool = True,
                 scale=1.0 / math.sqrt(D), cfg=cfg)
 
 
+def with_query_tokens(inputs: dict, q_len: int, seed: int = 0) -> dict:
+    """Multi-token (speculative) decode variant: q becomes [B, q_len, Hq, D]
+    (fresh U(-1, 1) draws, same dtype/device); context_lens keep counting the
+    new tokens, whose K/V are already in the cache."""
+    q = inputs["q"]
+    g = torch.Generator(device=q.device).manual_seed(seed + 77) if q.is_cuda else torch.Generator().manual_seed(seed + 77)
+    B, Hq, D = q.shape
+    x = torch.rand((B, q_len, Hq, D), generator=g, device=q.device, dtype=torch.float32).mul_(2).sub_(1)
+    out = dict(inputs)
+    out["q"] = x.to(q.dtype)
+    out["q_len"] = q_len
+    return out
+
+
 def quantize_kv_e4m3(inputs: dict, k_scale: float = 1.0 / 224, v_scale: float = 1.0 / 224) -> dict:
     """FP8 KV-cache variant of `inputs`: K and V stored as
     OCP e4m3 codes (uint8) of x / scale with per-tensor scales, NaN poison kept

@@ -377,3 +377,62 @@ def test_kv8_context_one_is_scaled_v_row(oracle_mod):
     codes = inp["v_cache"][int(inp["block_tables"][0, 0]), 0, 0]
     vrow = codes.view(torch.float8_e4m3fn).double().numpy() * 0.125
     assert np.array_equal(out[0, 0], vrow) and np.array_equal(out[0, 1], vrow)
+
+
+# ---- multi-token (speculative) decode --------------------
+
+def causal_reference(inp, b, i, h):
+    """numpy: query token i of sequence b at position L - q_len + i attends to
+    tokens t <= that position (explicit causal mask over the contiguous gather)."""
+    cfg = inp["cfg"]
+    q_len = inp["q_len"]
+    g = cfg.num_q_heads // cfg.num_kv_heads
+    L = int(inp["context_lens"][b])
+    bs = cfg.block_size
+    k = inp["k_cache"].double().numpy()
+    v = inp["v_cache"].double().numpy()
+    bt = inp["block_tables"].numpy()
+    pos = L - q_len + i
+    if pos < 0:
+        return np.zeros(cfg.head_dim)
+    K = np.stack([k[bt[b, t // bs], h // g, t % bs] for t in range(L)])
+    V = np.stack([v[bt[b, t // bs], h // g, t % bs] for t in range(L)])
+    s = inp["scale"] * (K @ inp["q"].double().numpy()[b, i, h])
+    s[np.arange(L) > pos] = -np.inf
+    w = np.exp(s - s.max())
+    return (w / w.sum()) @ V
+
+
+@pytest.mark.parametrize("q_len", [1, 2, 4])
+def test_mq_oracle_vs_causal_numpy(oracle_mod, q_len):
+    cfg = synth.Config("mq", 3, 8, 2, 64, (37, 2, 70), "fp16", poison_blocks=2)
+    inp = synth.with_query_tokens(synth.make_inputs(cfg, seed=5), q_len)
+    out = oracle_mod.paged_attention_mq(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                        inp["context_lens"], inp["scale"], "fp16")
+    assert np.isfinite(out).all()
+    for b in range(3):
+        for i in range(q_len):
+            for h in range(8):
+                np.testing.assert_allclose(out[b, i, h], causal_reference(inp, b, i, h), rtol=0, atol=1e-12)
+
+
+def test_mq_len_one_is_single_query_bitwise(oracle_mod):
+    inp = synth.make_inputs(synth.C1_TINY, seed=3)
+    one = oracle_mod.paged_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                     inp["context_lens"], inp["scale"], "fp16")
+    mq = oracle_mod.paged_attention_mq(inp["q"][:, None], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                       inp["context_lens"], inp["scale"], "fp16")
+    assert np.array_equal(mq[:, 0], one)
+
+
+def test_mq_last_token_sees_everything_first_token_sees_prefix(oracle_mod):
+    """token q_len-1 == single-query over L tokens; token 0 == single-query over L-q_len+1."""
+    cfg = synth.Config("mq2", 2, 4, 4, 64, (40, 19), "bf16")
+    inp = synth.with_query_tokens(synth.make_inputs(cfg, seed=6), 3)
+    mq = oracle_mod.paged_attention_mq(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                       inp["context_lens"], inp["scale"], "bf16")
+    last = oracle_mod.paged_attention(inp["q"][:, 2], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                      inp["context_lens"], inp["scale"], "bf16")
+    first = oracle_mod.paged_attention(inp["q"][:, 0], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                       inp["context_lens"] - 2, inp["scale"], "bf16")
+    assert np.array_equal(mq[:, 2], last) and np.array_equal(mq[:, 0], first)
