@@ -114,6 +114,11 @@ typedef struct {
     int32_t kv_dtype;           /* pda_dtype of k_cache / v_cache: == dtype, or PDA_E4M3 (1 byte per
                                    element; value = k_scale|v_scale * e4m3(code); head_dim 128 and the
                                    split-K kernel only; a bf16 q is converted to fp16 for the MMAs) */
+    int32_t q_len;              /* query tokens per sequence (0 or 1 = single-token decode).  > 1:
+                                   multi-token (speculative) decode, q and out are [B, q_len, Hq, D],
+                                   context_lens counts the q_len new tokens (already in the cache) and
+                                   query token i attends to tokens [0, L - q_len + i]; split-K kernel
+                                   only, q_len * (Hq / Hkv) <= 16 */
 } pda_shape;
 
 typedef struct {
@@ -232,7 +237,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 7: options.issue_mode; 6: e4m3 KV; 5: EV_AUTO */
+int32_t pda_abi_version(void);  /* 8: shape.q_len; 7: issue_mode; 6: e4m3 KV; 5: EV_AUTO */
 
 #ifdef __cplusplus
 }

@@ -41,7 +41,7 @@ class PdaError(RuntimeError):
 class Shape(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "num_seqs", "num_q_heads", "num_kv_heads", "head_dim", "block_size", "num_blocks",
-        "max_blocks_per_seq", "dtype", "out_dtype", "kv_dtype")]
+        "max_blocks_per_seq", "dtype", "out_dtype", "kv_dtype", "q_len")]
 
 
 class Options(ctypes.Structure):
@@ -126,12 +126,17 @@ def _dtype_code(dt) -> int:
 
 
 def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
-    B, Hq, D = q.shape
+    """q [B, Hq, D] (single-token decode) or [B, q_len, Hq, D] (multi-token)."""
+    q_len = 1
+    if q.dim() == 4:
+        B, q_len, Hq, D = q.shape
+    else:
+        B, Hq, D = q.shape
     nb, Hkv, bs, D2 = k_cache.shape
     if D2 != D:
         raise ValueError("q and k_cache head_dim differ")
     return Shape(B, Hq, Hkv, D, bs, nb, block_tables.shape[1], _dtype_code(q.dtype),
-                 _dtype_code(out_dtype if out_dtype is not None else q.dtype), _dtype_code(k_cache.dtype))
+                 _dtype_code(out_dtype if out_dtype is not None else q.dtype), _dtype_code(k_cache.dtype), q_len)
 
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,

@@ -105,6 +105,10 @@ struct BlockMath {
     float acc[MT][NT][4];        // O^T accumulators: (d = 16i + lane/4 + 8(r/2), h = 2(lane%4) + r%2)
     float m_run[NT][2];          // running max per head column (log2 domain)
     float l_run[NT][2];          // per-lane partial row sums (reduced at the end)
+    // multi-token decode: column (query token i, head) of this lane may see
+    // tokens < L - qoff, qoff = q_len - 1 - i; qm1 = q_len - 1 (0 = single query)
+    int qoff[NT][2] = {};
+    int qm1 = 0;
 
     __device__ __forceinline__ void reset() {
 #pragma unroll
@@ -117,6 +121,37 @@ struct BlockMath {
         for (int nt = 0; nt < NT; ++nt) {
             m_run[nt][0] = m_run[nt][1] = -INFINITY;
             l_run[nt][0] = l_run[nt][1] = 0.f;
+        }
+    }
+
+    // Columns = (query token i, head h) pairs, c = i * g + h, c < q_len * g.
+    __device__ __forceinline__ void set_q_tokens(int q_len, int g, int lane) {
+        qm1 = q_len - 1;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = nt * 8 + 2 * (lane & 3) + c;
+                qoff[nt][c] = col < q_len * g ? q_len - 1 - col / g : 0;
+            }
+    }
+
+    // q rows of the columns (token i, head h) of kv head kvh of sequence b
+    // (q [B, q_len, Hq, D]); padded columns are zero.
+    __device__ __forceinline__ void load_q_tokens(const uint16_t* q, int b, int kvh, int Hq, int q_len, int g,
+                                                  int lane) {
+        const int dq = 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int col = nt * 8 + (lane >> 2);
+            const bool ok = col < q_len * g;
+            const size_t row = ((size_t)b * q_len + (ok ? col / g : 0)) * Hq + kvh * g + (ok ? col % g : 0);
+            const uint32_t* qrow = reinterpret_cast<const uint32_t*>(q + row * D);
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                qf[kk][nt][0] = ok ? __ldg(qrow + ((kk * 16 + dq) >> 1)) : 0u;
+                qf[kk][nt][1] = ok ? __ldg(qrow + ((kk * 16 + dq + 8) >> 1)) : 0u;
+            }
         }
     }
 
@@ -136,15 +171,31 @@ struct BlockMath {
         }
     }
 
-    // One block: K slab at kbase, V slab at vbase (shared addresses); `valid`
-    // tokens (1..16) are inside the context, the rest are masked.
-    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
+    // One block: K slab at kbase, V slab at vbase (shared addresses); vq =
+    // L - (first token of the block): rows >= vq are outside the context (V
+    // zeroed), and column c additionally masks rows >= vq - qoff[c].
+    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk(kbase, lane, s, s2);
         uint32_t pb[NT][2], pb_lo[NT][2];
-        softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
-        pv(vbase, valid, lane, pb, pb_lo);
+        softmax(s, s2, vq, scale_log2, lane, pb, pb_lo);
+        pv(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb, pb_lo);
+    }
+
+    // Mask the scores of rows outside each column's context (select, never
+    // arithmetic: masked K rows may hold NaN).
+    __device__ __forceinline__ void mask_scores(float (&s)[NT][4], int vq, int lane) const {
+        if (vq - qm1 >= kBlockSize) return;  // no column reaches into this block's end
+        const int r0 = lane >> 2;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int lim = vq - qoff[nt][c];
+                if (r0 >= lim) s[nt][c] = -INFINITY;
+                if (r0 + 8 >= lim) s[nt][c + 2] = -INFINITY;
+            }
     }
 
     // ---- S4: S^T = K Q^T (two independent accumulator chains s, s2)
@@ -171,18 +222,16 @@ struct BlockMath {
 
     // ---- S5: scale (fp32), mask t >= valid, online softmax per head column;
     // P leaves as PV B fragments (transposed in registers with movmatrix)
-    __device__ __forceinline__ void softmax(float (&s)[NT][4], const float (&s2)[NT][4], int valid,
+    __device__ __forceinline__ void softmax(float (&s)[NT][4], const float (&s2)[NT][4], int vq,
                                             float scale_log2, int lane, uint32_t (&pb)[NT][2],
                                             uint32_t (&pb_lo)[NT][2]) {
-        const int r0 = lane >> 2;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) s[nt][r] = (s[nt][r] + s2[nt][r]) * scale_log2;
-            if (valid < kBlockSize) {
-                if (r0 >= valid) s[nt][0] = s[nt][1] = -INFINITY;
-                if (r0 + 8 >= valid) s[nt][2] = s[nt][3] = -INFINITY;
-            }
+        mask_scores(s, vq, lane);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
             float pr[4];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -191,10 +240,13 @@ struct BlockMath {
                 mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 8));
                 mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 16));
                 const float m_new = fmaxf(m_run[nt][c], mx);
-                const float alpha = ex2(m_run[nt][c] - m_new);
+                // a column with no visible token yet stays at -inf: use 0 as the
+                // reference so that alpha and p are 0, not NaN
+                const float m_ref = m_new == -INFINITY ? 0.f : m_new;
+                const float alpha = ex2(m_run[nt][c] - m_ref);
                 m_run[nt][c] = m_new;
-                pr[c] = ex2(s[nt][c] - m_new);
-                pr[c + 2] = ex2(s[nt][c + 2] - m_new);
+                pr[c] = ex2(s[nt][c] - m_ref);
+                pr[c + 2] = ex2(s[nt][c + 2] - m_ref);
                 l_run[nt][c] = l_run[nt][c] * alpha + pr[c] + pr[c + 2];
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {
@@ -290,17 +342,21 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
     static constexpr int MT = D / 16;
     static constexpr int kSlab = kBlockSize * D;  // 1 byte per element
 
-    // Q B fragments: qf[2j + half][nt] = Q[h][32j + 16 half + 4(lane%4) + {0,1 | 2,3}]
-    __device__ __forceinline__ void load_q(const uint16_t* q, size_t first_row, int g, int lane) {
-        const int h = lane >> 2, t = lane & 3;
+    // Q B fragments: qf[2j + half][nt] = Q[col][32j + 16 half + 4(lane%4) + {0,1 | 2,3}],
+    // columns = (query token i, head h), c = i * g + h
+    __device__ __forceinline__ void load_q_tokens(const uint16_t* q, int b, int kvh, int Hq, int q_len, int g,
+                                                  int lane) {
+        const int t = lane & 3;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const int hh = nt * 8 + h;
-            const uint16_t* qrow = q + (first_row + hh) * D;
+            const int col = nt * 8 + (lane >> 2);
+            const bool ok = col < q_len * g;
+            const size_t row = ((size_t)b * q_len + (ok ? col / g : 0)) * Hq + kvh * g + (ok ? col % g : 0);
+            const uint16_t* qrow = q + row * D;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
                 uint2 w = make_uint2(0u, 0u);
-                if (hh < g) w = __ldg(reinterpret_cast<const uint2*>(qrow + kk * 16 + 4 * t));
+                if (ok) w = __ldg(reinterpret_cast<const uint2*>(qrow + kk * 16 + 4 * t));
                 if constexpr (Q_BF16) {
                     const float2 a = unpack2<true>(w.x), b = unpack2<true>(w.y);
                     w.x = pack2<false>(a.x, a.y);
@@ -360,40 +416,35 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         }
     }
 
-    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int valid, float scale_log2,
+    __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk8(kbase, lane, s, s2);
         uint32_t pb[NT][2], pb_lo[NT][2];
-        this->softmax(s, s2, valid, scale_log2, lane, pb, pb_lo);
-        pv8(vbase, valid, lane, pb);
+        this->softmax(s, s2, vq, scale_log2, lane, pb, pb_lo);
+        pv8(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb);
     }
 
     // Two blocks (32 tokens) per step: independent QK chains, ONE online-softmax
     // update (shared max / rescale), two PV tiles -- halves the per-block
     // latency chain, which bounds the e4m3 path (half the bytes per block).
-    __device__ __forceinline__ void block2(uint32_t kb0, uint32_t vb0, int valid0, uint32_t kb1, uint32_t vb1,
-                                           int valid1, float scale_log2, int lane) {
+    __device__ __forceinline__ void block2(uint32_t kb0, uint32_t vb0, int vq0, uint32_t kb1, uint32_t vb1,
+                                           int vq1, float scale_log2, int lane) {
         float sa[NT][4], sa2[NT][4], sb[NT][4], sb2[NT][4];
         qk8(kb0, lane, sa, sa2);
         qk8(kb1, lane, sb, sb2);
-        const int r0 = lane >> 2;
         uint32_t pa[NT][2], pbb[NT][2];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 sa[nt][r] = (sa[nt][r] + sa2[nt][r]) * scale_log2;
                 sb[nt][r] = (sb[nt][r] + sb2[nt][r]) * scale_log2;
             }
-            if (valid0 < kBlockSize) {
-                if (r0 >= valid0) sa[nt][0] = sa[nt][1] = -INFINITY;
-                if (r0 + 8 >= valid0) sa[nt][2] = sa[nt][3] = -INFINITY;
-            }
-            if (valid1 < kBlockSize) {
-                if (r0 >= valid1) sb[nt][0] = sb[nt][1] = -INFINITY;
-                if (r0 + 8 >= valid1) sb[nt][2] = sb[nt][3] = -INFINITY;
-            }
+        this->mask_scores(sa, vq0, lane);
+        this->mask_scores(sb, vq1, lane);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
             float pra[4], prb[4];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -402,12 +453,13 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
                 mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 8));
                 mx = fmaxf(mx, __shfl_xor_sync(kFullMask, mx, 16));
                 const float m_new = fmaxf(this->m_run[nt][c], mx);
-                const float alpha = ex2(this->m_run[nt][c] - m_new);
+                const float m_ref = m_new == -INFINITY ? 0.f : m_new;  // column not started yet
+                const float alpha = ex2(this->m_run[nt][c] - m_ref);
                 this->m_run[nt][c] = m_new;
-                pra[c] = ex2(sa[nt][c] - m_new);
-                pra[c + 2] = ex2(sa[nt][c + 2] - m_new);
-                prb[c] = ex2(sb[nt][c] - m_new);
-                prb[c + 2] = ex2(sb[nt][c + 2] - m_new);
+                pra[c] = ex2(sa[nt][c] - m_ref);
+                pra[c + 2] = ex2(sa[nt][c + 2] - m_ref);
+                prb[c] = ex2(sb[nt][c] - m_ref);
+                prb[c + 2] = ex2(sb[nt][c + 2] - m_ref);
                 this->l_run[nt][c] = this->l_run[nt][c] * alpha + (pra[c] + pra[c + 2]) + (prb[c] + prb[c + 2]);
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {
@@ -420,8 +472,8 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
             pbb[nt][0] = movmatrix_trans(pack2<false>(prb[0], prb[1]));
             pbb[nt][1] = movmatrix_trans(pack2<false>(prb[2], prb[3]));
         }
-        pv8(vb0, valid0, lane, pa);
-        pv8(vb1, valid1, lane, pbb);
+        pv8(vb0, vq0 < kBlockSize ? vq0 : kBlockSize, lane, pa);
+        pv8(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
     }
 
     // Output column d held by accumulator acc[i][*][r]: rows 0-7 of a tile are

@@ -98,9 +98,12 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
                 rec[3] = 0;
             }
         }
-        if (part == 0 && L <= 0) {  // context_len == 0 => zero row (reading R6)
-            for (int i = threadIdx.x; i < g * D; i += blockDim.x)
-                store_out(p.out, ((size_t)b * p.Hq + kvh * g) * D + i, 0.f, p.out_dtype);
+        if (part == 0 && L <= 0) {  // context_len == 0 => zero rows (reading R6), every query token
+            for (int i = threadIdx.x; i < p.q_len * g * D; i += blockDim.x) {
+                const int col = i / D, dd = i % D;
+                const size_t row = ((size_t)b * p.q_len + col / g) * p.Hq + kvh * g + col % g;
+                store_out(p.out, row * D + dd, 0.f, p.out_dtype);
+            }
         }
         return;
     }
@@ -178,7 +181,8 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
 
     // ============================== consumer warps ==============================
     BM bm;
-    bm.load_q(p.q, (size_t)b * p.Hq + kvh * g, g, lane);
+    bm.set_q_tokens(p.q_len, g, lane);
+    bm.load_q_tokens(p.q, b, kvh, p.Hq, p.q_len, g, lane);
     bm.reset();
     if constexpr (SELF) {
         // A warp takes blocks in groups of PAIR (e4m3: pairs 2w, 2w+1 mod 8 with
@@ -242,10 +246,10 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
             mbar_wait(&full[st0], (j / STAGES) & 1);
             if (two) mbar_wait(&full[st1], ((j + 1) / STAGES) & 1);
             const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
-            const int v0 = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
+            const int v0 = L - (sb + j) * kBlockSize;  // tokens of the context from this block on
             if constexpr (PAIR == 2) {
                 if (two) {
-                    const int v1 = min(kBlockSize, e_tok - (sb + j + 1) * kBlockSize);
+                    const int v1 = L - (sb + j + 1) * kBlockSize;
                     bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
                 } else {
                     bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
@@ -273,8 +277,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
             const uint32_t round = j / STAGES;
             mbar_wait(&full[stage], round & 1);
             const uint32_t kbase = smem_u32(ring + stage * G::kStage);
-            const int valid = min(kBlockSize, e_tok - (sb + j) * kBlockSize);
-            bm.block(kbase, kbase + G::kSlab, valid, p.scale_log2, lane);
+            bm.block(kbase, kbase + G::kSlab, L - (sb + j) * kBlockSize, p.scale_log2, lane);
             mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
         }
     }
@@ -313,11 +316,12 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 
     const bool direct = n_parts == 1;
-    for (int idx = threadIdx.x; idx < g * D; idx += kConsumerWarps * 32) {
-        const int h = idx / D, dd = idx % D;
+    for (int idx = threadIdx.x; idx < p.q_len * g * D; idx += kConsumerWarps * 32) {
+        const int h = idx / D, dd = idx % D;  // h: column = (query token, head)
         float M = -INFINITY;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, merge_m[w * NH + h]);
+        if (M == -INFINITY) M = 0.f;  // column with no visible token in this unit
         float num = 0.f, den = 0.f;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) {
@@ -325,13 +329,14 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
             den += sc * merge_l[w * NH + h];
             num += sc * merge_acc[(w * NH + h) * (D + 4) + dd];
         }
-        const float o = num / den * p.out_scale;  // v_scale for the e4m3 cache, else 1
-        const size_t row = (size_t)b * p.Hq + kvh * g + h;
+        // den == 0: no visible token for this column in this unit (multi-token decode)
+        const float o = den > 0.f ? num / den * p.out_scale : 0.f;  // v_scale for the e4m3 cache, else 1
+        const size_t row = ((size_t)b * p.q_len + h / g) * p.Hq + kvh * g + h % g;
         if (direct) {
             store_out(p.out, row * D + dd, o, p.out_dtype);
         } else {
             p.ws_o[(row * p.p_max + part) * D + dd] = o;
-            if (dd == 0) p.ws_lse[row * p.p_max + part] = M + __log2f(den);
+            if (dd == 0) p.ws_lse[row * p.p_max + part] = den > 0.f ? M + __log2f(den) : -INFINITY;
         }
     }
 }
@@ -342,8 +347,8 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
     constexpr int PER = D / 32;
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (row >= p.B * p.Hq) return;
-    const int b = row / p.Hq;
+    if (row >= p.B * p.q_len * p.Hq) return;
+    const int b = row / (p.q_len * p.Hq);
     int L = p.lens[b];
     L = L < p.max_tokens ? L : p.max_tokens;
     const int n_parts = (L + p.part_tokens - 1) / p.part_tokens;
@@ -353,6 +358,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
     for (int i = lane; i < n_parts; i += 32) M = fmaxf(M, lse[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+    if (M == -INFINITY) M = 0.f;  // every partition empty for this column
     float accv[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) accv[e] = 0.f;
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
             accv[1] += w * x.y;
         }
     }
-    const float inv = 1.f / den;
+    const float inv = den > 0.f ? 1.f / den : 0.f;  // no visible token at all: zero row
 #pragma unroll
     for (int e = 0; e < PER; ++e)
         store_out(p.out, (size_t)row * D + lane * PER + e, accv[e] * inv, p.out_dtype);
@@ -499,7 +505,7 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream) {
     // (a programmatic-dependent-launch variant measured neutral to -2 %)
-    const int rows = p.B * p.Hq;
+    const int rows = p.B * p.q_len * p.Hq;
     const dim3 grid((rows + 3) / 4);
     if (head_dim == 64)
         combine_kernel<64><<<grid, 128, 0, stream>>>(p);

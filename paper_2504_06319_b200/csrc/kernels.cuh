@@ -25,6 +25,7 @@ struct SplitKParams {
     float* ws_lse;        // [B, Hq, P_max]      log2-sum-exp of each partition
     int32_t* trace;       // debug trace (TRACE instantiation only)
     int B, Hq, Hkv, g, max_blocks, part_tokens, p_max;
+    int q_len;  // query tokens per sequence (multi-token decode); columns = q_len * g <= 16
     int out_dtype;
     int pf_mode, pf_dist;
     int eviction;  // pda_eviction bits
@@ -94,6 +95,7 @@ struct CombineParams {
     const int32_t* lens;
     void* out;
     int B, Hq, p_max, part_tokens, max_tokens;
+    int q_len;
     int out_dtype;
 };
 

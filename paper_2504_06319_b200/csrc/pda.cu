@@ -25,6 +25,8 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 size_t elem_bytes(int dt) { return dt == PDA_F32 ? 4 : 2; }
 
+int q_tokens(const pda_shape* s) { return s->q_len > 1 ? s->q_len : 1; }
+
 pda_status validate(const pda_shape* s, const pda_options* o) {
     if (!s || !o) return PDA_ERR_NULL;
     if (s->num_seqs < 0 || s->num_seqs > 65535 || s->num_q_heads <= 0 || s->num_kv_heads <= 0 ||
@@ -49,6 +51,11 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         return PDA_ERR_UNSUPPORTED;  // self-issue block-id window reaches 32 blocks ahead
     if (s->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
     if (s->num_q_heads / s->num_kv_heads > 16) return PDA_ERR_UNSUPPORTED;
+    if (s->q_len < 0 || s->q_len > 16) return PDA_ERR_SHAPE;
+    if (q_tokens(s) > 1 &&
+        (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) > 16 ||
+         (o && o->kernel != PDA_KERNEL_AUTO && o->kernel != PDA_KERNEL_SPLITK)))
+        return PDA_ERR_UNSUPPORTED;
     if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_LINE_L2) return PDA_ERR_SHAPE;
     if (o->prefetch != PDA_PF_OFF && (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
         return PDA_ERR_SHAPE;
@@ -168,7 +175,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // S0: split-K plan.  Units (partition, kv head, seq) are independent; pick
     // the partition size so the grid holds >= 4 waves of resident CTAs while a
     // partition keeps >= 512 tokens (32 blocks) to amortise pipeline fill.
-    const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
+    const int n_tiles = q_tokens(s) * (Hq / Hkv) <= 8 ? 1 : 2;
     // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
     const int stages = o->smem_stages ? o->smem_stages
                                       : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
@@ -199,8 +206,8 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->threads = pda::splitk_threads(self_issue(s, o));
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
-    pl->workspace_bytes =
-        p_max > 1 ? align256((size_t)B * Hq * p_max * D * 4) + align256((size_t)B * Hq * p_max * 4) : 0;
+    const size_t rows = (size_t)B * q_tokens(s) * Hq;
+    pl->workspace_bytes = p_max > 1 ? align256(rows * p_max * D * 4) + align256(rows * p_max * 4) : 0;
     return PDA_OK;
 }
 
@@ -376,7 +383,8 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.bt = bt;
     p.lens = lens;
     p.out = out;
-    const size_t o_bytes = align256((size_t)s->num_seqs * s->num_q_heads * pl.p_max * s->head_dim * 4);
+    const size_t o_bytes =
+        align256((size_t)s->num_seqs * q_tokens(s) * s->num_q_heads * pl.p_max * s->head_dim * 4);
     p.ws_o = pl.p_max > 1 ? static_cast<float*>(ws) : nullptr;
     p.ws_lse = pl.p_max > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
     p.trace = trace;
@@ -392,9 +400,10 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.pf_dist = pf_dist;
     p.eviction = pl.eviction;
     p.trace_rec_len = pl.trace_rec_len;
+    p.q_len = q_tokens(s);
     p.scale_log2 = (float)((double)scale * k_scale * 1.4426950408889634);
     p.out_scale = kv8 && o->v_scale > 0.f ? o->v_scale : 1.f;
-    const int n_tiles = p.g <= 8 ? 1 : 2;
+    const int n_tiles = p.q_len * p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,
                              dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream, kv8, self_issue(s, o));
@@ -413,6 +422,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         c.p_max = p.p_max;
         c.part_tokens = p.part_tokens;
         c.max_tokens = s->max_blocks_per_seq * s->block_size;
+        c.q_len = p.q_len;
         c.out_dtype = s->out_dtype;
         err = pda::launch_combine(c, s->head_dim, stream);
         if (err != cudaSuccess) return PDA_ERR_CUDA;
@@ -473,9 +483,9 @@ pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_
     if (st != PDA_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t B = shape->num_seqs;
-    const size_t q_bytes = B * shape->num_q_heads * shape->head_dim * 2;
+    const size_t q_bytes = B * q_tokens(shape) * shape->num_q_heads * shape->head_dim * 2;
     const size_t bt_bytes = B * shape->max_blocks_per_seq * 4;
-    const size_t out_bytes = B * shape->num_q_heads * shape->head_dim * elem_bytes(shape->out_dtype);
+    const size_t out_bytes = B * q_tokens(shape) * shape->num_q_heads * shape->head_dim * elem_bytes(shape->out_dtype);
     if (cudaMemcpyAsync(q_dev, q_host, q_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(block_tables_dev, block_tables_host, bt_bytes, cudaMemcpyHostToDevice, s) !=
             cudaSuccess ||
@@ -517,6 +527,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 7; }
+int32_t pda_abi_version(void) { return 8; }
 
 }  // extern "C"

@@ -45,6 +45,7 @@ def shape(**kw):
              max_blocks_per_seq=16, dtype=0, out_dtype=0)
     d.update(kw)
     d.setdefault("kv_dtype", d["dtype"])
+    d.setdefault("q_len", 1)
     return _lib.Shape(**d)
 
 
@@ -69,6 +70,9 @@ def opts(**kw):
     (dict(kv_dtype=3), 3),                 # e4m3 needs head_dim 128
     (dict(kv_dtype=3, head_dim=128), 0),
     (dict(kv_dtype=1), 3),                 # bf16 cache with an fp16 q
+    (dict(q_len=4), 0),                    # 4 tokens x g=2 = 8 columns
+    (dict(q_len=9), 3),                    # 18 columns > 16
+    (dict(q_len=17), 2),
 ])
 def test_check_args_shape(kw, status):
     assert pda.check_args(shape(**kw), opts()) == status
@@ -202,6 +206,14 @@ def test_eviction_auto_resolution():
     assert pda.plan(big, opts(eviction=2))["eviction"] == 2
 
 
+def test_multi_token_needs_splitk_and_sizes_workspace():
+    s = shape(q_len=4, max_blocks_per_seq=64)
+    assert pda.check_args(s, opts(kernel=1)) == 3 and pda.check_args(s, opts(kernel=4)) == 3
+    p = pda.plan(s, opts(kernel=2, partition_tokens=256))
+    rows = 2 * 4 * 4  # B * q_len * Hq
+    assert p["p_max"] == 4 and p["workspace_bytes"] == rows * 4 * 64 * 4 + ((rows * 4 * 4 + 255) // 256) * 256
+
+
 def test_e4m3_cache_needs_splitk():
     s = shape(head_dim=128, kv_dtype=3)
     assert pda.check_args(s, opts(kernel=2)) == 0
@@ -212,7 +224,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 7
+    assert pda.lib().pda_abi_version() == 8
 
 
 def test_product_never_imports_oracle():

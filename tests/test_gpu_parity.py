@@ -431,3 +431,57 @@ def test_tp_shards_bitwise_equal_unsharded(pda, world, kernel):
         assert torch.equal(got, full)
     else:  # balanced: ranges differ with the head count, results agree to rounding
         assert (got.float() - full.float()).abs().max().item() <= 2e-3
+
+
+# ---- multi-token (speculative) decode ---------------------
+
+MQ_CASES = [
+    (synth.Config("mq_mha", 3, 4, 4, 128, (37, 300, 5), "fp16", poison_blocks=3), 8),
+    (synth.Config("mq_gqa4", 2, 16, 4, 128, (700, 33), "bf16", poison_blocks=2), 4),
+    (synth.Config("mq_gqa2_d64", 3, 8, 4, 64, (2, 129, 64), "fp16", poison_blocks=2), 4),
+    (synth.Config("mq_gqa8", 2, 16, 2, 128, (95, 250), "bf16", poison_blocks=2), 2),
+]
+
+
+@pytest.mark.parametrize("cfg,q_len", MQ_CASES, ids=lambda x: x.name if hasattr(x, "name") else str(x))
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=16), dict(partition_tokens=64, smem_stages=4)],
+                         ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
+def test_multi_token_parity_vs_oracle(pda, oracle_mod, cfg, q_len, kw):
+    inp = synth.with_query_tokens(synth.make_inputs(cfg, seed=21), q_len)
+    ref = oracle_mod.paged_attention_mq(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                        inp["context_lens"], inp["scale"], cfg.dtype)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, **kw)
+    assert out.shape == inp["q"].shape
+    assert max_err(out, ref) <= TOL
+    assert max_err(gpu(pda, dev, out_dtype=torch.float32, **kw), ref) <= 5e-4
+
+
+def test_multi_token_q_len_one_matches_single_query_bitwise(pda):
+    dev = to_dev(synth.make_inputs(SHAPES[2], seed=4))
+    a = gpu(pda, dev, partition_tokens=64)
+    q4 = dict(dev, q=dev["q"][:, None].contiguous())
+    b = gpu(pda, q4, partition_tokens=64)
+    assert torch.equal(a, b[:, 0])
+
+
+def test_multi_token_e4m3(pda, oracle_mod):
+    cfg = synth.Config("mq_kv8", 2, 8, 2, 128, (200, 41), "fp16", poison_blocks=2)
+    inp = kv8(synth.with_query_tokens(synth.make_inputs(cfg, seed=5), 3))
+    deq = dict(inp)
+    deq["k_cache"] = (inp["k_cache"].view(torch.float8_e4m3fn).float() * inp["k_scale"]).double()
+    deq["v_cache"] = (inp["v_cache"].view(torch.float8_e4m3fn).float() * inp["v_scale"]).double()
+    # reference: the mq oracle on the exactly dequantised cache, via per-token single-query kv8 calls
+    ref = np.stack([oracle_mod.paged_attention_kv8(inp["q"][:, i], inp["k_cache"], inp["v_cache"], inp["k_scale"],
+                                                   inp["v_scale"], inp["block_tables"],
+                                                   inp["context_lens"] - 2 + i, inp["scale"], "fp16")
+                    for i in range(3)], axis=1)
+    out = gpu_kv8(pda, to_dev(inp), partition_tokens=32)
+    assert max_err(out, ref) <= TOL
+
+
+def test_multi_token_prefetch_bitwise_invisible(pda):
+    dev = to_dev(synth.with_query_tokens(synth.make_inputs(MQ_CASES[1][0], seed=6), 4))
+    base = gpu(pda, dev, prefetch="off")
+    for mode in ("bulk", "line"):
+        assert torch.equal(gpu(pda, dev, prefetch=mode, prefetch_distance=3), base)
