@@ -14,7 +14,10 @@ from bench import workload_config
 cfg = workload_config(sys.argv[1])
 variants = eval(sys.argv[2])
 kv8 = len(sys.argv) > 3 and sys.argv[3] == "kv8"
+q_len = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 inp = synth.make_inputs(cfg, seed=0, device="cuda")
+if q_len > 1:
+    inp = synth.with_query_tokens(inp, q_len)
 if kv8:
     inp = synth.quantize_kv_e4m3(inp)
     variants = [dict(v, k_scale=inp["k_scale"], v_scale=inp["v_scale"]) for v in variants]
@@ -42,4 +45,6 @@ for rnd in range(5):
 tot = cfg.kv_bytes() // (2 if kv8 else 1) + cfg.other_bytes()
 for i, v in enumerate(variants):
     us = statistics.median(res[i])
-    print(json.dumps(dict(cell=cfg.name + ("_kv8" if kv8 else ""), **v, us=round(us, 1), gbs=round(tot / us / 1e3))))
+    print(json.dumps(dict(cell=cfg.name + ("_kv8" if kv8 else "") + (f"_q{q_len}" if q_len > 1 else ""), **v,
+                          us=round(us, 1), gbs=round(tot / us / 1e3),
+                          tokens_per_s=round(cfg.num_seqs * q_len / us * 1e6))))
