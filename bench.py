@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--partition", type=int, default=0)
     ap.add_argument("--kernel", default=None, help="auto|splitk|balanced|stream|paper")
     ap.add_argument("--no-extras", action="store_true", help="skip ablation arms / e2e / cpu baseline")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="TP output all-gather inside the kernel's stores (symmetric memory) instead of NCCL")
     ap.add_argument("--sweep", action="store_true", help="prefetch-distance x stages sweep (extra JSON lines on stderr)")
     return ap.parse_args()
 
@@ -235,6 +237,10 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    elif args.fused_gather:  # symmetric memory needs a process group, even of one rank
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", dev_index))
     pda.lib()
 
     cfg = workload_config(args.config)
@@ -260,7 +266,7 @@ def main():
         return TPDecodeAttention(inp["k_cache"], inp["v_cache"], local_cfg.num_seqs,
                                  local_cfg.num_q_heads, local_cfg.max_blocks_per_seq, dt, **kw)
 
-    step_main = make_step(**opt_kw)
+    step_main = make_step(**opt_kw, fused_gather=args.fused_gather)
     q, bt, lens, scale = inp["q"], inp["block_tables"], inp["context_lens"], inp["scale"]
     stream = torch.cuda.current_stream()
 
@@ -423,6 +429,7 @@ def main():
             "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
             "eviction": ["normal", "demand_first", "prefetch_last", "both"][pl["eviction"]],
             "issue": "self (consumer warps refill their ring stages)" if pl["threads"] == 128 else "producer warp",
+            "tp_gather": "fused into the kernel stores (symmetric memory)" if args.fused_gather else "NCCL all_gather_into_tensor",
             "p_max": pl["p_max"],
             "l2": f"no flush: inputs larger than L2 ({cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)",
             "bytes_per_step": total_bytes,
@@ -442,7 +449,7 @@ def main():
     line.update(extras)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

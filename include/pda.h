@@ -213,6 +213,26 @@ pda_status paged_decode_attention_trace(const void* q, const void* k_cache, cons
                                         void* workspace, size_t workspace_bytes, int32_t* trace,
                                         size_t trace_words, void* stream);
 
+/* The decode step with the tensor-parallel output all-gather fused into its
+ * stores (S9 fused): every output element this rank
+ * computes is written directly into the output buffer of each of the n_peers
+ * ranks of its group, over NVLink.
+ *   out_peers      HOST array of n_peers (1..8) device pointers, each rank's
+ *                  [B, q_len, total_q_heads, D] out_dtype buffer, mapped into
+ *                  this device's address space (e.g. symmetric memory)
+ *   head_offset    first global q head of this rank's shard (its Hq heads land
+ *                  at [head_offset, head_offset + Hq) of every buffer)
+ * Other arguments as paged_decode_attention; split-K kernel only.  Completion
+ * is ordered on `stream`; before any rank reads its buffer the group must pass
+ * a cross-device barrier after every rank's call (e.g. the symmetric-memory
+ * barrier), which is the caller's responsibility. */
+pda_status paged_decode_attention_gather(const void* q, const void* k_cache, const void* v_cache,
+                                         const int32_t* block_tables, const int32_t* context_lens,
+                                         float scale, void* const* out_peers, int32_t n_peers,
+                                         int32_t head_offset, int32_t total_q_heads,
+                                         const pda_shape* shape, const pda_options* opt, void* workspace,
+                                         size_t workspace_bytes, void* stream);
+
 /* End-to-end decode step from HOST buffers: copies this step's inputs
  * (q, block_tables, context_lens; pinned host memory recommended) to the
  * device staging buffers, runs paged_decode_attention against the
@@ -237,7 +257,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 8: shape.q_len; 7: issue_mode; 6: e4m3 KV; 5: EV_AUTO */
+int32_t pda_abi_version(void);  /* 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
 
 #ifdef __cplusplus
 }

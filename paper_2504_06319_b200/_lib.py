@@ -86,6 +86,8 @@ def lib():
             L.paged_decode_attention.restype = i32
             L.paged_decode_attention_trace.argtypes = [p, p, p, p, p, f32, p, ps, po, p, sz, p, sz, p]
             L.paged_decode_attention_trace.restype = i32
+            L.paged_decode_attention_gather.argtypes = [p, p, p, p, p, f32, p, i32, i32, i32, ps, po, p, sz, p]
+            L.paged_decode_attention_gather.restype = i32
             L.pda_decode_step_host.argtypes = [p, p, p, p, p, p, p, p, p, p, f32, ps, po, p, sz, p]
             L.pda_decode_step_host.restype = i32
             L.pda_read_roofline.argtypes = [p, sz, p, p]
@@ -232,6 +234,35 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
         ws_ptr, wsb, s)
     _check(st, "paged_decode_attention")
     return out
+
+
+def paged_decode_attention_gather(q, k_cache, v_cache, block_tables, context_lens, scale, out_peers,
+                                  head_offset, total_q_heads, *, out_dtype=None, workspace=None, stream=None,
+                                  **opt_kw):
+    """Decode step whose stores also perform the TP output all-gather (include/pda.h).
+
+    out_peers: list of device pointers (ints) or CUDA tensors, one per rank, each
+    [B, (q_len,) total_q_heads, D]; this rank's heads go to
+    [head_offset, head_offset + Hq).  The caller barriers across ranks afterwards.
+    """
+    import torch
+    _require_cuda(q, k_cache, v_cache, block_tables, context_lens)
+    ptrs = [t.data_ptr() if hasattr(t, "data_ptr") else int(t) for t in out_peers]
+    if out_dtype is None:
+        t0 = out_peers[0]
+        out_dtype = t0.dtype if hasattr(t0, "dtype") else q.dtype
+    shape = make_shape(q, k_cache, block_tables, out_dtype)
+    opts = make_options(**opt_kw)
+    info = plan(shape, opts)
+    wsb = info["workspace_bytes"]
+    if wsb and (workspace is None or workspace.numel() * workspace.element_size() < wsb):
+        workspace = torch.zeros(wsb, dtype=torch.uint8, device=q.device)
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    st = lib().paged_decode_attention_gather(
+        q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(), context_lens.data_ptr(),
+        float(scale), arr, len(ptrs), int(head_offset), int(total_q_heads), ctypes.byref(shape),
+        ctypes.byref(opts), workspace.data_ptr() if wsb else None, wsb, _stream_handle(stream))
+    _check(st, "paged_decode_attention_gather")
 
 
 class HostDecodeStep:

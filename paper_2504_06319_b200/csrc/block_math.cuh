@@ -33,6 +33,15 @@ __device__ __forceinline__ void store_out(void* out, size_t idx, float x, int ou
     }
 }
 
+// Write one output element of (row = (b * q_len + i) * Hq + local head, d) to
+// every destination rank (S9 fused: the TP all-gather happens in the store).
+__device__ __forceinline__ void store_out_peers(const OutPeers& o, size_t row, int Hq, int D, int dd, float x,
+                                                int out_dtype) {
+    const size_t bi = row / Hq, h = row % Hq;
+    const size_t idx = (bi * o.Hq_out + o.head_off + h) * D + dd;
+    for (int r = 0; r < o.n; ++r) store_out(o.ptr[r], idx, x, out_dtype);
+}
+
 // S3: TMA loads of one block's K and V slabs (kChunks boxes of 16 rows x
 // 128 B each) into a ring stage, completion counted on `bar`; demand loads
 // optionally evict_first (the block is not needed again this step).

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
             for (int i = threadIdx.x; i < p.q_len * g * D; i += blockDim.x) {
                 const int col = i / D, dd = i % D;
                 const size_t row = ((size_t)b * p.q_len + col / g) * p.Hq + kvh * g + col % g;
-                store_out(p.out, row * D + dd, 0.f, p.out_dtype);
+                store_out_peers(p.outs, row, p.Hq, D, dd, 0.f, p.out_dtype);
             }
         }
         return;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         const float o = den > 0.f ? num / den * p.out_scale : 0.f;  // v_scale for the e4m3 cache, else 1
         const size_t row = ((size_t)b * p.q_len + h / g) * p.Hq + kvh * g + h % g;
         if (direct) {
-            store_out(p.out, row * D + dd, o, p.out_dtype);
+            store_out_peers(p.outs, row, p.Hq, D, dd, o, p.out_dtype);
         } else {
             p.ws_o[(row * p.p_max + part) * D + dd] = o;
             if (dd == 0) p.ws_lse[row * p.p_max + part] = den > 0.f ? M + __log2f(den) : -INFINITY;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
     const float inv = den > 0.f ? 1.f / den : 0.f;  // no visible token at all: zero row
 #pragma unroll
     for (int e = 0; e < PER; ++e)
-        store_out(p.out, (size_t)row * D + lane * PER + e, accv[e] * inv, p.out_dtype);
+        store_out_peers(p.outs, row, p.Hq, D, lane * PER + e, accv[e] * inv, p.out_dtype);
 }
 
 template <int D, int NT, int STAGES, bool KV8 = false>

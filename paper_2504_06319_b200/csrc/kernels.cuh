@@ -14,13 +14,26 @@ constexpr int kPaperWarps = 4;     // paper kernel: 128 threads = 4 warps (Table
 
 enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };
 
+constexpr int kMaxPeers = 8;  // fused output all-gather: ranks written by one kernel
+
+// Output destinations of the split-K path: out_peers[0..n_peers) are the [B,
+// q_len, Hq_out, D] output buffers of every rank of a tensor-parallel group
+// (NVLink peer-mapped, e.g. symmetric memory); this rank's heads land at
+// [head_off, head_off + Hq).  Single-GPU: n_peers = 1, Hq_out = Hq, head_off = 0.
+struct OutPeers {
+    void* ptr[kMaxPeers];
+    int n;
+    int head_off;
+    int Hq_out;
+};
+
 struct SplitKParams {
     const uint16_t* q;  // [B, Hq, D]
     const uint8_t* k;   // [num_blocks, Hkv, 16, D] (bytes: prefetch addresses)
     const uint8_t* v;
     const int32_t* bt;    // [B, max_blocks]
     const int32_t* lens;  // [B]
-    void* out;            // [B, Hq, D]
+    OutPeers outs;        // out [B, q_len, Hq, D] on every destination rank
     float* ws_o;          // [B, Hq, P_max, D]   split-K partial outputs (normalised)
     float* ws_lse;        // [B, Hq, P_max]      log2-sum-exp of each partition
     int32_t* trace;       // debug trace (TRACE instantiation only)
@@ -93,7 +106,7 @@ struct CombineParams {
     const float* ws_o;
     const float* ws_lse;
     const int32_t* lens;
-    void* out;
+    OutPeers outs;
     int B, Hq, p_max, part_tokens, max_tokens;
     int q_len;
     int out_dtype;

@@ -259,7 +259,8 @@ pda_status use_device_of(const void* ptr) {
 pda_status run(const void* q, const void* k_cache, const void* v_cache, const int32_t* bt,
                const int32_t* lens, float scale, void* out, const pda_shape* s,
                const pda_options* o, void* ws, size_t ws_bytes, int32_t* trace, size_t trace_words,
-               cudaStream_t stream) {
+               cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0, int head_off = 0,
+               int hq_out = 0) {
     pda_plan_info pl;
     pda_status st = plan(s, o, &pl);
     if (st != PDA_OK) return st;
@@ -382,7 +383,10 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.v = static_cast<const uint8_t*>(v_cache);
     p.bt = bt;
     p.lens = lens;
-    p.out = out;
+    p.outs.n = n_peers > 0 ? n_peers : 1;
+    for (int r = 0; r < p.outs.n; ++r) p.outs.ptr[r] = n_peers > 0 ? peers[r] : out;
+    p.outs.head_off = n_peers > 0 ? head_off : 0;
+    p.outs.Hq_out = n_peers > 0 ? hq_out : s->num_q_heads;
     const size_t o_bytes =
         align256((size_t)s->num_seqs * q_tokens(s) * s->num_q_heads * pl.p_max * s->head_dim * 4);
     p.ws_o = pl.p_max > 1 ? static_cast<float*>(ws) : nullptr;
@@ -416,7 +420,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         c.ws_o = p.ws_o;
         c.ws_lse = p.ws_lse;
         c.lens = lens;
-        c.out = out;
+        c.outs = p.outs;
         c.B = p.B;
         c.Hq = p.Hq;
         c.p_max = p.p_max;
@@ -466,6 +470,28 @@ pda_status paged_decode_attention_trace(const void* q, const void* k_cache, cons
     if (!trace) return PDA_ERR_NULL;
     return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
                workspace_bytes, trace, trace_words, static_cast<cudaStream_t>(stream));
+}
+
+pda_status paged_decode_attention_gather(const void* q, const void* k_cache, const void* v_cache,
+                                         const int32_t* block_tables, const int32_t* context_lens,
+                                         float scale, void* const* out_peers, int32_t n_peers,
+                                         int32_t head_offset, int32_t total_q_heads,
+                                         const pda_shape* shape, const pda_options* opt, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+    pda_status st = validate(shape, opt);
+    if (st != PDA_OK) return st;
+    if (!out_peers) return PDA_ERR_NULL;
+    if (n_peers < 1 || n_peers > pda::kMaxPeers || head_offset < 0 ||
+        head_offset + shape->num_q_heads > total_q_heads)
+        return PDA_ERR_SHAPE;
+    if (opt->kernel != PDA_KERNEL_AUTO && opt->kernel != PDA_KERNEL_SPLITK) return PDA_ERR_UNSUPPORTED;
+    for (int r = 0; r < n_peers; ++r) {
+        if (!out_peers[r]) return PDA_ERR_NULL;
+        if (!aligned16(out_peers[r])) return PDA_ERR_ALIGN;
+    }
+    return run(q, k_cache, v_cache, block_tables, context_lens, scale, out_peers[0], shape, opt, workspace,
+               workspace_bytes, nullptr, 0, static_cast<cudaStream_t>(stream), out_peers, n_peers, head_offset,
+               total_q_heads);
 }
 
 pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_host,
@@ -527,6 +553,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 8; }
+int32_t pda_abi_version(void) { return 9; }
 
 }  // extern "C"

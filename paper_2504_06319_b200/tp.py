@@ -46,13 +46,18 @@ class TPDecodeAttention:
 
     k_cache / v_cache hold only this rank's KV heads ([num_blocks, Hkv/N, 16, D]);
     q_local holds this rank's q heads.  __call__ runs the CUDA decode kernels
-    on the local shard and all-gathers the heads.
+    on the local shard and all-gathers the heads -- with NCCL
+    (all_gather_into_tensor, default), or, with fused_gather=True, inside the
+    kernel's own stores into every rank's symmetric-memory output buffer
+    followed by one symmetric-memory barrier.
     """
 
     def __init__(self, k_cache, v_cache, num_seqs, num_q_heads_local, max_blocks, dtype, group=None,
-                 **opts):
+                 fused_gather=False, **opts):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.fused = fused_gather
         D = k_cache.shape[-1]
         dev = k_cache.device
         self.k, self.v = k_cache, v_cache
@@ -69,12 +74,26 @@ class TPDecodeAttention:
         self.plan = _lib.plan(shape, opt)
         wsb = self.plan["workspace_bytes"]
         self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)  # stream tickets start at 0
+        self.hq_local = num_q_heads_local
+        if self.fused:
+            import torch.distributed._symmetric_memory as symm_mem
+            hq = num_q_heads_local * self.world
+            self.out_full = symm_mem.empty((num_seqs, hq, D), dtype=dtype, device=dev)
+            grp = group if group is not None else dist.group.WORLD
+            self.symm = symm_mem.rendezvous(self.out_full, grp)
+            self.peer_ptrs = list(self.symm.buffer_ptrs)
 
     def launches_per_step(self) -> int:
         # split-K launches its combine kernel when sequences are split
         return 1 + (1 if self.plan["kernel"] == 2 and self.plan["p_max"] > 1 else 0)
 
     def __call__(self, q_local, block_tables, context_lens, scale):
+        if self.fused:
+            _lib.paged_decode_attention_gather(q_local, self.k, self.v, block_tables, context_lens, scale,
+                                               self.peer_ptrs, self.rank * self.hq_local,
+                                               self.hq_local * self.world, workspace=self.ws, **self.opts)
+            self.symm.barrier(channel=0)  # every rank's stores have landed everywhere
+            return self.out_full.view(self.out_full.shape[0], 1, *self.out_full.shape[1:])
         _lib.paged_decode_attention(q_local, self.k, self.v, block_tables, context_lens, scale,
                                     out=self.out_local, workspace=self.ws, **self.opts)
         if self.world == 1:

@@ -21,7 +21,8 @@ def built():
 
 def test_exports_every_header_symbol():
     syms = pda.header_symbols()
-    assert {"paged_decode_attention", "paged_decode_attention_trace", "pda_check_args", "pda_plan",
+    assert {"paged_decode_attention", "paged_decode_attention_trace", "paged_decode_attention_gather",
+            "pda_check_args", "pda_plan",
             "pda_workspace_bytes", "pda_decode_step_host", "pda_read_roofline", "pda_status_string",
             "pda_abi_version"} <= set(syms)
     L = pda.lib()
@@ -224,7 +225,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 8
+    assert pda.lib().pda_abi_version() == 9
 
 
 def test_product_never_imports_oracle():

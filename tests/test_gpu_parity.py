@@ -485,3 +485,42 @@ def test_multi_token_prefetch_bitwise_invisible(pda):
     base = gpu(pda, dev, prefetch="off")
     for mode in ("bulk", "line"):
         assert torch.equal(gpu(pda, dev, prefetch=mode, prefetch_distance=3), base)
+
+
+# ---- fused TP output all-gather ----------------------------
+
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=32), dict(q_len=2)],
+                         ids=["direct", "combine", "multi_token"])
+def test_fused_gather_writes_every_peer_slice(pda, kw):
+    """The kernel's stores land this rank's heads in every destination buffer at
+    its head offset (three local buffers stand in for three ranks' peer-mapped
+    buffers) and touch nothing else; values equal the plain call bitwise."""
+    q_len = kw.pop("q_len", 1)
+    cfg = synth.Config("fg", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
+    inp = synth.make_inputs(cfg, seed=9)
+    if q_len > 1:
+        inp = synth.with_query_tokens(inp, q_len)
+    dev = to_dev(inp)
+    ref = gpu(pda, dev, **kw)
+    world, rank = 3, 1
+    shape = (3, q_len, 8 * world, 128) if q_len > 1 else (3, 8 * world, 128)
+    peers = [torch.full(shape, 7.0, dtype=torch.bfloat16, device="cuda") for _ in range(world)]
+    pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                      dev["context_lens"], dev["scale"], peers, rank * 8, 8 * world, **kw)
+    torch.cuda.synchronize()
+    for pb in peers:
+        mine = pb[..., 8:16, :]
+        assert torch.equal(mine, ref)
+        others = torch.cat([pb[..., :8, :], pb[..., 16:, :]], dim=-2)
+        assert (others == 7.0).all()
+
+
+def test_fused_gather_rejects_bad_offsets(pda):
+    dev = to_dev(synth.make_inputs(synth.C1_TINY, seed=0))
+    buf = torch.zeros((2, 8, 64), dtype=torch.float16, device="cuda")
+    with pytest.raises(pda.PdaError):
+        pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                          dev["context_lens"], dev["scale"], [buf], 6, 8)
+    with pytest.raises(pda.PdaError):
+        pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                          dev["context_lens"], dev["scale"], [buf], 0, 8, kernel="paper")
