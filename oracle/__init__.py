@@ -75,6 +75,15 @@ def lib():
             L.oracle_l2_residency_bound.argtypes = [i64, i64]
             L.oracle_l2_residency_bound.restype = i64
             L.oracle_max_threads.restype = i32
+            L.oracle_validate_inputs.argtypes = [p, p, i32, i32, i32, i64, p]
+            L.oracle_validate_inputs.restype = i32
+            L.oracle_e4m3_encode.argtypes = [ctypes.c_float]
+            L.oracle_e4m3_encode.restype = ctypes.c_uint8
+            L.oracle_kv_append.argtypes = [p, p, p, p, p, p, i32, i32, i32, i32, i32, i32]
+            L.oracle_kv_append.restype = i32
+            L.oracle_kv_append_e4m3.argtypes = [p, p, i32, ctypes.c_float, ctypes.c_float, p, p, p, p, i32,
+                                                i32, i32, i32, i32, i32]
+            L.oracle_kv_append_e4m3.restype = i32
             _lib = L
     return _lib
 
@@ -249,3 +258,46 @@ def l2_residency_bound(l2_bytes: int, m_total_b1: int) -> int:
 
 def max_threads() -> int:
     return lib().oracle_max_threads()
+
+
+def validate_inputs(block_tables, context_lens, num_blocks: int, block_size: int = 16):
+    """(sequences with an invalid length, referenced block ids out of range, invalid sequences)."""
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    counts = np.zeros(3, dtype=np.int64)
+    lib().oracle_validate_inputs(_ptr(bt), _ptr(lens), lens.shape[0], bt.shape[1], block_size, int(num_blocks),
+                                 _ptr(counts))
+    return tuple(int(c) for c in counts)
+
+
+def e4m3_encode(x: float) -> int:
+    """fp32 value -> e4m3 code (nearest, ties to even, saturating, NaN -> 0x7F)."""
+    return int(lib().oracle_e4m3_encode(float(x)))
+
+
+def kv_append(k_new, v_new, k_cache, v_cache, block_tables, context_lens):
+    """Return copies of the 16-bit caches with the new rows [B, q_len, Hkv, D] written in place."""
+    kn, vn = _u16(k_new), _u16(v_new)
+    kc, vc = _u16(k_cache).copy(), _u16(v_cache).copy()
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    B, q_len, Hkv, D = kn.shape
+    bs = kc.shape[2]
+    rc = lib().oracle_kv_append(_ptr(kn), _ptr(vn), _ptr(kc), _ptr(vc), _ptr(bt), _ptr(lens), B, q_len, Hkv, D,
+                                bs, bt.shape[1])
+    if rc != 0:
+        raise ValueError("oracle_kv_append: invalid arguments")
+    return kc, vc
+
+
+def kv_append_e4m3(k_new, v_new, dtype: str, k_scale: float, v_scale: float, k_cache, v_cache, block_tables,
+                   context_lens):
+    """Return copies of the e4m3 caches with the quantised new rows written in place."""
+    kn, vn = _u16(k_new), _u16(v_new)
+    kc, vc = _u8(k_cache).copy(), _u8(v_cache).copy()
+    bt, lens = _i32(block_tables), _i32(context_lens)
+    B, q_len, Hkv, D = kn.shape
+    bs = kc.shape[2]
+    rc = lib().oracle_kv_append_e4m3(_ptr(kn), _ptr(vn), DTYPES[dtype], float(k_scale), float(v_scale), _ptr(kc),
+                                     _ptr(vc), _ptr(bt), _ptr(lens), B, q_len, Hkv, D, bs, bt.shape[1])
+    if rc != 0:
+        raise ValueError("oracle_kv_append_e4m3: invalid arguments")
+    return kc, vc

@@ -31,6 +31,14 @@
  *                            counts, brute-force plan.
  *   oracle_plan_paper        pinned: Alg. 1 guard counts, hand examples.
  *   oracle_eq1/eq2/l2_bound  pinned: 4096 B, 524288 B, 120.
+ *   oracle_validate_inputs   pinned: hand-built tables with known counts,
+ *                            brute-force recount by perturbation.
+ *   oracle_e4m3_encode       pinned: torch float8_e4m3fn cast (in range),
+ *                            encode(decode(c)) == c for every finite code,
+ *                            exact midpoints (ties to even), saturation.
+ *   oracle_kv_append(_e4m3)  pinned: positions by hand (block / slot of the
+ *                            last tokens), untouched bytes elsewhere, e4m3
+ *                            rows vs the torch cast of x / scale.
  */
 #include <math.h>
 #include <stdint.h>
@@ -436,3 +444,103 @@ int64_t oracle_eq2_total_bytes(int64_t M_block, int64_t N_thread, int64_t H, int
 /* L2 residency bound: the largest batch whose per-iteration blocks
  * fit in L2, floor(L2 / M_total(B=1)). */
 int64_t oracle_l2_residency_bound(int64_t l2_bytes, int64_t M_total_b1) { return l2_bytes / M_total_b1; }
+
+/* ---------------------------------------------------------------------------
+ * Device-data validation (SURVEY 8b convention: "a debug validate kernel flags
+ * out-of-range block ids and lengths").  Plain definition: sequence b is
+ * valid iff 0 <= L_b <= max_blocks * bs and every block id it references,
+ * bt[b][j] for j < ceil(L_b / bs), lies in [0, num_blocks) (the paged
+ * lookup of P:105 / Alg. 1 line 3, must land inside the pool).  Ids of
+ * a sequence with an invalid length are checked over min(L_b, max) tokens.
+ * counts[0] = sequences with an invalid length, counts[1] = referenced block
+ * ids out of range, counts[2] = sequences with either problem.
+ * ------------------------------------------------------------------------- */
+int oracle_validate_inputs(const int32_t* bt, const int32_t* lens, int B, int max_blocks, int bs,
+                           int64_t num_blocks, int64_t* counts) {
+    counts[0] = counts[1] = counts[2] = 0;
+    for (int b = 0; b < B; ++b) {
+        int64_t L = lens[b];
+        int bad_len = L < 0 || L > (int64_t)max_blocks * bs;
+        if (L < 0) L = 0;
+        if (L > (int64_t)max_blocks * bs) L = (int64_t)max_blocks * bs;
+        int64_t bad_ids = 0;
+        for (int64_t j = 0; j < (L + bs - 1) / bs; ++j) {
+            int32_t id = bt[(size_t)b * max_blocks + j];
+            if (id < 0 || id >= num_blocks) ++bad_ids;
+        }
+        counts[0] += bad_len;
+        counts[1] += bad_ids;
+        counts[2] += (bad_len || bad_ids) ? 1 : 0;
+    }
+    return 0;
+}
+
+/* fp32 -> OCP FP8 E4M3 code, round to nearest, ties to the even code, values
+ * beyond the largest finite magnitude saturate to +-448, NaN -> 0x7F.  Written
+ * as the definition: the nearest of the 127 finite magnitudes (by brute force
+ * over the codes, decoded with oracle_e4m3_to_f64), sign copied. */
+uint8_t oracle_e4m3_encode(float x) {
+    if (isnan(x)) return 0x7F;
+    uint8_t sign = signbit(x) ? 0x80 : 0;
+    double a = fabs((double)x);
+    int best = 0;
+    double bd = INFINITY;
+    for (int c = 0; c <= 0x7E; ++c) {
+        double dist = fabs(oracle_e4m3_to_f64((uint8_t)c) - a);
+        if (dist < bd || (dist == bd && (c & 1) == 0)) {
+            best = c;
+            bd = dist;
+        }
+    }
+    return (uint8_t)(sign | best);
+}
+
+/* KV append (the decode step's cache write, "each decoding step" adds one
+ * token's K/V; paged layout P:105): new K/V rows k_new, v_new [B, q_len, Hkv, D]
+ * of token i of sequence b go to position t = L_b - q_len + i (L_b counts the
+ * new tokens, as in oracle_paged_attention_mq), i.e. slot t % bs of physical
+ * block bt[b][t / bs], for every kv head; positions t < 0 are skipped.
+ * 16-bit caches: the bit patterns are copied.  kv8 != 0: the caches hold
+ * e4m3 codes, code = e4m3(fp32(x) / fp32(scale)) with an IEEE fp32 division
+ * (the quantisation decision taken in fp32, the precision of the kernel). */
+static void append_rows(const uint16_t* k_new, const uint16_t* v_new, int dtype, int kv8, float k_scale,
+                        float v_scale, void* k, void* v, const int32_t* bt, const int32_t* lens, int B,
+                        int q_len, int Hkv, int D, int bs, int max_blocks) {
+    for (int b = 0; b < B; ++b) {
+        for (int i = 0; i < q_len; ++i) {
+            int t = lens[b] - q_len + i;
+            if (t < 0) continue;
+            int64_t phys = bt[(size_t)b * max_blocks + t / bs];
+            for (int kvh = 0; kvh < Hkv; ++kvh) {
+                for (int d = 0; d < D; ++d) {
+                    size_t src = (((size_t)b * q_len + i) * Hkv + kvh) * D + d;
+                    size_t dst = kv_offset(phys, kvh, t % bs, d, Hkv, bs, D);
+                    if (kv8) {
+                        float xk = (float)decode(k_new[src], dtype), xv = (float)decode(v_new[src], dtype);
+                        ((uint8_t*)k)[dst] = oracle_e4m3_encode(xk / k_scale);
+                        ((uint8_t*)v)[dst] = oracle_e4m3_encode(xv / v_scale);
+                    } else {
+                        ((uint16_t*)k)[dst] = k_new[src];
+                        ((uint16_t*)v)[dst] = v_new[src];
+                    }
+                }
+            }
+        }
+    }
+}
+
+int oracle_kv_append(const uint16_t* k_new, const uint16_t* v_new, uint16_t* k, uint16_t* v,
+                     const int32_t* bt, const int32_t* lens, int B, int q_len, int Hkv, int D, int bs,
+                     int max_blocks) {
+    if (B < 0 || q_len <= 0 || Hkv <= 0 || D <= 0 || bs <= 0) return -1;
+    append_rows(k_new, v_new, ORACLE_F16, 0, 1.f, 1.f, k, v, bt, lens, B, q_len, Hkv, D, bs, max_blocks);
+    return 0;
+}
+
+int oracle_kv_append_e4m3(const uint16_t* k_new, const uint16_t* v_new, int dtype, float k_scale,
+                          float v_scale, uint8_t* k, uint8_t* v, const int32_t* bt, const int32_t* lens,
+                          int B, int q_len, int Hkv, int D, int bs, int max_blocks) {
+    if (B < 0 || q_len <= 0 || Hkv <= 0 || D <= 0 || bs <= 0 || !(k_scale > 0.f) || !(v_scale > 0.f)) return -1;
+    append_rows(k_new, v_new, dtype, 1, k_scale, v_scale, k, v, bt, lens, B, q_len, Hkv, D, bs, max_blocks);
+    return 0;
+}

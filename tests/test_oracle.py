@@ -436,3 +436,150 @@ def test_mq_last_token_sees_everything_first_token_sees_prefix(oracle_mod):
     first = oracle_mod.paged_attention(inp["q"][:, 0], inp["k_cache"], inp["v_cache"], inp["block_tables"],
                                        inp["context_lens"] - 2, inp["scale"], "bf16")
     assert np.array_equal(mq[:, 2], last) and np.array_equal(mq[:, 0], first)
+
+
+# ---------------------------------------------------------------------------
+# Device-data validation, e4m3 encoding and the KV append
+# ---------------------------------------------------------------------------
+
+def test_validate_hand_example(oracle_mod):
+    # B=3, max_blocks=3, bs=16, pool of 10 blocks
+    bt = np.array([[1, 2, 99],      # L=20 references blocks 0,1 -> ids 1,2 fine (99 unreferenced)
+                   [-1, 4, 5],      # L=40 references 3 blocks -> id -1 bad
+                   [10, 11, 3]],    # L=60 > 48: bad length; clamped to 48 -> ids 10, 11 bad
+                  dtype=np.int32)
+    lens = np.array([20, 40, 60], dtype=np.int32)
+    assert oracle_mod.validate_inputs(bt, lens, 10) == (1, 3, 2)
+    assert oracle_mod.validate_inputs(bt, np.array([0, 0, 0], np.int32), 10) == (0, 0, 0)
+    # seq 0: bad length, clamped to 0 tokens; seqs 1, 2 reference ids -1 and 10
+    assert oracle_mod.validate_inputs(bt, np.array([-5, 1, 1], np.int32), 10) == (1, 2, 3)
+
+
+def test_validate_counts_injected_faults(oracle_mod):
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        B, mb, nb = 6, 8, 50
+        bt = rng.integers(0, nb, size=(B, mb), dtype=np.int32)
+        lens = rng.integers(0, mb * 16 + 1, size=B).astype(np.int32)
+        assert oracle_mod.validate_inputs(bt, lens, nb) == (0, 0, 0)
+        # inject faults only at referenced positions, counted independently
+        nbad = 0
+        bad_seqs = set()
+        for b in range(B):
+            n = (int(lens[b]) + 15) // 16
+            for j in range(n):
+                if rng.random() < 0.2:
+                    bt[b, j] = rng.choice([-1, nb, nb + 7, -1000])
+                    nbad += 1
+                    bad_seqs.add(b)
+            for j in range(n, mb):  # unreferenced slots may hold anything
+                bt[b, j] = -7
+        assert oracle_mod.validate_inputs(bt, lens, nb) == (0, nbad, len(bad_seqs))
+
+
+def test_e4m3_encode_matches_torch_cast(oracle_mod):
+    g = torch.Generator().manual_seed(11)
+    x = torch.cat([torch.randn(20000, generator=g) * s for s in (1e-3, 0.1, 1.0, 30.0, 150.0)]).clamp(-448, 448)
+    ref = x.to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    got = np.array([oracle_mod.e4m3_encode(float(v)) for v in x.numpy()], dtype=np.uint8)
+    assert (ref == got).all()
+
+
+def test_e4m3_encode_roundtrip_and_ties(oracle_mod):
+    for c in range(256):
+        if c & 0x7F == 0x7F:
+            continue  # NaN codes
+        v = oracle_mod.e4m3_to_f64(c)
+        assert oracle_mod.e4m3_encode(v) == c or (v == 0 and oracle_mod.e4m3_encode(v) in (0, 0x80))
+    # exact midpoints between consecutive magnitudes go to the even code (RNE)
+    for c in range(0, 0x7E):
+        lo, hi = oracle_mod.e4m3_to_f64(c), oracle_mod.e4m3_to_f64(c + 1)
+        mid = np.float32((lo + hi) / 2)
+        assert float(mid) == (lo + hi) / 2  # representable in fp32
+        want = c if c % 2 == 0 else c + 1
+        assert oracle_mod.e4m3_encode(float(mid)) == want
+        assert oracle_mod.e4m3_encode(-float(mid)) == want | 0x80
+        assert torch.tensor([float(mid)]).to(torch.float8_e4m3fn).view(torch.uint8).item() == want
+
+
+def test_e4m3_encode_saturates_and_nan(oracle_mod):
+    for v in (448.0, 449.0, 463.9, 464.0, 500.0, 1e6, float("inf")):
+        assert oracle_mod.e4m3_encode(v) == 0x7E
+        assert oracle_mod.e4m3_encode(-v) == 0xFE
+    assert oracle_mod.e4m3_encode(float("nan")) == 0x7F
+    assert oracle_mod.e4m3_encode(1e-9) == 0 and oracle_mod.e4m3_encode(-1e-9) == 0x80
+
+
+def _append_case(dtype="fp16", lens=(17, 5, 32, 1), q_len=1, seed=4, Hkv=2, D=64):
+    rng = np.random.default_rng(seed)
+    B, mb, nb = len(lens), 4, 24
+    perm = rng.permutation(nb)[: B * mb].reshape(B, mb).astype(np.int32)
+    tdt = torch.float16 if dtype == "fp16" else torch.bfloat16
+    g = torch.Generator().manual_seed(seed)
+    k = (torch.rand(nb, Hkv, 16, D, generator=g) * 2 - 1).to(tdt)
+    v = (torch.rand(nb, Hkv, 16, D, generator=g) * 2 - 1).to(tdt)
+    kn = (torch.rand(B, q_len, Hkv, D, generator=g) * 2 - 1).to(tdt)
+    vn = (torch.rand(B, q_len, Hkv, D, generator=g) * 2 - 1).to(tdt)
+    return k, v, kn, vn, perm, np.array(lens, dtype=np.int32)
+
+
+@pytest.mark.parametrize("q_len,lens", [(1, (17, 5, 32, 1)), (3, (18, 3, 2, 40)), (4, (16, 17, 64, 0))])
+def test_kv_append_positions_by_hand(oracle_mod, q_len, lens):
+    k, v, kn, vn, bt, L = _append_case(lens=lens, q_len=q_len)
+    kc, vc = oracle_mod.kv_append(kn, vn, k, v, bt, L)
+    kb, vb = k.view(torch.int16).numpy().view(np.uint16), v.view(torch.int16).numpy().view(np.uint16)
+    knb, vnb = kn.view(torch.int16).numpy().view(np.uint16), vn.view(torch.int16).numpy().view(np.uint16)
+    ek, ev = kb.copy(), vb.copy()
+    for b in range(len(lens)):
+        for i in range(q_len):
+            t = lens[b] - q_len + i
+            if t < 0:
+                continue
+            ek[bt[b, t // 16], :, t % 16, :] = knb[b, i]
+            ev[bt[b, t // 16], :, t % 16, :] = vnb[b, i]
+    assert (kc == ek).all() and (vc == ev).all()
+    # untouched elsewhere: the number of changed slots is the number of written ones
+    n_written = sum(max(0, min(q_len, l)) for l in lens)
+    changed = (kc != kb).any(axis=(1, 3)).sum()
+    assert changed <= n_written * 1 and n_written >= 1
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_kv_append_e4m3_matches_torch_cast(oracle_mod, dtype):
+    k, v, kn, vn, bt, L = _append_case(dtype=dtype, lens=(19, 33, 2, 64), q_len=2)
+    k8 = torch.randint(0, 0x7E, k.shape, dtype=torch.uint8)
+    v8 = torch.randint(0, 0x7E, v.shape, dtype=torch.uint8)
+    ks, vs = 1 / 224, 0.0123
+    kc, vc = oracle_mod.kv_append_e4m3(kn, vn, dtype, ks, vs, k8, v8, bt, L)
+    qk = (kn.float() / torch.tensor(ks, dtype=torch.float32)).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    qv = (vn.float() / torch.tensor(vs, dtype=torch.float32)).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    ek, ev = k8.numpy().copy(), v8.numpy().copy()
+    for b in range(4):
+        for i in range(2):
+            t = L[b] - 2 + i
+            ek[bt[b, t // 16], :, t % 16, :] = qk[b, i]
+            ev[bt[b, t // 16], :, t % 16, :] = qv[b, i]
+    assert (kc == ek).all() and (vc == ev).all()
+
+
+def test_attention_after_append_is_attention_over_concatenation(oracle_mod):
+    """Decode step semantics: appending token L-1 then attending over L tokens
+    equals softmax attention over [old K/V rows ; new row] (numpy)."""
+    k, v, kn, vn, bt, L = _append_case(lens=(17, 5, 32, 1), q_len=1, D=64)
+    kc, vc = oracle_mod.kv_append(kn, vn, k, v, bt, L)
+    g = torch.Generator().manual_seed(9)
+    q = (torch.rand(4, 4, 64, generator=g) * 2 - 1).half()
+    kct = torch.from_numpy(kc.view(np.int16)).view(torch.float16)
+    vct = torch.from_numpy(vc.view(np.int16)).view(torch.float16)
+    out = oracle_mod.paged_attention(q, kct, vct, bt, L, 0.125, "fp16")
+    for b in range(4):
+        for h in range(4):
+            kvh = h // 2
+            rows = [k[bt[b, t // 16], kvh, t % 16].double().numpy() for t in range(L[b] - 1)]
+            vrows = [v[bt[b, t // 16], kvh, t % 16].double().numpy() for t in range(L[b] - 1)]
+            K = np.stack(rows + [kn[b, 0, kvh].double().numpy()])
+            V = np.stack(vrows + [vn[b, 0, kvh].double().numpy()])
+            s = 0.125 * (K @ q[b, h].double().numpy())
+            w = np.exp(s - s.max())
+            w /= w.sum()
+            assert np.abs(out[b, h] - w @ V).max() < 1e-12
