@@ -358,6 +358,43 @@ def main():
                                      "tokens_per_s": cfg.num_seqs / (ms8 * 1e-3),
                                      "desc": "K/V as OCP e4m3 codes + per-tensor scales, 1 B/element"}
                 del q8, ws8
+            # the decode step with its KV append (SURVEY 8f NEXT f3 alternative):
+            # fused into the split-K kernel vs a separate append launch first
+            kn, vn = synth.new_kv_rows(inp, 1, seed=rank)
+
+            def app_fused():
+                pda.paged_decode_attention(q, inp["k_cache"], inp["v_cache"], bt, lens, scale,
+                                           out=step_main.out_local, workspace=step_main.ws, k_new=kn, v_new=vn,
+                                           **opt_kw)
+
+            def app_separate():
+                pda.kv_append(kn, vn, inp["k_cache"], inp["v_cache"], bt, lens)
+                pda.paged_decode_attention(q, inp["k_cache"], inp["v_cache"], bt, lens, scale,
+                                           out=step_main.out_local, workspace=step_main.ws, **opt_kw)
+
+            def app_none():
+                pda.paged_decode_attention(q, inp["k_cache"], inp["v_cache"], bt, lens, scale,
+                                           out=step_main.out_local, workspace=step_main.ws, **opt_kw)
+
+            app_arms = {"fused": app_fused, "separate": app_separate, "attention_only": app_none}
+            app_per = {k: [] for k in app_arms}
+            for fn in app_arms.values():
+                fn()
+            torch.cuda.synchronize()
+            for _ in range(max(10, args.steps // 4)):
+                for k, fn in app_arms.items():
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    app_per[k].append((e0, e1))
+            torch.cuda.synchronize()
+            am = {k: statistics.median(a.elapsed_time(b) for a, b in v) * 1e3 for k, v in app_per.items()}
+            extras["kv_append"] = {
+                "fused_us": am["fused"], "separate_us": am["separate"], "attention_only_us": am["attention_only"],
+                "desc": "step = append the new token's K/V into its paged slot + attention; fused: the split-K "
+                        "CTA owning the slot writes it before its TMA loads (one launch fewer)"}
+            del kn, vn
             # in-run read roofline (read-only stream over a 4 GiB buffer)
             buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
             sink = torch.zeros(4, dtype=torch.int32, device="cuda")

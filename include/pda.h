@@ -20,7 +20,8 @@
  *    launch failures map to PDA_ERR_CUDA.  No C++ exception crosses the ABI.
  *  - Device-resident values (block ids, lengths) are not validated: a block
  *    id outside [0, num_blocks) is undefined behaviour; context_lens[b] is
- *    clamped to max_blocks_per_seq * block_size.
+ *    clamped to max_blocks_per_seq * block_size.  pda_validate_inputs is
+ *    the debug check that flags them.
  *  - Layouts (all row-major, contiguous):
  *      q, out        [num_seqs, num_q_heads, head_dim]
  *      k_cache/v_cache [num_blocks, num_kv_heads, block_size, head_dim]
@@ -233,6 +234,46 @@ pda_status paged_decode_attention_gather(const void* q, const void* k_cache, con
                                          const pda_shape* shape, const pda_options* opt, void* workspace,
                                          size_t workspace_bytes, void* stream);
 
+/* KV append, the decode step's cache write ("each decoding step requires
+ * loading the KV Cache" of all tokens so far; paged layout P:105): the
+ * step's q_len new tokens (q_len = shape->q_len, 0 means 1) of each sequence
+ * are written into their paged slots.  Token i of sequence b goes to position
+ * t = L_b - q_len + i (L_b = context_lens[b] counts the new tokens), i.e. slot
+ * t % bs of physical block block_tables[b][t / bs], for every kv head;
+ * positions t < 0 are skipped.
+ *   k_new, v_new  [B, q_len, Hkv, D] dtype             (device, read)
+ *   k_cache, v_cache                                   (device, written)
+ * 16-bit caches receive the bit patterns; an e4m3 cache (kv_dtype E4M3)
+ * receives code = e4m3(fp32(x) / opt->k_scale) (resp. v_scale): IEEE fp32
+ * division, then round to nearest even, saturating to +-448 (scales must be
+ * > 0: PDA_ERR_SHAPE otherwise).  The written slots must not be shared with
+ * another sequence of the same call (they never are in a paged cache: a
+ * sequence's last block is its own). */
+pda_status pda_kv_append(const void* k_new, const void* v_new, void* k_cache, void* v_cache,
+                         const int32_t* block_tables, const int32_t* context_lens, const pda_shape* shape,
+                         const pda_options* opt, void* stream);
+
+/* pda_kv_append followed by paged_decode_attention on the updated cache, as
+ * one call.  The split-K kernel fuses the append: the CTA whose partition
+ * holds a new token writes it before loading its blocks (one launch fewer);
+ * the other kernels run pda_kv_append's kernel first on the same stream.
+ * Output identical to the two separate calls (bitwise). */
+pda_status paged_decode_attention_append(const void* q, const void* k_new, const void* v_new, void* k_cache,
+                                         void* v_cache, const int32_t* block_tables,
+                                         const int32_t* context_lens, float scale, void* out,
+                                         const pda_shape* shape, const pda_options* opt, void* workspace,
+                                         size_t workspace_bytes, void* stream);
+
+/* Debug validation of the device-resident inputs the hot path does not check
+ * (block ids, lengths): counts (DEVICE, int64 x 3, written) receives
+ *   [0] sequences with context_lens[b] outside [0, max_blocks_per_seq * bs],
+ *   [1] referenced block ids (block_tables[b][j], j < ceil(min(L_b, max) / bs))
+ *       outside [0, num_blocks),
+ *   [2] sequences with either problem.
+ * Uses num_seqs, max_blocks_per_seq, num_blocks and block_size of `shape`. */
+pda_status pda_validate_inputs(const int32_t* block_tables, const int32_t* context_lens,
+                               const pda_shape* shape, int64_t* counts, void* stream);
+
 /* End-to-end decode step from HOST buffers: copies this step's inputs
  * (q, block_tables, context_lens; pinned host memory recommended) to the
  * device staging buffers, runs paged_decode_attention against the
@@ -257,7 +298,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
+int32_t pda_abi_version(void);  /* 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
 
 #ifdef __cplusplus
 }

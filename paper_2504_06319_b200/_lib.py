@@ -90,6 +90,12 @@ def lib():
             L.paged_decode_attention_gather.restype = i32
             L.pda_decode_step_host.argtypes = [p, p, p, p, p, p, p, p, p, p, f32, ps, po, p, sz, p]
             L.pda_decode_step_host.restype = i32
+            L.pda_kv_append.argtypes = [p, p, p, p, p, p, ps, po, p]
+            L.pda_kv_append.restype = i32
+            L.paged_decode_attention_append.argtypes = [p, p, p, p, p, p, p, f32, p, ps, po, p, sz, p]
+            L.paged_decode_attention_append.restype = i32
+            L.pda_validate_inputs.argtypes = [p, p, ps, p, p]
+            L.pda_validate_inputs.restype = i32
             L.pda_read_roofline.argtypes = [p, sz, p, p]
             L.pda_read_roofline.restype = i32
             L.pda_status_string.argtypes = [i32]
@@ -186,16 +192,30 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
                            num_sms=0, eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0,
-                           issue_mode=0, workspace=None, stream=None, trace=False):
+                           issue_mode=0, workspace=None, stream=None, trace=False, k_new=None, v_new=None):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16 like q, or
     uint8/float8_e4m3fn e4m3 codes dequantised with k_scale / v_scale),
     block_tables [B, max_blocks] int32, context_lens [B] int32, all CUDA.
+    k_new/v_new [B, (q_len,) Hkv, D]: append the step's new tokens to the
+    caches first (paged_decode_attention_append; fused in the split-K kernel).
     Returns out [B, Hq, D] (and the int32 bookkeeping trace if trace=True).
     """
     import torch
     _require_cuda(q, k_cache, v_cache, block_tables, context_lens)
+    if (k_new is None) != (v_new is None):
+        raise ValueError("k_new and v_new go together")
+    if k_new is not None:
+        _require_cuda(k_new, v_new)
+        if trace:
+            raise ValueError("trace and append are separate calls")
+        if k_new.dtype != q.dtype or v_new.dtype != q.dtype:
+            raise TypeError("k_new / v_new must have q's dtype")
+        q_len = q.shape[1] if q.dim() == 4 else 1
+        want = q.shape[0] * q_len * k_cache.shape[1] * k_cache.shape[3]
+        if k_new.numel() != want or v_new.numel() != want:
+            raise ValueError("k_new / v_new must be [B, q_len, Hkv, D]")
     if block_tables.dtype != torch.int32 or context_lens.dtype != torch.int32:
         raise TypeError("block_tables / context_lens must be int32")
     if out is not None:
@@ -228,12 +248,57 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
             ctypes.byref(opts), ws_ptr, wsb, tr.data_ptr(), words, s)
         _check(st, "paged_decode_attention_trace")
         return out, tr, info
+    if k_new is not None:
+        st = L.paged_decode_attention_append(
+            q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+            block_tables.data_ptr(), context_lens.data_ptr(), float(scale), out.data_ptr(), ctypes.byref(shape),
+            ctypes.byref(opts), ws_ptr, wsb, s)
+        _check(st, "paged_decode_attention_append")
+        return out
     st = L.paged_decode_attention(
         q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(),
         context_lens.data_ptr(), float(scale), out.data_ptr(), ctypes.byref(shape), ctypes.byref(opts),
         ws_ptr, wsb, s)
     _check(st, "paged_decode_attention")
     return out
+
+
+def kv_append(k_new, v_new, k_cache, v_cache, block_tables, context_lens, *, k_scale=0.0, v_scale=0.0,
+              stream=None):
+    """Write the step's new K/V rows [B, (q_len,) Hkv, D] into their paged slots
+    (positions context_lens[b] - q_len + i; include/pda.h pda_kv_append)."""
+    import torch
+    _require_cuda(k_new, v_new, k_cache, v_cache, block_tables, context_lens)
+    if k_new.shape != v_new.shape or k_new.dtype != v_new.dtype:
+        raise ValueError("k_new / v_new differ")
+    if block_tables.dtype != torch.int32 or context_lens.dtype != torch.int32:
+        raise TypeError("block_tables / context_lens must be int32")
+    q_len = k_new.shape[1] if k_new.dim() == 4 else 1
+    B, Hkv, D = k_new.shape[0], k_new.shape[-2], k_new.shape[-1]
+    nb, Hkv2, bs, D2 = k_cache.shape
+    if (Hkv2, D2) != (Hkv, D):
+        raise ValueError("k_new and k_cache disagree on (Hkv, D)")
+    shape = Shape(B, Hkv, Hkv, D, bs, nb, block_tables.shape[1], _dtype_code(k_new.dtype),
+                  _dtype_code(k_new.dtype), _dtype_code(k_cache.dtype), q_len)
+    opts = make_options(k_scale=k_scale, v_scale=v_scale)
+    _check(lib().pda_kv_append(k_new.data_ptr(), v_new.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+                               block_tables.data_ptr(), context_lens.data_ptr(), ctypes.byref(shape),
+                               ctypes.byref(opts), _stream_handle(stream)), "pda_kv_append")
+
+
+def validate_inputs(block_tables, context_lens, num_blocks, block_size=16, stream=None):
+    """Debug check of device-resident tables/lengths (pda_validate_inputs):
+    returns (invalid lengths, out-of-range referenced block ids, invalid sequences)."""
+    import torch
+    _require_cuda(block_tables, context_lens)
+    if block_tables.dtype != torch.int32 or context_lens.dtype != torch.int32:
+        raise TypeError("block_tables / context_lens must be int32")
+    counts = torch.empty(3, dtype=torch.int64, device=block_tables.device)
+    shape = Shape(context_lens.shape[0], 1, 1, 128, block_size, int(num_blocks), block_tables.shape[1],
+                  PDA_F16, PDA_F16, PDA_F16, 1)
+    _check(lib().pda_validate_inputs(block_tables.data_ptr(), context_lens.data_ptr(), ctypes.byref(shape),
+                                     counts.data_ptr(), _stream_handle(stream)), "pda_validate_inputs")
+    return tuple(int(c) for c in counts.cpu())
 
 
 def paged_decode_attention_gather(q, k_cache, v_cache, block_tables, context_lens, scale, out_peers,

@@ -22,7 +22,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpda.so")
 
-SOURCES = ["pda.cu", "decode_splitk.cu", "decode_stream.cu", "decode_balanced.cu", "decode_paper.cu", "roofline.cu"]
+SOURCES = ["pda.cu", "decode_splitk.cu", "decode_stream.cu", "decode_balanced.cu", "decode_paper.cu", "roofline.cu",
+           "kv_cache.cu"]
 HEADERS = ["ptx.cuh", "kernels.cuh", "block_math.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

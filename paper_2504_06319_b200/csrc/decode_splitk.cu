@@ -19,6 +19,7 @@
 //    otherwise the normalised partial and its log2-sum-exp go to the
 //    workspace and combine_kernel (S8) merges partitions in fixed order.
 #include "block_math.cuh"
+#include "kv_append.cuh"
 
 namespace pda {
 
@@ -110,6 +111,25 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     const int sb = s_tok / kBlockSize;
     const int n = (e_tok + kBlockSize - 1) / kBlockSize - sb;  // blocks in this unit
     const int n_parts = (L + P - 1) / P;
+
+    if (p.app.k_new != nullptr) {
+        // Fused KV append: the step's new tokens that fall in [s_tok, e_tok)
+        // are written by this unit before any of its loads (partitions are
+        // whole blocks, so no other CTA reads these slots); the proxy fence +
+        // the __syncthreads below order the stores before the TMA reads.
+        const int first_new = L - p.q_len;
+        const int t0 = first_new > s_tok ? first_new : s_tok;
+        const int rows = e_tok - t0;
+        if (rows > 0) {
+            constexpr int CH = D / 8;
+            for (int c = threadIdx.x; c < rows * 2 * CH; c += blockDim.x) {
+                const int t = t0 + c / (2 * CH);
+                append_chunk(p.app, p.bt, p.max_blocks, p.q_len, p.Hkv, D, b, t - first_new, kvh, t,
+                             (c / CH) & 1, c % CH);
+            }
+            fence_proxy_async_global();
+        }
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {

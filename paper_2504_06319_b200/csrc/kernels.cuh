@@ -27,6 +27,19 @@ struct OutPeers {
     int Hq_out;
 };
 
+// KV append (the decode step's cache write, SURVEY 8f NEXT f3 alternative):
+// the new tokens' K/V rows k_new/v_new [B, q_len, Hkv, D] (dtype) go to
+// positions L_b - q_len + i of their sequence's paged cache.  k_new == nullptr:
+// no append.  An e4m3 cache stores e4m3(x / scale) (fp32 division).
+struct AppendParams {
+    const uint16_t* k_new;
+    const uint16_t* v_new;
+    uint8_t* k;  // the caches, as bytes
+    uint8_t* v;
+    int kv8, bf16;
+    float k_scale, v_scale;
+};
+
 struct SplitKParams {
     const uint16_t* q;  // [B, Hq, D]
     const uint8_t* k;   // [num_blocks, Hkv, 16, D] (bytes: prefetch addresses)
@@ -45,6 +58,7 @@ struct SplitKParams {
     int trace_rec_len;
     float scale_log2;  // scale * log2(e) (* k_scale for an e4m3 cache), fp32
     float out_scale;   // v_scale for an e4m3 cache, else 1
+    AppendParams app;  // fused KV append (app.k_new == nullptr: none)
 };
 
 struct PaperParams {
@@ -134,6 +148,17 @@ cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t st
 
 cudaError_t launch_paper(const PaperParams& p, bool bf16, int head_dim, bool trace, dim3 grid,
                          cudaStream_t stream);
+
+// Standalone KV append (every kernel other than split-K, and the unfused
+// comparison): one launch writing all B * q_len * Hkv new rows.
+cudaError_t launch_kv_append(const AppendParams& a, const int32_t* bt, const int32_t* lens, int B,
+                             int q_len, int Hkv, int head_dim, int max_blocks, cudaStream_t stream);
+
+// Debug validation of the device-resident block tables / lengths:
+// counts[0..3) (int64, device) = invalid lengths, out-of-range referenced
+// block ids, invalid sequences.
+cudaError_t launch_validate(const int32_t* bt, const int32_t* lens, int B, int max_blocks,
+                            int64_t num_blocks, long long* counts, cudaStream_t stream);
 
 cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms,
                                  cudaStream_t stream);

@@ -256,11 +256,30 @@ pda_status use_device_of(const void* ptr) {
     return PDA_OK;
 }
 
+// AppendParams of a call; validates the extra pointers.
+pda_status make_append(const void* k_new, const void* v_new, void* k_cache, void* v_cache,
+                       const pda_shape* s, const pda_options* o, pda::AppendParams* a) {
+    if (!k_new || !v_new || !k_cache || !v_cache) return PDA_ERR_NULL;
+    if (!aligned16(k_new) || !aligned16(v_new) || !aligned16(k_cache) || !aligned16(v_cache))
+        return PDA_ERR_ALIGN;
+    const bool kv8 = s->kv_dtype == PDA_E4M3;
+    if (kv8 && !(o->k_scale > 0.f && o->v_scale > 0.f)) return PDA_ERR_SHAPE;  // encoding needs the scales
+    a->k_new = static_cast<const uint16_t*>(k_new);
+    a->v_new = static_cast<const uint16_t*>(v_new);
+    a->k = static_cast<uint8_t*>(k_cache);
+    a->v = static_cast<uint8_t*>(v_cache);
+    a->kv8 = kv8;
+    a->bf16 = s->dtype == PDA_BF16;
+    a->k_scale = kv8 ? o->k_scale : 1.f;
+    a->v_scale = kv8 ? o->v_scale : 1.f;
+    return PDA_OK;
+}
+
 pda_status run(const void* q, const void* k_cache, const void* v_cache, const int32_t* bt,
                const int32_t* lens, float scale, void* out, const pda_shape* s,
                const pda_options* o, void* ws, size_t ws_bytes, int32_t* trace, size_t trace_words,
                cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0, int head_off = 0,
-               int hq_out = 0) {
+               int hq_out = 0, const pda::AppendParams* app = nullptr) {
     pda_plan_info pl;
     pda_status st = plan(s, o, &pl);
     if (st != PDA_OK) return st;
@@ -282,6 +301,12 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         return PDA_ERR_CUDA;
 
     cudaError_t err;
+    if (app && pl.kernel != PDA_KERNEL_SPLITK) {
+        // KV append as its own launch ahead of the kernels that do not fuse it
+        err = pda::launch_kv_append(*app, bt, lens, s->num_seqs, q_tokens(s), s->num_kv_heads, s->head_dim,
+                                    s->max_blocks_per_seq, stream);
+        if (err != cudaSuccess) return PDA_ERR_CUDA;
+    }
     if (pl.kernel == PDA_KERNEL_PAPER) {
         pda::PaperParams p{};
         p.q = static_cast<const uint16_t*>(q);
@@ -407,6 +432,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.q_len = q_tokens(s);
     p.scale_log2 = (float)((double)scale * k_scale * 1.4426950408889634);
     p.out_scale = kv8 && o->v_scale > 0.f ? o->v_scale : 1.f;
+    if (app) p.app = *app;  // fused into the split-K kernel (else p.app.k_new == nullptr)
     const int n_tiles = p.q_len * p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,
@@ -494,6 +520,54 @@ pda_status paged_decode_attention_gather(const void* q, const void* k_cache, con
                total_q_heads);
 }
 
+pda_status pda_kv_append(const void* k_new, const void* v_new, void* k_cache, void* v_cache,
+                         const int32_t* block_tables, const int32_t* context_lens, const pda_shape* shape,
+                         const pda_options* opt, void* stream) {
+    pda_status st = validate(shape, opt);
+    if (st != PDA_OK) return st;
+    if (!block_tables || !context_lens) return PDA_ERR_NULL;
+    pda::AppendParams a{};
+    st = make_append(k_new, v_new, k_cache, v_cache, shape, opt, &a);
+    if (st != PDA_OK) return st;
+    if (shape->num_seqs == 0) return PDA_OK;
+    st = use_device_of(k_cache);
+    if (st != PDA_OK) return st;
+    return pda::launch_kv_append(a, block_tables, context_lens, shape->num_seqs, q_tokens(shape),
+                                 shape->num_kv_heads, shape->head_dim, shape->max_blocks_per_seq,
+                                 static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? PDA_OK
+               : PDA_ERR_CUDA;
+}
+
+pda_status paged_decode_attention_append(const void* q, const void* k_new, const void* v_new, void* k_cache,
+                                         void* v_cache, const int32_t* block_tables,
+                                         const int32_t* context_lens, float scale, void* out,
+                                         const pda_shape* shape, const pda_options* opt, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+    pda_status st = validate(shape, opt);
+    if (st != PDA_OK) return st;
+    pda::AppendParams a{};
+    st = make_append(k_new, v_new, k_cache, v_cache, shape, opt, &a);
+    if (st != PDA_OK) return st;
+    return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
+               workspace_bytes, nullptr, 0, static_cast<cudaStream_t>(stream), nullptr, 0, 0, 0, &a);
+}
+
+pda_status pda_validate_inputs(const int32_t* block_tables, const int32_t* context_lens,
+                               const pda_shape* shape, int64_t* counts, void* stream) {
+    if (!shape || !block_tables || !context_lens || !counts) return PDA_ERR_NULL;
+    if (shape->num_seqs < 0 || shape->max_blocks_per_seq <= 0 || shape->num_blocks <= 0)
+        return PDA_ERR_SHAPE;
+    if (shape->block_size != pda::kBlockSize) return PDA_ERR_UNSUPPORTED;
+    pda_status st = use_device_of(counts);
+    if (st != PDA_OK) return st;
+    return pda::launch_validate(block_tables, context_lens, shape->num_seqs, shape->max_blocks_per_seq,
+                                shape->num_blocks, reinterpret_cast<long long*>(counts),
+                                static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? PDA_OK
+               : PDA_ERR_CUDA;
+}
+
 pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_host,
                                 const int32_t* context_lens_host, void* out_host, void* q_dev,
                                 int32_t* block_tables_dev, int32_t* context_lens_dev,
@@ -553,6 +627,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 9; }
+int32_t pda_abi_version(void) { return 10; }
 
 }  // extern "C"

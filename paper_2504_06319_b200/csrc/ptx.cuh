@@ -31,6 +31,12 @@ __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Order this thread's generic-proxy global stores before later async-proxy
+// (TMA) reads of the same bytes (the fused KV append, FENCE.VIEW.ASYNC.G).
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
@@ -204,6 +210,14 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
         __half2 h = *reinterpret_cast<__half2*>(&w);
         return __half22float2(h);
     }
+}
+
+// 2 x fp32 -> 2 OCP e4m3 codes (low byte = a), round to nearest even,
+// saturating to +-448 (F2FP.SATFINITE.E4M3).
+__device__ __forceinline__ uint16_t cvt_e4m3x2(float a, float b) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(r) : "f"(a), "f"(b));
+    return r;
 }
 
 }  // namespace pda

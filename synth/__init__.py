@@ -187,6 +187,18 @@ def with_query_tokens(inputs: dict, q_len: int, seed: int = 0) -> dict:
     return out
 
 
+def new_kv_rows(inputs: dict, q_len: int = 1, seed: int = 0):
+    """The decode step's new K/V rows to append, k_new/v_new [B, q_len, Hkv, D]
+    (U(-1, 1) in the cache dtype, or q's dtype for an e4m3 cache; same device)."""
+    cfg, q = inputs["cfg"], inputs["q"]
+    dt = q.dtype
+    g = torch.Generator(device=q.device).manual_seed(seed + 131) if q.is_cuda else torch.Generator().manual_seed(seed + 131)
+    shape = (cfg.num_seqs, q_len, cfg.num_kv_heads, cfg.head_dim)
+    k = torch.rand(shape, generator=g, device=q.device, dtype=torch.float32).mul_(2).sub_(1).to(dt)
+    v = torch.rand(shape, generator=g, device=q.device, dtype=torch.float32).mul_(2).sub_(1).to(dt)
+    return k, v
+
+
 def quantize_kv_e4m3(inputs: dict, k_scale: float = 1.0 / 224, v_scale: float = 1.0 / 224) -> dict:
     """FP8 KV-cache variant of `inputs`: K and V stored as
     OCP e4m3 codes (uint8) of x / scale with per-tensor scales, NaN poison kept

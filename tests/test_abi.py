@@ -37,7 +37,8 @@ def test_sass_targets_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
-    for mnemonic in ("UTMALDG", "UBLKPF", "HMMA.16816.F32", "LDSM", "MOVM", "SYNCS"):
+    for mnemonic in ("UTMALDG", "UBLKPF", "HMMA.16816.F32", "LDSM", "MOVM", "SYNCS",
+                     "FENCE.VIEW.ASYNC.G", "F2FP.SATFINITE.E4M3"):
         assert mnemonic in sass, f"{mnemonic} missing from SASS"
 
 
@@ -225,7 +226,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 9
+    assert pda.lib().pda_abi_version() == 10
 
 
 def test_product_never_imports_oracle():

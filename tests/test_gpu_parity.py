@@ -524,3 +524,148 @@ def test_fused_gather_rejects_bad_offsets(pda):
     with pytest.raises(pda.PdaError):
         pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
                                           dev["context_lens"], dev["scale"], [buf], 0, 8, kernel="paper")
+
+
+# ---- KV append, fused and standalone (SURVEY 8f NEXT f3 alternative) ------------
+
+APPEND_CFGS = [
+    synth.Config("app_mha", 4, 4, 4, 128, (1, 15, 17, 300), "fp16", poison_blocks=3),
+    synth.Config("app_gqa4_bf16", 3, 16, 4, 128, (100, 1000, 513), "bf16", poison_blocks=2),
+    synth.Config("app_d64", 3, 8, 2, 64, (64, 2, 0), "fp16", poison_blocks=2),
+]
+
+
+def _bytes(t):
+    return t.contiguous().view(torch.uint8).cpu().numpy().ravel()
+
+
+def _oracle_append(oracle_mod, inp, kn, vn):
+    if inp.get("kv_dtype") == "e4m3":
+        kc, vc = oracle_mod.kv_append_e4m3(kn.cpu(), vn.cpu(), inp["cfg"].dtype, inp["k_scale"], inp["v_scale"],
+                                           inp["k_cache"].cpu(), inp["v_cache"].cpu(), inp["block_tables"].cpu(),
+                                           inp["context_lens"].cpu())
+    else:
+        kc, vc = oracle_mod.kv_append(kn.cpu(), vn.cpu(), inp["k_cache"].cpu(), inp["v_cache"].cpu(),
+                                      inp["block_tables"].cpu(), inp["context_lens"].cpu())
+    return kc.view(np.uint8).ravel(), vc.view(np.uint8).ravel()
+
+
+def _as_cache(arr_u8, like):
+    t = torch.from_numpy(arr_u8.copy())
+    return t.view(like.dtype).view(like.shape) if like.dtype != torch.uint8 else t.view(like.shape)
+
+
+@pytest.mark.parametrize("cfg", APPEND_CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("q_len", [1, 3])
+@pytest.mark.parametrize("e4m3", [False, True])
+def test_kv_append_standalone_bitwise_vs_oracle(pda, oracle_mod, cfg, q_len, e4m3):
+    inp = synth.make_inputs(cfg, seed=12)
+    if e4m3:
+        inp = kv8(inp)
+    kn, vn = synth.new_kv_rows(inp, q_len, seed=3)
+    ek, ev = _oracle_append(oracle_mod, inp, kn, vn)
+    dev = to_dev(inp)
+    kw = dict(k_scale=inp["k_scale"], v_scale=inp["v_scale"]) if e4m3 else {}
+    pda.kv_append(kn.cuda(), vn.cuda(), dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"],
+                  **kw)
+    torch.cuda.synchronize()
+    assert (_bytes(dev["k_cache"]) == ek).all() and (_bytes(dev["v_cache"]) == ev).all()
+
+
+FUSED_KW = [dict(), dict(partition_tokens=16), dict(partition_tokens=64, issue_mode="producer"),
+            dict(kernel="paper"), dict(kernel="balanced"), dict(kernel="stream")]
+
+
+@pytest.mark.parametrize("cfg", APPEND_CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("kw", FUSED_KW, ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
+def test_fused_append_attention_vs_oracle(pda, oracle_mod, cfg, kw):
+    """One call = append + attention: the caches afterwards equal the oracle's
+    append bitwise, the output matches the oracle attention over the updated
+    cache, and equals the two separate calls bitwise."""
+    inp = synth.make_inputs(cfg, seed=13)
+    kn, vn = synth.new_kv_rows(inp, 1, seed=4)
+    ek, ev = _oracle_append(oracle_mod, inp, kn, vn)
+    upd = dict(inp, k_cache=_as_cache(ek, inp["k_cache"]), v_cache=_as_cache(ev, inp["v_cache"]))
+    ref = oracle_out(oracle_mod, upd)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, k_new=kn.cuda(), v_new=vn.cuda(), **kw)
+    torch.cuda.synchronize()
+    assert (_bytes(dev["k_cache"]) == ek).all() and (_bytes(dev["v_cache"]) == ev).all()
+    assert max_err(out, ref) <= TOL
+    dev2 = to_dev(inp)
+    pda.kv_append(kn.cuda(), vn.cuda(), dev2["k_cache"], dev2["v_cache"], dev2["block_tables"],
+                  dev2["context_lens"])
+    assert torch.equal(gpu(pda, dev2, **kw), out)
+
+
+@pytest.mark.parametrize("q_len,kw", [(3, dict()), (3, dict(partition_tokens=16)), (4, dict(partition_tokens=32))])
+def test_fused_append_multi_token(pda, oracle_mod, q_len, kw):
+    """q_len new tokens (they may straddle a block and a partition boundary)."""
+    cfg = synth.Config("app_mq", 3, 8, 4, 128, (18, 33, 2), "bf16", poison_blocks=2)
+    inp = synth.with_query_tokens(synth.make_inputs(cfg, seed=14), q_len)
+    kn, vn = synth.new_kv_rows(inp, q_len, seed=5)
+    ek, ev = _oracle_append(oracle_mod, inp, kn, vn)
+    upd = dict(inp, k_cache=_as_cache(ek, inp["k_cache"]), v_cache=_as_cache(ev, inp["v_cache"]))
+    ref = oracle_mod.paged_attention_mq(upd["q"], upd["k_cache"], upd["v_cache"], upd["block_tables"],
+                                        upd["context_lens"], upd["scale"], cfg.dtype)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, k_new=kn.cuda(), v_new=vn.cuda(), **kw)
+    torch.cuda.synchronize()
+    assert (_bytes(dev["k_cache"]) == ek).all() and (_bytes(dev["v_cache"]) == ev).all()
+    assert max_err(out, ref) <= TOL
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=16)], ids=["default", "p16"])
+def test_fused_append_e4m3(pda, oracle_mod, kw):
+    cfg = synth.Config("app_kv8", 3, 8, 2, 128, (200, 17, 1), "fp16", poison_blocks=2)
+    inp = kv8(synth.make_inputs(cfg, seed=15))
+    kn, vn = synth.new_kv_rows(inp, 1, seed=6)
+    ek, ev = _oracle_append(oracle_mod, inp, kn, vn)
+    upd = dict(inp, k_cache=_as_cache(ek, inp["k_cache"]), v_cache=_as_cache(ev, inp["v_cache"]))
+    ref = oracle_kv8(oracle_mod, upd)
+    dev = to_dev(inp)
+    out = gpu_kv8(pda, dev, k_new=kn.cuda(), v_new=vn.cuda(), **kw)
+    torch.cuda.synchronize()
+    assert (_bytes(dev["k_cache"]) == ek).all() and (_bytes(dev["v_cache"]) == ev).all()
+    assert max_err(out, ref) <= TOL
+
+
+def test_fused_append_full_size_c2_sampled(pda, oracle_mod):
+    """BASELINE C2 at full size in the bench launch configuration: the written
+    slots match the oracle append (all B x Hkv rows), outputs on sampled rows."""
+    cfg = synth.C2_LLAMA2_7B
+    inp = synth.make_inputs(cfg, seed=16, device="cuda")
+    kn, vn = synth.new_kv_rows(inp, 1, seed=7)
+    out = gpu(pda, inp, k_new=kn, v_new=vn)
+    torch.cuda.synchronize()
+    bt, L = inp["block_tables"].long(), inp["context_lens"].long()
+    t = L - 1
+    phys = bt[torch.arange(cfg.num_seqs, device="cuda"), t // 16]
+    assert torch.equal(inp["k_cache"][phys, :, t % 16], kn[:, 0])
+    assert torch.equal(inp["v_cache"][phys, :, t % 16], vn[:, 0])
+    seqs = [0, 31, 63]
+    sub = synth.sample_rows(inp, seqs)
+    ref = oracle_out(oracle_mod, sub)
+    assert max_err(out[seqs], ref) <= TOL
+
+
+# ---- debug validation of device-resident tables / lengths ------------------------
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_validate_inputs_matches_oracle(pda, oracle_mod, seed):
+    rng = np.random.default_rng(seed)
+    B, mb, nb = 300, 40, 5000
+    bt = rng.integers(0, nb, size=(B, mb), dtype=np.int32)
+    lens = rng.integers(0, mb * 16 + 1, size=B).astype(np.int32)
+    # faults: ids out of range anywhere (only referenced ones count), bad lengths
+    mask = rng.random((B, mb)) < 0.01
+    bt[mask] = rng.choice(np.array([-1, nb, 2**31 - 1, -2**31], dtype=np.int64), size=mask.sum()).astype(np.int32)
+    bad_len = rng.random(B) < 0.05
+    lens[bad_len] = rng.choice(np.array([-1, mb * 16 + 1, 2**31 - 1, -2**31], dtype=np.int64),
+                               size=bad_len.sum()).astype(np.int32)
+    want = oracle_mod.validate_inputs(bt, lens, nb)
+    assert want[1] > 0 and want[0] > 0
+    got = pda.validate_inputs(torch.from_numpy(bt).cuda(), torch.from_numpy(lens).cuda(), nb)
+    assert got == want
+    good = synth.make_inputs(SHAPES[1], seed=1, device="cuda")
+    assert pda.validate_inputs(good["block_tables"], good["context_lens"], good["k_cache"].shape[0]) == (0, 0, 0)
