@@ -112,24 +112,29 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     const int n = (e_tok + kBlockSize - 1) / kBlockSize - sb;  // blocks in this unit
     const int n_parts = (L + P - 1) / P;
 
-    if (p.app.k_new != nullptr) {
-        // Fused KV append: the step's new tokens that fall in [s_tok, e_tok)
-        // are written by this unit before any of its loads (partitions are
-        // whole blocks, so no other CTA reads these slots); the proxy fence +
-        // the __syncthreads below order the stores before the TMA reads.
-        const int first_new = L - p.q_len;
-        const int t0 = first_new > s_tok ? first_new : s_tok;
-        const int rows = e_tok - t0;
-        if (rows > 0) {
-            constexpr int CH = D / 8;
-            for (int c = threadIdx.x; c < rows * 2 * CH; c += blockDim.x) {
-                const int t = t0 + c / (2 * CH);
-                append_chunk(p.app, p.bt, p.max_blocks, p.q_len, p.Hkv, D, b, t - first_new, kvh, t,
-                             (c / CH) & 1, c % CH);
-            }
-            fence_proxy_async_global();
+    // Fused KV append: the step's new tokens in [t_new0, e_tok) are written by
+    // the warp that issues the TMA load of their block, before that issue
+    // (partitions are whole blocks, so no other CTA reads these slots).  All
+    // lanes store, fence the generic->async proxy, __syncwarp; then lane 0
+    // issues the load.
+    const int first_new = L - p.q_len;
+    const int t_new0 = p.app.k_new == nullptr ? e_tok : (first_new > s_tok ? first_new : s_tok);
+    auto write_new = [&](int pos) {  // warp-wide: new-token rows of unit block `pos`
+        const int lo = (sb + pos) * kBlockSize, hi = lo + kBlockSize;
+        const int ta = t_new0 > lo ? t_new0 : lo, tb = e_tok < hi ? e_tok : hi;
+        if (ta >= tb) return;
+        constexpr int CH = D / 8;
+        for (int c = lane; c < (tb - ta) * 2 * CH; c += 32) {
+            const int t = ta + c / (2 * CH);
+            append_chunk(p.app, p.bt, p.max_blocks, p.q_len, p.Hkv, D, b, t - first_new, kvh, t, (c / CH) & 1,
+                         c % CH);
         }
-    }
+        fence_proxy_async_global();
+        __syncwarp();
+    };
+    // unit blocks holding new tokens: [jn0, jn1]
+    const int jn0 = t_new0 < e_tok ? t_new0 / kBlockSize - sb : n;
+    const int jn1 = t_new0 < e_tok ? (e_tok - 1) / kBlockSize - sb : n - 1;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;
         const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+        for (int j = jn0; j <= jn1; ++j) write_new(j);
         // block ids for 32 blocks at a time, the next chunk loaded one chunk ahead
         int cur = lane < n ? btrow[lane] : 0;
         int pfv = (d > 0 && lane + d < n) ? btrow[lane + d] : -1;
@@ -256,9 +262,17 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
             }
         };
         for (int pos = PAIR * warp; pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
+            if (pos >= jn0 && pos <= jn1) write_new(pos);
             issue(pos);
-            if (PAIR == 2 && pos + 1 < n) issue(pos + 1);
+            if (PAIR == 2 && pos + 1 < n) {
+                if (pos + 1 >= jn0 && pos + 1 <= jn1) write_new(pos + 1);
+                issue(pos + 1);
+            }
         }
+        // new-token blocks past the prologue: written now (overlapping the
+        // prologue loads), ahead of their refill issue by this same warp
+        for (int j = jn0 > STAGES ? jn0 : STAGES; j <= jn1; ++j)
+            if ((j / PAIR) % kConsumerWarps == warp) write_new(j);
         int mine = 0;
         for (int j = PAIR * warp; j < n; j += PAIR * kConsumerWarps) {
             const bool two = PAIR == 2 && j + 1 < n;

@@ -559,6 +559,8 @@ def _as_cache(arr_u8, like):
 @pytest.mark.parametrize("q_len", [1, 3])
 @pytest.mark.parametrize("e4m3", [False, True])
 def test_kv_append_standalone_bitwise_vs_oracle(pda, oracle_mod, cfg, q_len, e4m3):
+    if e4m3 and cfg.head_dim != 128:
+        pytest.skip("e4m3 caches are head_dim 128 only")
     inp = synth.make_inputs(cfg, seed=12)
     if e4m3:
         inp = kv8(inp)
