@@ -289,6 +289,26 @@ pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_
                                 float scale, const pda_shape* shape, const pda_options* opt,
                                 void* workspace, size_t workspace_bytes, void* stream);
 
+/* Pipelined form of pda_decode_step_host for back-to-back steps: the input
+ * copies and the output copy run on `copy_stream`, the kernels on
+ * `compute_stream`, linked by two caller-owned CUDA events (cudaEvent_t):
+ *   copy_stream:    H2D q, block_tables, context_lens; record inputs_ready
+ *   compute_stream: wait inputs_ready; the decode kernel(s); record step_done
+ *   copy_stream:    wait step_done; D2H out
+ * With one compute stream and one copy stream + staging slot + event pair per
+ * in-flight step (e.g. two, used alternately), a step's copies overlap the
+ * previous step's kernels while the kernels themselves stay in issue order.
+ * The caller synchronises copy_stream before reading out_host and must not
+ * reuse a slot's staging buffers before that slot's previous step finished
+ * (issuing the slot's steps on the same copy_stream guarantees it). */
+pda_status pda_decode_step_host_async(const void* q_host, const int32_t* block_tables_host,
+                                      const int32_t* context_lens_host, void* out_host, void* q_dev,
+                                      int32_t* block_tables_dev, int32_t* context_lens_dev, void* out_dev,
+                                      const void* k_cache, const void* v_cache, float scale,
+                                      const pda_shape* shape, const pda_options* opt, void* workspace,
+                                      size_t workspace_bytes, void* compute_stream, void* copy_stream,
+                                      void* inputs_ready, void* step_done);
+
 /* Measurement helper (not part of the method): stream-read `bytes` of device
  * memory at `buf` with 16-byte loads on a grid of num_sms * 4 CTAs, writing a
  * checksum word to `sink` (device, 16 B).  Gives the in-run read roofline. */
@@ -298,7 +318,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
+int32_t pda_abi_version(void);  /* 11: pda_decode_step_host_async; 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
 
 #ifdef __cplusplus
 }

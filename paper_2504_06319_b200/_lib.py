@@ -96,6 +96,8 @@ def lib():
             L.paged_decode_attention_append.restype = i32
             L.pda_validate_inputs.argtypes = [p, p, ps, p, p]
             L.pda_validate_inputs.restype = i32
+            L.pda_decode_step_host_async.argtypes = [p, p, p, p, p, p, p, p, p, p, f32, ps, po, p, sz, p, p, p, p]
+            L.pda_decode_step_host_async.restype = i32
             L.pda_read_roofline.argtypes = [p, sz, p, p]
             L.pda_read_roofline.restype = i32
             L.pda_status_string.argtypes = [i32]
@@ -333,9 +335,16 @@ def paged_decode_attention_gather(q, k_cache, v_cache, block_tables, context_len
 class HostDecodeStep:
     """End-to-end step from pinned host buffers through pda_decode_step_host:
     H2D of q / block_tables / context_lens, the decode kernel(s) against the
-    device-resident caches, D2H of out -- all on one stream."""
+    device-resident caches, D2H of out -- all on one stream per step.
 
-    def __init__(self, k_cache, v_cache, num_seqs, num_q_heads, max_blocks, dtype, out_dtype=None,
+    slots > 1 pipelines consecutive steps through pda_decode_step_host_async:
+    step k uses staging slot k % slots (device buffers, pinned host output, a
+    copy stream and two events); its copies run on the slot's copy stream and
+    overlap the previous step's kernels, which stay in order on the caller's
+    (compute) stream.  join(stream) makes `stream` wait for every output copy
+    issued so far (call it before reading a result or recording a timer)."""
+
+    def __init__(self, k_cache, v_cache, num_seqs, num_q_heads, max_blocks, dtype, out_dtype=None, slots=1,
                  **opt_kw):
         import torch
         _require_cuda(k_cache, v_cache)
@@ -343,16 +352,35 @@ class HostDecodeStep:
         D = k_cache.shape[-1]
         self.k, self.v = k_cache, v_cache
         self.out_dtype = out_dtype or dtype
-        self.q_dev = torch.empty((num_seqs, num_q_heads, D), dtype=dtype, device=dev)
-        self.bt_dev = torch.empty((num_seqs, max_blocks), dtype=torch.int32, device=dev)
-        self.lens_dev = torch.empty((num_seqs,), dtype=torch.int32, device=dev)
-        self.out_dev = torch.empty((num_seqs, num_q_heads, D), dtype=self.out_dtype, device=dev)
-        self.out_host = torch.empty(self.out_dev.shape, dtype=self.out_dtype, pin_memory=True)
+        self.slots = []
+        for _ in range(max(1, int(slots))):
+            sl = dict(q_dev=torch.empty((num_seqs, num_q_heads, D), dtype=dtype, device=dev),
+                      bt_dev=torch.empty((num_seqs, max_blocks), dtype=torch.int32, device=dev),
+                      lens_dev=torch.empty((num_seqs,), dtype=torch.int32, device=dev),
+                      out_dev=torch.empty((num_seqs, num_q_heads, D), dtype=self.out_dtype, device=dev))
+            sl["out_host"] = torch.empty(sl["out_dev"].shape, dtype=self.out_dtype, pin_memory=True)
+            self.slots.append(sl)
+        s0 = self.slots[0]
+        self.q_dev, self.bt_dev, self.lens_dev, self.out_dev = s0["q_dev"], s0["bt_dev"], s0["lens_dev"], s0["out_dev"]
+        self.out_host = s0["out_host"]
         self.shape = make_shape(self.q_dev, k_cache, self.bt_dev, self.out_dtype)
         self.opts = make_options(**opt_kw)
         wsb = workspace_bytes(self.shape, self.opts)
+        # one workspace: the kernels of all slots run in order on the compute stream
         self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)
+        for sl in self.slots:
+            sl["ws"] = self.ws
         self.wsb = wsb
+        self.streams = []
+        if len(self.slots) > 1:
+            for sl in self.slots:
+                sl["copy"] = torch.cuda.Stream(device=dev)
+                sl["ev_in"], sl["ev_done"] = torch.cuda.Event(), torch.cuda.Event()
+                for ev in (sl["ev_in"], sl["ev_done"]):  # create the events now (torch creates on record)
+                    ev.record(sl["copy"])
+                self.streams.append(sl["copy"])
+            torch.cuda.synchronize(dev)
+        self.n = 0
 
     def h2d_bytes(self):
         return sum(t.numel() * t.element_size() for t in (self.q_dev, self.bt_dev, self.lens_dev))
@@ -360,15 +388,40 @@ class HostDecodeStep:
     def d2h_bytes(self):
         return self.out_dev.numel() * self.out_dev.element_size()
 
-    def __call__(self, q_host, bt_host, lens_host, scale, stream=None):
+    def _run(self, sl, q_host, bt_host, lens_host, scale, stream):
         st = lib().pda_decode_step_host(
-            q_host.data_ptr(), bt_host.data_ptr(), lens_host.data_ptr(), self.out_host.data_ptr(),
-            self.q_dev.data_ptr(), self.bt_dev.data_ptr(), self.lens_dev.data_ptr(),
-            self.out_dev.data_ptr(), self.k.data_ptr(), self.v.data_ptr(), float(scale),
-            ctypes.byref(self.shape), ctypes.byref(self.opts), self.ws.data_ptr() if self.wsb else None,
+            q_host.data_ptr(), bt_host.data_ptr(), lens_host.data_ptr(), sl["out_host"].data_ptr(),
+            sl["q_dev"].data_ptr(), sl["bt_dev"].data_ptr(), sl["lens_dev"].data_ptr(),
+            sl["out_dev"].data_ptr(), self.k.data_ptr(), self.v.data_ptr(), float(scale),
+            ctypes.byref(self.shape), ctypes.byref(self.opts), sl["ws"].data_ptr() if self.wsb else None,
             self.wsb, _stream_handle(stream))
         _check(st, "pda_decode_step_host")
-        return self.out_host
+        return sl["out_host"]
+
+    def __call__(self, q_host, bt_host, lens_host, scale, stream=None):
+        """Issue one step; returns the pinned host tensor its output lands in
+        (valid once the step's stream has been joined / synchronised)."""
+        import torch
+        if not self.streams:
+            return self._run(self.slots[0], q_host, bt_host, lens_host, scale, stream)
+        sl = self.slots[self.n % len(self.slots)]
+        self.n += 1
+        cs = stream if stream is not None else torch.cuda.current_stream()
+        st = lib().pda_decode_step_host_async(
+            q_host.data_ptr(), bt_host.data_ptr(), lens_host.data_ptr(), sl["out_host"].data_ptr(),
+            sl["q_dev"].data_ptr(), sl["bt_dev"].data_ptr(), sl["lens_dev"].data_ptr(),
+            sl["out_dev"].data_ptr(), self.k.data_ptr(), self.v.data_ptr(), float(scale),
+            ctypes.byref(self.shape), ctypes.byref(self.opts), self.ws.data_ptr() if self.wsb else None,
+            self.wsb, ctypes.c_void_p(cs.cuda_stream), ctypes.c_void_p(sl["copy"].cuda_stream),
+            ctypes.c_void_p(sl["ev_in"].cuda_event), ctypes.c_void_p(sl["ev_done"].cuda_event))
+        _check(st, "pda_decode_step_host_async")
+        return sl["out_host"]
+
+    def join(self, stream=None):
+        import torch
+        caller = stream if stream is not None else torch.cuda.current_stream()
+        for s in self.streams:
+            caller.wait_stream(s)
 
 
 def read_roofline(buf, sink, stream=None):

@@ -600,6 +600,45 @@ pda_status pda_decode_step_host(const void* q_host, const int32_t* block_tables_
     return PDA_OK;
 }
 
+pda_status pda_decode_step_host_async(const void* q_host, const int32_t* block_tables_host,
+                                      const int32_t* context_lens_host, void* out_host, void* q_dev,
+                                      int32_t* block_tables_dev, int32_t* context_lens_dev, void* out_dev,
+                                      const void* k_cache, const void* v_cache, float scale,
+                                      const pda_shape* shape, const pda_options* opt, void* workspace,
+                                      size_t workspace_bytes, void* compute_stream, void* copy_stream,
+                                      void* inputs_ready, void* step_done) {
+    pda_status st = validate(shape, opt);
+    if (st != PDA_OK) return st;
+    if (!q_host || !block_tables_host || !context_lens_host || !out_host || !q_dev ||
+        !block_tables_dev || !context_lens_dev || !out_dev || !inputs_ready || !step_done)
+        return PDA_ERR_NULL;
+    st = use_device_of(out_dev);
+    if (st != PDA_OK) return st;
+    cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+    cudaStream_t xs = static_cast<cudaStream_t>(copy_stream);
+    cudaEvent_t in_ev = static_cast<cudaEvent_t>(inputs_ready);
+    cudaEvent_t done_ev = static_cast<cudaEvent_t>(step_done);
+    const size_t B = shape->num_seqs;
+    const size_t q_bytes = B * q_tokens(shape) * shape->num_q_heads * shape->head_dim * 2;
+    const size_t bt_bytes = B * shape->max_blocks_per_seq * 4;
+    const size_t out_bytes = B * q_tokens(shape) * shape->num_q_heads * shape->head_dim * elem_bytes(shape->out_dtype);
+    // inputs on the copy stream, the kernels on the compute stream once they landed,
+    // the output back on the copy stream once the kernels finished
+    if (cudaMemcpyAsync(q_dev, q_host, q_bytes, cudaMemcpyHostToDevice, xs) != cudaSuccess ||
+        cudaMemcpyAsync(block_tables_dev, block_tables_host, bt_bytes, cudaMemcpyHostToDevice, xs) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(context_lens_dev, context_lens_host, B * 4, cudaMemcpyHostToDevice, xs) != cudaSuccess ||
+        cudaEventRecord(in_ev, xs) != cudaSuccess || cudaStreamWaitEvent(cs, in_ev, 0) != cudaSuccess)
+        return PDA_ERR_CUDA;
+    st = run(q_dev, k_cache, v_cache, block_tables_dev, context_lens_dev, scale, out_dev, shape, opt, workspace,
+             workspace_bytes, nullptr, 0, cs);
+    if (st != PDA_OK) return st;
+    if (cudaEventRecord(done_ev, cs) != cudaSuccess || cudaStreamWaitEvent(xs, done_ev, 0) != cudaSuccess ||
+        cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, xs) != cudaSuccess)
+        return PDA_ERR_CUDA;
+    return PDA_OK;
+}
+
 pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream) {
     if (!buf || !sink) return PDA_ERR_NULL;
     if (!aligned16(buf) || !aligned16(sink)) return PDA_ERR_ALIGN;
@@ -627,6 +666,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 10; }
+int32_t pda_abi_version(void) { return 11; }
 
 }  // extern "C"

@@ -226,7 +226,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 10
+    assert pda.lib().pda_abi_version() == 11
 
 
 def test_product_never_imports_oracle():

@@ -275,6 +275,28 @@ def test_host_e2e_step_matches_device_path(pda):
     assert torch.equal(out, ref.cpu())
 
 
+def test_host_e2e_pipelined_slots(pda):
+    """Two staging slots on two streams: every step's host output equals the
+    device path; steps with different inputs do not mix."""
+    cfg = synth.Config("e2e2", 4, 8, 2, 128, (300, 64, 1, 999), "bf16")
+    inps = [synth.make_inputs(cfg, seed=s) for s in (31, 32, 33)]
+    dev = to_dev(inps[0])
+    step = pda.HostDecodeStep(dev["k_cache"], dev["v_cache"], 4, 8, cfg.max_blocks_per_seq, torch.bfloat16,
+                              slots=2)
+    refs, outs = [], []
+    for i, inp in enumerate(inps):
+        d = dict(dev, q=inp["q"].cuda())
+        refs.append(gpu(pda, d).cpu())
+        out = step(inp["q"].pin_memory(), inp["block_tables"].pin_memory() if i == 0 else
+                   inps[0]["block_tables"].pin_memory(), inps[0]["context_lens"].pin_memory(), inp["scale"])
+        step.join()
+        torch.cuda.synchronize()
+        outs.append(out.clone())
+    for r, o in zip(refs, outs):
+        assert torch.equal(o, r)
+    assert not torch.equal(outs[0], outs[1])
+
+
 def test_nan_poison_never_leaks(pda):
     cfg = synth.Config("poison", 4, 8, 8, 128, (17, 31, 33, 1), "fp16", poison_blocks=20)
     dev = to_dev(synth.make_inputs(cfg, seed=3))
@@ -671,3 +693,39 @@ def test_validate_inputs_matches_oracle(pda, oracle_mod, seed):
     assert got == want
     good = synth.make_inputs(SHAPES[1], seed=1, device="cuda")
     assert pda.validate_inputs(good["block_tables"], good["context_lens"], good["k_cache"].shape[0]) == (0, 0, 0)
+
+
+# ---- maximum sizes ----------------------------------------------------------------
+
+def test_full_size_c5_unsharded(pda, oracle_mod):
+    """Llama-3-70B shape on one GPU (TP=1): 17 GB of KV, 64 q / 8 kv heads."""
+    cfg = synth.C5_LLAMA3_70B
+    sampled_check(pda, oracle_mod, cfg, [0, 255])
+
+
+@pytest.mark.parametrize("kernel", ["splitk", "balanced"])
+def test_max_context_single_sequence(pda, oracle_mod, kernel):
+    """One sequence of 256k tokens (16384 blocks), g = 8: the longest split."""
+    cfg = synth.Config("ctx256k", 1, 8, 1, 128, (262144 - 5,), "bf16", poison_blocks=3)
+    inp = synth.make_inputs(cfg, seed=2, device="cuda")
+    out = gpu(pda, inp, kernel=kernel)
+    torch.cuda.synchronize()
+    rows = [0, 5]
+    ref = oracle_mod.paged_attention(inp["q"].cpu(), inp["k_cache"].cpu(), inp["v_cache"].cpu(),
+                                     inp["block_tables"].cpu(), inp["context_lens"].cpu(), inp["scale"], "bf16",
+                                     rows=rows)
+    g = out.double().cpu().numpy().reshape(-1, 128)
+    assert np.abs(g[rows] - ref.reshape(-1, 128)[rows]).max() <= TOL
+
+
+def test_large_batch_short_contexts(pda, oracle_mod):
+    """8192 sequences (grid z) of 1-64 tokens, MHA D=64."""
+    rng = np.random.default_rng(5)
+    lens = tuple(int(x) for x in rng.integers(0, 65, size=8192))
+    cfg = synth.Config("b8192", 8192, 4, 4, 64, lens, "fp16", poison_blocks=16)
+    inp = synth.make_inputs(cfg, seed=3, device="cuda")
+    out = gpu(pda, inp)
+    torch.cuda.synchronize()
+    seqs = [0, 1, 4095, 8191] + [int(i) for i in np.flatnonzero(np.array(lens) == 0)[:2]]
+    sub = synth.sample_rows(inp, seqs)
+    assert max_err(out[seqs], oracle_out(oracle_mod, sub)) <= TOL
