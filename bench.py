@@ -8,7 +8,8 @@ online softmax, PV, combine; plus the TP output all-gather when N > 1).
 Inputs are seeded synthetic tensors shaped like BASELINE.json's configs
 (default configs[1], Llama-2-7B: B=64, 32 heads, D=128, ctx 4096, fp16),
 resident in HBM before the timed region; KV per step (4.3 GB) is far larger
-than L2 (126 MB), so no flush is needed between steps.
+than L2 (126 MB), so no flush is needed between steps (smaller --config
+cells, KV < 4 x L2, flush L2 between individually timed steps).
 
 N > 1 (torchrun): tensor parallel over KV heads -- rank r holds
 Hkv/N heads of the same batch and the step ends with an NCCL all-gather of
@@ -33,6 +34,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decode attention us/step & achieved HBM GB/s (prefetch on/off); tokens/s at 1-8 GPU"
 KERNEL_NAMES = {1: "paper_kernel", 2: "splitk_kernel", 3: "stream_kernel", 4: "balanced_kernel"}
+
+
+L2_BYTES = 126 * 1024 * 1024  # B200 L2
 
 
 def parse():
@@ -274,6 +278,11 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # steps whose KV fits in a few L2s would hit in L2 across back-to-back
+    # steps: flush it between timed steps (outside the timed spans)
+    flush_buf = (torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+                 if local_cfg.kv_bytes() < 4 * L2_BYTES else None)
+
     def time_steps(fn, steps, warmup, join=None):
         for _ in range(warmup):
             fn(q, bt, lens, scale)
@@ -282,16 +291,31 @@ def main():
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            fn(q, bt, lens, scale)
-        if join:
-            join(stream)  # multi-stream steps: the timer's stream waits for all of them
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        ms = e0.elapsed_time(e1) / steps
+        if flush_buf is not None:
+            spans = []
+            for _ in range(steps):
+                flush_buf.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn(q, bt, lens, scale)
+                if join:
+                    join(stream)
+                e1.record(stream)
+                spans.append((e0, e1))
+            torch.cuda.synchronize()
+            barrier()
+            ms = sum(a.elapsed_time(b) for a, b in spans) / steps
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                fn(q, bt, lens, scale)
+            if join:
+                join(stream)  # multi-stream steps: the timer's stream waits for all of them
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            ms = e0.elapsed_time(e1) / steps
         if world > 1:
             t = torch.tensor([ms], device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -322,6 +346,8 @@ def main():
             n_rep = max(10, args.steps // 4)
             for _ in range(n_rep):
                 for k, fn in arms.items():
+                    if flush_buf is not None:
+                        flush_buf.zero_()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn(q, bt, lens, scale)
@@ -387,6 +413,8 @@ def main():
             torch.cuda.synchronize()
             for _ in range(max(10, args.steps // 4)):
                 for k, fn in app_arms.items():
+                    if flush_buf is not None:
+                        flush_buf.zero_()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn()
@@ -473,7 +501,9 @@ def main():
             "issue": "self (consumer warps refill their ring stages)" if pl["threads"] == 128 else "producer warp",
             "tp_gather": "fused into the kernel stores (symmetric memory)" if args.fused_gather else "NCCL all_gather_into_tensor",
             "p_max": pl["p_max"],
-            "l2": f"no flush: inputs larger than L2 ({cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)",
+            "l2": (f"no flush: inputs larger than L2 ({local_cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)"
+                   if flush_buf is None else
+                   "L2 flushed between timed steps (512 MiB write outside the per-step CUDA-event spans)"),
             "bytes_per_step": total_bytes,
         },
         "roofline": {
