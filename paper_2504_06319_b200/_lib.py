@@ -13,7 +13,7 @@ import re
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpda.so")
+LIB_PATH = os.environ.get("PDA_LIB_PATH") or os.path.join(HERE, "libpda.so")  # override: A/B experiments only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
 PDA_F16, PDA_BF16, PDA_F32, PDA_E4M3 = 0, 1, 2, 3

@@ -37,14 +37,17 @@ for i, v in enumerate(variants):
     res[i] = []
 for rnd in range(5):
     for i in graphs:
-        for _ in range(3):
+        spans = []
+        for _ in range(3):  # all reps queued, one sync: no host gaps inside a span
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(); graphs[i].replay(); e1.record(); e1.synchronize()
-            res[i].append(e0.elapsed_time(e1) * 1e3)
+            e0.record(); graphs[i].replay(); e1.record()
+            spans.append((e0, e1))
+        torch.cuda.synchronize()
+        res[i].extend(e0.elapsed_time(e1) * 1e3 for e0, e1 in spans)
 tot = cfg.kv_bytes() // (2 if kv8 else 1) + cfg.other_bytes()
 for i, v in enumerate(variants):
     us = statistics.median(res[i])
     print(json.dumps(dict(cell=cfg.name + ("_kv8" if kv8 else "") + (f"_q{q_len}" if q_len > 1 else ""), **v,
-                          us=round(us, 1), gbs=round(tot / us / 1e3),
+                          us=round(us, 2), gbs=round(tot / us / 1e3),
                           tokens_per_s=round(cfg.num_seqs * q_len / us * 1e6))))

@@ -125,7 +125,8 @@ def main():
                         with torch.cuda.graph(g, capture_error_mode="relaxed"):
                             run()
                         graphs[i] = g
-                for _ in range(a.reps):
+                spans = []
+                for _ in range(a.reps):  # all reps queued, one sync: no host gaps inside a span
                     flush.zero_()
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
@@ -135,8 +136,9 @@ def main():
                     else:
                         graphs[i].replay()
                     e1.record()
-                    e1.synchronize()
-                    times[i].append(e0.elapsed_time(e1) * 1e3)
+                    spans.append((e0, e1))
+                torch.cuda.synchronize()
+                times[i].extend(e0.elapsed_time(e1) * 1e3 for e0, e1 in spans)
         # bitwise invariance of prefetch within each kernel/stages family
         for i, v in enumerate(vs):
             base = next(j for j, w in enumerate(vs) if w["kernel"] == v["kernel"]
