@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip ablation arms / e2e / cpu baseline")
     ap.add_argument("--fused-gather", action="store_true",
                     help="TP output all-gather inside the kernel's stores (symmetric memory) instead of NCCL")
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="N > 1: always gather with NCCL (default: the fused gather when its first step "
+                         "matches the NCCL step bitwise on every rank)")
     ap.add_argument("--sweep", action="store_true", help="prefetch-distance x stages sweep (extra JSON lines on stderr)")
     return ap.parse_args()
 
@@ -241,7 +244,9 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
-    elif args.fused_gather:  # symmetric memory needs a process group, even of one rank
+    # PDA_BENCH_CHECK_FUSED=1 (testing only): run the N > 1 fused-gather selection at N = 1
+    check_fused_1 = os.environ.get("PDA_BENCH_CHECK_FUSED") == "1" and world == 1
+    if world == 1 and (args.fused_gather or check_fused_1):  # symmetric memory needs a process group
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", dev_index))
@@ -273,6 +278,25 @@ def main():
     step_main = make_step(**opt_kw, fused_gather=args.fused_gather)
     q, bt, lens, scale = inp["q"], inp["block_tables"], inp["context_lens"], inp["scale"]
     stream = torch.cuda.current_stream()
+    tp_gather = "fused" if args.fused_gather else "nccl"
+    step_nccl = None
+    if (world > 1 or check_fused_1) and not share and not args.fused_gather and not args.nccl_gather:
+        # fused output all-gather when it works here: its first
+        # step must equal the NCCL step bit for bit on every rank, else NCCL
+        ok = 1
+        try:
+            step_fused = make_step(**opt_kw, fused_gather=True)
+            ref = step_main(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
+            got = step_fused(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
+            torch.cuda.synchronize()
+            ok = int(torch.equal(ref.view(torch.int16), got.view(torch.int16)))
+        except Exception as e:  # noqa: BLE001 -- any failure selects the NCCL path
+            print(f"[bench rank {rank}] fused gather unavailable: {e}", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            step_nccl, step_main, tp_gather = step_main, step_fused, "fused"
 
     def barrier():
         if world > 1:
@@ -329,6 +353,8 @@ def main():
     with ClockSampler(dev_index) as clk:
         ms = time_steps(step_main, args.steps, args.warmup)
         extras = {}
+        if step_nccl is not None:  # the NCCL-gather step, for comparison with the fused one
+            extras["tp_nccl_gather_us_per_step"] = time_steps(step_nccl, args.steps, 2) * 1e3
         if not args.no_extras:
             # prefetch ablation arms on the same inputs, interleaved step by step
             # (A B A B ...) with per-step CUDA events, medians per arm
@@ -499,7 +525,8 @@ def main():
             "smem_stages": pl["smem_stages"], "partition_tokens": pl["partition_tokens"],
             "eviction": ["normal", "demand_first", "prefetch_last", "both"][pl["eviction"]],
             "issue": "self (consumer warps refill their ring stages)" if pl["threads"] == 128 else "producer warp",
-            "tp_gather": "fused into the kernel stores (symmetric memory)" if args.fused_gather else "NCCL all_gather_into_tensor",
+            "tp_gather": ("fused into the kernel stores (symmetric memory; first step checked bitwise against NCCL)"
+                          if tp_gather == "fused" else "NCCL all_gather_into_tensor"),
             "p_max": pl["p_max"],
             "l2": (f"no flush: inputs larger than L2 ({local_cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)"
                    if flush_buf is None else
