@@ -237,3 +237,40 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "oracle.c" not in text and "liboracle" not in text, f
+
+
+def test_append_entries_reject_before_launch():
+    """pda_kv_append / paged_decode_attention_append / pda_validate_inputs:
+    argument errors come back synchronously, before any CUDA call."""
+    L = pda.lib()
+    base = 0x10000000
+    s, o = shape(), opts()
+    # NULL new rows / caches
+    assert L.pda_kv_append(None, base, base, base, base, base, ctypes.byref(s), ctypes.byref(o), None) == 1
+    assert L.pda_kv_append(base, base, base, base, None, base, ctypes.byref(s), ctypes.byref(o), None) == 1
+    # misaligned new rows
+    assert L.pda_kv_append(base + 4, base, base, base, base, base, ctypes.byref(s), ctypes.byref(o), None) == 4
+    # e4m3 cache without scales: the encoding is undefined
+    s8 = shape(head_dim=128, kv_dtype=3)
+    assert L.pda_kv_append(base, base, base, base, base, base, ctypes.byref(s8), ctypes.byref(o), None) == 2
+    # fused entry: same checks, then the attention's own
+    rc = L.paged_decode_attention_append(base, None, base, base, base, base, base, 1.0, base, ctypes.byref(s),
+                                         ctypes.byref(o), None, 0, None)
+    assert rc == 1
+    rc = L.paged_decode_attention_append(base, base, base + 8, base, base, base, base, 1.0, base, ctypes.byref(s),
+                                         ctypes.byref(o), None, 0, None)
+    assert rc == 4
+    # validation entry
+    assert L.pda_validate_inputs(None, base, ctypes.byref(s), base, None) == 1
+    assert L.pda_validate_inputs(base, base, ctypes.byref(shape(block_size=32)), base, None) == 3
+    assert L.pda_validate_inputs(base, base, ctypes.byref(shape(num_blocks=0)), base, None) == 2
+
+
+def test_host_async_entry_rejects_before_launch():
+    L = pda.lib()
+    base = 0x10000000
+    s, o = shape(), opts()
+    args = [base] * 10
+    rc = L.pda_decode_step_host_async(*args[:8], base, base, 1.0, ctypes.byref(s), ctypes.byref(o), None, 0,
+                                      None, None, None, base)
+    assert rc == 1  # NULL inputs_ready event
