@@ -536,7 +536,9 @@ def main():
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": load_traffic(cfg.name),
-            "kernel": KERNEL_NAMES[pl["kernel"]] + (" + combine_kernel" if pl["kernel"] == 2 and pl["p_max"] > 1 else ""),
+            "kernel": KERNEL_NAMES[pl["kernel"]] + (
+                (f" (clusters of {pl['cluster']}, DSMEM merge)" if pl["cluster"] else " + combine_kernel")
+                if pl["kernel"] == 2 and pl["p_max"] > 1 else ""),
             "launch_us": attn_ms * 1e3, "algorithmic_bytes_per_launch": local_bytes,
             "peak_source": peak_src,
         },

@@ -143,6 +143,12 @@ typedef struct {
                                   self-issue limits prefetch_distance to 32 */
     float k_scale;             /* e4m3 cache only: K dequantisation scale (0 = 1.0) */
     float v_scale;             /* e4m3 cache only: V dequantisation scale (0 = 1.0) */
+    int32_t merge;             /* split-K partition merge (S8) when P_max > 1: 0 = auto (cluster
+                                  when P_max <= 8, else combine kernel), 1 = combine kernel
+                                  through the workspace, 2 = cluster (P_max <= 16): the
+                                  partitions of a (seq, kv head) row run as one thread-block
+                                  cluster and merge through distributed shared memory, no
+                                  workspace, no second launch.  Bitwise-identical results. */
 } pda_options;
 
 /* Result of the (host-only, deterministic) split-K planner. */
@@ -156,6 +162,8 @@ typedef struct {
     int32_t trace_rec_len;    /* int32 words per trace record (see paged_decode_attention_trace) */
     int32_t trace_records;    /* number of trace records */
     int32_t eviction;         /* resolved pda_eviction (never PDA_EV_AUTO) */
+    int32_t cluster;          /* split-K: CTAs per cluster (= p_max) when partitions merge in a
+                                 cluster, else 0 (combine kernel when p_max > 1) */
     size_t workspace_bytes;   /* == pda_workspace_bytes() */
 } pda_plan_info;
 
@@ -318,7 +326,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 11: pda_decode_step_host_async; 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
+int32_t pda_abi_version(void);  /* 12: cluster merge (options.merge, plan.cluster); 11: pda_decode_step_host_async; 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
 
 #ifdef __cplusplus
 }

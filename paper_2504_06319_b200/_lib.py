@@ -48,13 +48,14 @@ class Options(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms",
         "stream_warps", "eviction", "issue_mode")] + [("k_scale", ctypes.c_float),
-                                                      ("v_scale", ctypes.c_float)]
+                                                      ("v_scale", ctypes.c_float),
+                                                      ("merge", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "kernel", "partition_tokens", "p_max", "smem_stages", "grid_x", "grid_y", "grid_z",
-        "threads", "trace_rec_len", "trace_records", "eviction")] + [("workspace_bytes", ctypes.c_size_t)]
+        "threads", "trace_rec_len", "trace_records", "eviction", "cluster")] + [("workspace_bytes", ctypes.c_size_t)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -149,16 +150,20 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
                  _dtype_code(out_dtype if out_dtype is not None else q.dtype), _dtype_code(k_cache.dtype), q_len)
 
 
+MERGE = {"auto": 0, "combine": 1, "cluster": 2}
+
+
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
                  smem_stages=0, kernel="auto", num_sms=0, stream_warps=0,
-                 eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0, issue_mode=0) -> Options:
+                 eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0, issue_mode=0, merge="auto") -> Options:
     mode = PREFETCH[prefetch] if not isinstance(prefetch, int) else prefetch
     if prefetch_distance is None:
         prefetch_distance = DEFAULT_DISTANCE if mode else 0
     kern = KERNEL[kernel] if not isinstance(kernel, int) else kernel
     return Options(mode, int(prefetch_distance), int(partition_tokens), int(smem_stages), kern,
                    int(num_sms), int(stream_warps), int(EVICTION.get(eviction, eviction)),
-                   int(ISSUE.get(issue_mode, issue_mode)), float(k_scale), float(v_scale))
+                   int(ISSUE.get(issue_mode, issue_mode)), float(k_scale), float(v_scale),
+                   int(MERGE.get(merge, merge)))
 
 
 def plan(shape: Shape, opts: Options) -> dict:
@@ -194,7 +199,8 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
                            out_dtype=None, prefetch=DEFAULT_PREFETCH, prefetch_distance=None,
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
                            num_sms=0, eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0,
-                           issue_mode=0, workspace=None, stream=None, trace=False, k_new=None, v_new=None):
+                           issue_mode=0, merge="auto", workspace=None, stream=None, trace=False, k_new=None,
+                           v_new=None):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16 like q, or
@@ -227,7 +233,7 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     shape = make_shape(q, k_cache, block_tables, out_dtype)
     opts = make_options(prefetch, prefetch_distance, partition_tokens, smem_stages, kernel,
                         num_sms=num_sms, stream_warps=stream_warps, eviction=eviction,
-                        k_scale=k_scale, v_scale=v_scale, issue_mode=issue_mode)
+                        k_scale=k_scale, v_scale=v_scale, issue_mode=issue_mode, merge=merge)
     if scale is None:
         scale = q.shape[-1] ** -0.5
     info = plan(shape, opts)

@@ -66,12 +66,16 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     uint8_t* ring = smem;
     constexpr int kRingBytes = STAGES * G::kStage;
     constexpr int kMergeAccBytes = kConsumerWarps * NH * (D + 4) * 4;
-    constexpr int kBigBytes = kRingBytes > kMergeAccBytes ? kRingBytes : kMergeAccBytes;
+    constexpr int kClBytes = NH * D * 4 + NH * 4;  // this CTA's partial (o, lse) for the cluster merge
+    constexpr int kBigBytes =
+        kRingBytes > kMergeAccBytes + kClBytes ? kRingBytes : kMergeAccBytes + kClBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBigBytes);
     uint64_t* empty = full + STAGES;
     float* merge_m = reinterpret_cast<float*>(empty + STAGES);
     float* merge_l = merge_m + kConsumerWarps * NH;
     float* merge_acc = reinterpret_cast<float*>(ring);
+    float* cl_o = reinterpret_cast<float*>(ring + kMergeAccBytes);  // [NH][D], after the main loop
+    float* cl_lse = cl_o + NH * D;                                   // [NH]
 
     const int part = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5;
@@ -90,6 +94,38 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         rec = p.trace + ((size_t)(b * p.Hkv + kvh) * p.p_max + part) * p.trace_rec_len;
     }
 
+    const int n_parts = (L + P - 1) / P;
+
+    // S8 inside a cluster (p.cluster > 1: the P_max partitions of this (seq, kv
+    // head) row are one thread-block cluster): each CTA merges a slice of the
+    // row's outputs from every partition's (o, lse) read over DSMEM -- the
+    // same arithmetic, in the same partition order, as combine_kernel.
+    auto cluster_merge = [&]() {
+        cluster_sync_all();  // every partition's (o, lse) is in its shared memory
+        if (threadIdx.x < kConsumerWarps * 32) {
+            const int E = p.q_len * g * D;
+            const int per = (E + p.cluster - 1) / p.cluster;
+            const int e1 = (part + 1) * per < E ? (part + 1) * per : E;
+            const uint32_t o_base = smem_u32(cl_o), l_base = smem_u32(cl_lse);
+            for (int idx = part * per + threadIdx.x; idx < e1; idx += kConsumerWarps * 32) {
+                const int h = idx / D, dd = idx % D;
+                float M = -INFINITY;
+                for (int q = 0; q < n_parts; ++q) M = fmaxf(M, ld_cluster_f32(cluster_map(l_base + h * 4, q)));
+                if (M == -INFINITY) M = 0.f;  // every partition empty for this column
+                float acc = 0.f, den = 0.f;
+                for (int q = 0; q < n_parts; ++q) {
+                    const float w = ex2(ld_cluster_f32(cluster_map(l_base + h * 4, q)) - M);
+                    den += w;
+                    acc += w * ld_cluster_f32(cluster_map(o_base + (h * D + dd) * 4, q));
+                }
+                const float inv = den > 0.f ? 1.f / den : 0.f;  // no visible token at all: zero row
+                const size_t row = ((size_t)b * p.q_len + h / g) * p.Hq + kvh * g + h % g;
+                store_out_peers(p.outs, row, p.Hq, D, dd, acc * inv, p.out_dtype);
+            }
+        }
+        cluster_sync_all();  // partials stay alive until every reader is done
+    };
+
     if (e_tok <= s_tok) {  // empty unit (S0): nothing to read
         if constexpr (TRACE) {
             if (threadIdx.x == 0) {
@@ -98,6 +134,10 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
                 rec[2] = 0;
                 rec[3] = 0;
             }
+        }
+        if (p.cluster > 1) {  // still merges its slice of the row
+            cluster_merge();
+            return;
         }
         if (part == 0 && L <= 0) {  // context_len == 0 => zero rows (reading R6), every query token
             for (int i = threadIdx.x; i < p.q_len * g * D; i += blockDim.x) {
@@ -110,7 +150,6 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     }
     const int sb = s_tok / kBlockSize;
     const int n = (e_tok + kBlockSize - 1) / kBlockSize - sb;  // blocks in this unit
-    const int n_parts = (L + P - 1) / P;
 
     // Fused KV append: the step's new tokens in [t_new0, e_tok) are written by
     // the warp that issues the TMA load of their block, before that issue
@@ -201,6 +240,10 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
                 rec[2] = n;
                 rec[3] = npf;
             }
+        }
+        if (p.cluster > 1) {  // the cluster barriers count every thread
+            cluster_sync_all();
+            cluster_sync_all();
         }
         return;
     }
@@ -366,13 +409,18 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         // den == 0: no visible token for this column in this unit (multi-token decode)
         const float o = den > 0.f ? num / den * p.out_scale : 0.f;  // v_scale for the e4m3 cache, else 1
         const size_t row = ((size_t)b * p.q_len + h / g) * p.Hq + kvh * g + h % g;
-        if (direct) {
+        const float lse = den > 0.f ? M + __log2f(den) : -INFINITY;
+        if (p.cluster > 1) {
+            cl_o[h * D + dd] = o;
+            if (dd == 0) cl_lse[h] = lse;
+        } else if (direct) {
             store_out_peers(p.outs, row, p.Hq, D, dd, o, p.out_dtype);
         } else {
             p.ws_o[(row * p.p_max + part) * D + dd] = o;
-            if (dd == 0) p.ws_lse[row * p.p_max + part] = den > 0.f ? M + __log2f(den) : -INFINITY;
+            if (dd == 0) p.ws_lse[row * p.p_max + part] = lse;
         }
     }
+    if (p.cluster > 1) cluster_merge();
 }
 
 // S8: out = sum_p 2^(lse_p - M) o_p / sum_p 2^(lse_p - M), partitions in fixed order.
@@ -424,7 +472,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
 template <int D, int NT, int STAGES, bool KV8 = false>
 constexpr size_t smem_bytes_for() {
     constexpr int ring = STAGES * Geometry<D, KV8>::kStage;
-    constexpr int merge = kConsumerWarps * 8 * NT * (D + 4) * 4;
+    constexpr int merge = kConsumerWarps * 8 * NT * (D + 4) * 4 + 8 * NT * (D + 1) * 4;  // + cluster partial
     constexpr int big = ring > merge ? ring : merge;
     return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
 }
@@ -441,6 +489,26 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured_device = dev;
+    }
+    if (p.cluster > 1) {
+        // one cluster per (seq, kv head) row: its P_max partition CTAs (grid.x == P_max)
+        if (p.cluster > 8) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(splitk_block_threads<SELF>(), 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)p.cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, tmK, tmV, p);
     }
     kern<<<grid, splitk_block_threads<SELF>(), smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();

@@ -59,6 +59,8 @@ struct SplitKParams {
     float scale_log2;  // scale * log2(e) (* k_scale for an e4m3 cache), fp32
     float out_scale;   // v_scale for an e4m3 cache, else 1
     AppendParams app;  // fused KV append (app.k_new == nullptr: none)
+    int cluster;       // > 1: launched as clusters of P_max CTAs (one per partition of a
+                       // (seq, kv head) row) that merge their partials through DSMEM
 };
 
 struct PaperParams {

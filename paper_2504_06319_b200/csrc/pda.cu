@@ -19,6 +19,8 @@ constexpr int kDefaultBalancedStages = 8;
 constexpr size_t kSmemPerSm = 233472;  // 228 KB per SM on B200
 constexpr size_t kSmemReservedPerCta = 1024;
 constexpr int kDefaultSms = 148;  // B200
+constexpr int kMaxCluster = 16;     // non-portable cluster size limit (split-K merge in a cluster)
+constexpr int kAutoMaxCluster = 8;  // planner: portable cluster sizes only
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -45,6 +47,7 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         return PDA_ERR_UNSUPPORTED;
     if (o && (!(o->k_scale >= 0.f) || !(o->v_scale >= 0.f))) return PDA_ERR_SHAPE;
     if (o && (o->issue_mode < 0 || o->issue_mode > 2)) return PDA_ERR_SHAPE;
+    if (o && (o->merge < 0 || o->merge > 2)) return PDA_ERR_SHAPE;
     if (o && s->kv_dtype == PDA_E4M3 && o->issue_mode == 1) return PDA_ERR_UNSUPPORTED;
     if (o && o->issue_mode != 1 && (o->kernel == PDA_KERNEL_AUTO || o->kernel == PDA_KERNEL_SPLITK) &&
         o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32)
@@ -180,7 +183,6 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     const int stages = o->smem_stages ? o->smem_stages
                                       : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
     const int sms = o->num_sms ? o->num_sms : kDefaultSms;
-    (void)n_tiles;
     int64_t P;
     if (o->partition_tokens > 0) {
         P = o->partition_tokens;
@@ -206,8 +208,20 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->threads = pda::splitk_threads(self_issue(s, o));
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
+    // S8: merge partitions inside a thread-block cluster (DSMEM) when they fit
+    // one.  Auto only when the whole grid is one wave of resident CTAs: there
+    // the merge saves the combine launch (B=1-4, ctx 4k: 8-10 % faster); with
+    // more waves a cluster's CTAs hold their SMs while waiting for the slowest
+    // partner (B=16-64, ctx 4k: 14-15 % slower) -- DESIGN.md 7.
+    if (p_max > 1 && o->merge != 1) {
+        if (o->merge == 2 && p_max > kMaxCluster) return PDA_ERR_UNSUPPORTED;
+        const int64_t conc = (int64_t)sms * (n_tiles == 1 ? 3 : 2);
+        const bool one_wave = (int64_t)B * Hkv * p_max <= conc;
+        if (o->merge == 2 || (p_max <= kAutoMaxCluster && one_wave)) pl->cluster = (int32_t)p_max;
+    }
     const size_t rows = (size_t)B * q_tokens(s) * Hq;
-    pl->workspace_bytes = p_max > 1 ? align256(rows * p_max * D * 4) + align256(rows * p_max * 4) : 0;
+    pl->workspace_bytes = p_max > 1 && pl->cluster == 0
+                              ? align256(rows * p_max * D * 4) + align256(rows * p_max * 4) : 0;
     return PDA_OK;
 }
 
@@ -414,8 +428,10 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.outs.Hq_out = n_peers > 0 ? hq_out : s->num_q_heads;
     const size_t o_bytes =
         align256((size_t)s->num_seqs * q_tokens(s) * s->num_q_heads * pl.p_max * s->head_dim * 4);
-    p.ws_o = pl.p_max > 1 ? static_cast<float*>(ws) : nullptr;
-    p.ws_lse = pl.p_max > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
+    const bool via_ws = pl.p_max > 1 && pl.cluster == 0;
+    p.ws_o = via_ws ? static_cast<float*>(ws) : nullptr;
+    p.ws_lse = via_ws ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
+    p.cluster = pl.cluster;
     p.trace = trace;
     p.B = s->num_seqs;
     p.Hq = s->num_q_heads;
@@ -438,7 +454,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
                              pl.smem_stages, trace != nullptr,
                              dim3(pl.grid_x, pl.grid_y, pl.grid_z), stream, kv8, self_issue(s, o));
     if (err != cudaSuccess) return PDA_ERR_CUDA;
-    if (pl.p_max > 1) {
+    if (via_ws) {
         // S8 as its own small kernel: measured faster than merging in the last
         // partition CTA (the fused epilogue's fence + ticket cost every CTA a
         // few microseconds)
@@ -666,6 +682,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 11; }
+int32_t pda_abi_version(void) { return 12; }
 
 }  // extern "C"

@@ -220,4 +220,25 @@ __device__ __forceinline__ uint16_t cvt_e4m3x2(float a, float b) {
     return r;
 }
 
+// ---------------------------------------------------------------- clusters (DSMEM)
+// Cluster-wide barrier: every thread of every CTA of the cluster arrives
+// (release: its prior shared-memory writes become visible) and waits
+// (acquire).  All threads of a warp must execute it together.
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Shared-memory address of the same variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t cluster_map(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 }  // namespace pda

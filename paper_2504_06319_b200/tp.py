@@ -70,7 +70,7 @@ class TPDecodeAttention:
         opt = _lib.make_options(**{k: v for k, v in opts.items()
                                    if k in ("prefetch", "prefetch_distance", "partition_tokens",
                                             "smem_stages", "kernel", "stream_warps", "eviction",
-                                            "issue_mode")})
+                                            "issue_mode", "merge")})
         self.plan = _lib.plan(shape, opt)
         wsb = self.plan["workspace_bytes"]
         self.ws = torch.zeros(max(1, wsb), dtype=torch.uint8, device=dev)  # stream tickets start at 0
@@ -84,8 +84,9 @@ class TPDecodeAttention:
             self.peer_ptrs = list(self.symm.buffer_ptrs)
 
     def launches_per_step(self) -> int:
-        # split-K launches its combine kernel when sequences are split
-        return 1 + (1 if self.plan["kernel"] == 2 and self.plan["p_max"] > 1 else 0)
+        # split-K launches its combine kernel when sequences are split and the
+        # partitions do not merge inside a cluster
+        return 1 + (1 if self.plan["kernel"] == 2 and self.plan["p_max"] > 1 and not self.plan["cluster"] else 0)
 
     def __call__(self, q_local, block_tables, context_lens, scale):
         if self.fused:

@@ -53,7 +53,7 @@ def shape(**kw):
 
 def opts(**kw):
     d = dict(prefetch=1, prefetch_distance=4, partition_tokens=0, smem_stages=0, kernel=0, num_sms=0,
-             stream_warps=0, eviction=0, issue_mode=0, k_scale=0.0, v_scale=0.0)
+             stream_warps=0, eviction=0, issue_mode=0, k_scale=0.0, v_scale=0.0, merge=0)
     d.update(kw)
     return _lib.Options(**d)
 
@@ -131,9 +131,10 @@ def test_misaligned_pointer_rejected_before_launch():
 
 def test_workspace_required():
     L = pda.lib()
-    s, o = shape(max_blocks_per_seq=64), opts(partition_tokens=256)
+    s, o = shape(max_blocks_per_seq=64), opts(partition_tokens=256, merge=1)  # combine kernel
     need = pda.workspace_bytes(s, o)
     assert need > 0
+    assert pda.workspace_bytes(s, opts(partition_tokens=256)) == 0  # auto: merge in a cluster of 4
     base = 0x10000000
     rc = L.paged_decode_attention(base, base, base, base, base, 1.0, base, ctypes.byref(s),
                                   ctypes.byref(o), None, 0, None)
@@ -157,8 +158,11 @@ def test_plan_split_llama3_8b():
               max_blocks_per_seq=512, dtype=1, out_dtype=1)
     p = pda.plan(s, opts(kernel=2))
     assert p["p_max"] == 2 and p["partition_tokens"] == 4096
+    assert p["cluster"] == 0  # 2048 CTAs > one wave: combine kernel (auto)
+    assert pda.plan(s, opts(kernel=2, merge=2))["cluster"] == 2
+    pc = pda.plan(s, opts(kernel=2, merge=1))
     B, Hq, P, D = 128, 32, 2, 128
-    assert p["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
+    assert pc["cluster"] == 0 and pc["workspace_bytes"] == B * Hq * P * D * 4 + B * Hq * P * 4
 
 
 def test_plan_explicit_partition_and_paper():
@@ -211,7 +215,7 @@ def test_eviction_auto_resolution():
 def test_multi_token_needs_splitk_and_sizes_workspace():
     s = shape(q_len=4, max_blocks_per_seq=64)
     assert pda.check_args(s, opts(kernel=1)) == 3 and pda.check_args(s, opts(kernel=4)) == 3
-    p = pda.plan(s, opts(kernel=2, partition_tokens=256))
+    p = pda.plan(s, opts(kernel=2, partition_tokens=256, merge=1))
     rows = 2 * 4 * 4  # B * q_len * Hq
     assert p["p_max"] == 4 and p["workspace_bytes"] == rows * 4 * 64 * 4 + ((rows * 4 * 4 + 255) // 256) * 256
 
@@ -226,7 +230,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 11
+    assert pda.lib().pda_abi_version() == 12
 
 
 def test_product_never_imports_oracle():
@@ -274,3 +278,17 @@ def test_host_async_entry_rejects_before_launch():
     rc = L.pda_decode_step_host_async(*args[:8], base, base, 1.0, ctypes.byref(s), ctypes.byref(o), None, 0,
                                       None, None, None, base)
     assert rc == 1  # NULL inputs_ready event
+
+
+def test_cluster_merge_planning():
+    """Auto: clusters for 2 <= P_max <= 8; explicit cluster up to 16; beyond: unsupported."""
+    s = shape(max_blocks_per_seq=64)  # 1024 tokens
+    assert pda.plan(s, opts(partition_tokens=128))["cluster"] == 8
+    p16 = pda.plan(s, opts(partition_tokens=64))
+    assert p16["cluster"] == 0 and p16["workspace_bytes"] > 0  # auto: 16 > 8 -> combine kernel
+    assert pda.plan(s, opts(partition_tokens=64, merge=2))["cluster"] == 16
+    assert pda.check_args(s, opts(merge=3)) == 2
+    info = _lib.PlanInfo()
+    assert pda.lib().pda_plan(ctypes.byref(s), ctypes.byref(opts(partition_tokens=32, merge=2)),
+                              ctypes.byref(info)) == 3  # 32 partitions do not fit a cluster
+    assert pda.plan(s, opts(partition_tokens=1024))["cluster"] == 0  # single partition

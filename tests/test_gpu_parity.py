@@ -729,3 +729,66 @@ def test_large_batch_short_contexts(pda, oracle_mod):
     seqs = [0, 1, 4095, 8191] + [int(i) for i in np.flatnonzero(np.array(lens) == 0)[:2]]
     sub = synth.sample_rows(inp, seqs)
     assert max_err(out[seqs], oracle_out(oracle_mod, sub)) <= TOL
+
+
+# ---- S8 merge inside a thread-block cluster (DSMEM) vs the combine kernel ---------
+
+CLUSTER_CASES = [
+    (SHAPES[1], dict(partition_tokens=64)),                      # mha, ragged, P_max 5
+    (SHAPES[2], dict(partition_tokens=128)),                     # gqa4 bf16, P_max 8
+    (SHAPES[3], dict(partition_tokens=64, merge="cluster")),     # gqa8, P_max 13 (non-portable)
+    (SHAPES[4], dict(partition_tokens=32, issue_mode="producer")),  # gqa16 (2 head tiles), producer warp
+    (synth.Config("zero_len_long", 3, 4, 2, 64, (0, 100, 0), "fp16", poison_blocks=1),
+     dict(partition_tokens=16)),                                 # zero-length rows, P_max 7
+]
+
+
+@pytest.mark.parametrize("cfg,kw", CLUSTER_CASES, ids=lambda x: x.name if hasattr(x, "name") else
+                         "-".join(f"{a}{b}" for a, b in x.items()))
+def test_cluster_merge_bitwise_equals_combine(pda, oracle_mod, cfg, kw):
+    inp = synth.make_inputs(cfg, seed=23)
+    dev = to_dev(inp)
+    kw = dict(kw)
+    mode = kw.pop("merge", "auto")
+    info = pda.plan(pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"]), pda.make_options(merge=mode, **kw))
+    assert info["cluster"] == info["p_max"] > 1
+    a = gpu(pda, dev, merge=mode, **kw)
+    b = gpu(pda, dev, merge="combine", **kw)
+    assert torch.equal(a, b)
+    assert max_err(a, oracle_out(oracle_mod, inp)) <= TOL
+
+
+def test_cluster_merge_multi_token_kv8_gather_trace(pda, oracle_mod):
+    # multi-token
+    dev = to_dev(synth.with_query_tokens(synth.make_inputs(MQ_CASES[1][0], seed=24), 4))
+    assert torch.equal(gpu(pda, dev, partition_tokens=64), gpu(pda, dev, partition_tokens=64, merge="combine"))
+    # e4m3 cache
+    d8 = to_dev(kv8(synth.make_inputs(KV8_SHAPES[1], seed=25)))
+    assert torch.equal(gpu_kv8(pda, d8, partition_tokens=128), gpu_kv8(pda, d8, partition_tokens=128,
+                                                                         merge="combine"))
+    # fused TP gather destinations
+    cfg = synth.Config("cl_fg", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
+    d = to_dev(synth.make_inputs(cfg, seed=26))
+    ref = gpu(pda, d, partition_tokens=64, merge="combine")
+    peers = [torch.full((3, 16, 128), 7.0, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    pda.paged_decode_attention_gather(d["q"], d["k_cache"], d["v_cache"], d["block_tables"], d["context_lens"],
+                                      d["scale"], peers, 8, 16, partition_tokens=64)
+    torch.cuda.synchronize()
+    for pb in peers:
+        assert torch.equal(pb[:, 8:], ref) and (pb[:, :8] == 7.0).all()
+    # the kernel's own bookkeeping is unchanged by the merge mode
+    inp = synth.make_inputs(SHAPES[2], seed=27)
+    dv = to_dev(inp)
+    _, tr_a, _ = gpu(pda, dv, partition_tokens=128, trace=True)
+    _, tr_b, _ = gpu(pda, dv, partition_tokens=128, merge="combine", trace=True)
+    assert torch.equal(tr_a, tr_b)
+
+
+def test_cluster_merge_full_size_c3(pda, oracle_mod):
+    """BASELINE C3 (P_max 2, the bench partitioning): clusters of 2 == combine, bitwise."""
+    inp = synth.make_inputs(synth.C3_LLAMA3_8B, seed=28, device="cuda")
+    a = gpu(pda, inp, merge="cluster")
+    b = gpu(pda, inp, merge="combine")
+    assert torch.equal(a, b)
+    seqs = [0, 127]
+    assert max_err(a[seqs], oracle_out(oracle_mod, synth.sample_rows(inp, seqs))) <= TOL
