@@ -151,6 +151,8 @@ def make_shape(q, k_cache, block_tables, out_dtype=None) -> Shape:
 
 
 MERGE = {"auto": 0, "combine": 1, "cluster": 2}
+OPTION_KEYS = ("prefetch", "prefetch_distance", "partition_tokens", "smem_stages", "kernel", "num_sms",
+               "stream_warps", "eviction", "k_scale", "v_scale", "issue_mode", "merge")
 
 
 def make_options(prefetch=DEFAULT_PREFETCH, prefetch_distance=None, partition_tokens=0,
@@ -307,6 +309,48 @@ def validate_inputs(block_tables, context_lens, num_blocks, block_size=16, strea
     _check(lib().pda_validate_inputs(block_tables.data_ptr(), context_lens.data_ptr(), ctypes.byref(shape),
                                      counts.data_ptr(), _stream_handle(stream)), "pda_validate_inputs")
     return tuple(int(c) for c in counts.cpu())
+
+
+class PreparedDecode:
+    """paged_decode_attention with shape, options, plan, workspace and output
+    fixed at construction: a call only marshals the data pointers (the
+    per-call Python checks of paged_decode_attention cost ~13 us of host time,
+    more than a small step's GPU time).  Calls must use tensors of the shapes
+    and dtypes given here (checked cheaply: q shape, cache shape).
+
+    step = PreparedDecode(q, k_cache, block_tables, **options)
+    out = step(q, k_cache, v_cache, block_tables, context_lens, scale)
+    """
+
+    def __init__(self, q, k_cache, block_tables, out_dtype=None, device=None, **opt_kw):
+        import torch
+        if k_cache.dtype in (torch.uint8, torch.float8_e4m3fn) and out_dtype is None:
+            out_dtype = q.dtype
+        self.shape = make_shape(q, k_cache, block_tables, out_dtype)
+        self.opts = make_options(**opt_kw)
+        self.info = plan(self.shape, self.opts)
+        dev = device if device is not None else k_cache.device
+        self.wsb = self.info["workspace_bytes"]
+        self.ws = torch.zeros(max(1, self.wsb), dtype=torch.uint8, device=dev)  # tickets start at 0
+        self._ws_ptr = self.ws.data_ptr() if self.wsb else None
+        self.out = torch.empty(tuple(q.shape), dtype=out_dtype or q.dtype, device=dev)
+        self._q_shape, self._k_shape = tuple(q.shape), tuple(k_cache.shape)
+        self._shape_ref, self._opts_ref = ctypes.byref(self.shape), ctypes.byref(self.opts)
+        self._fn = lib().paged_decode_attention
+
+    def __call__(self, q, k_cache, v_cache, block_tables, context_lens, scale, out=None, stream=None):
+        if q.shape != self._q_shape or k_cache.shape != self._k_shape:
+            raise ValueError("PreparedDecode: tensor shapes differ from the prepared ones")
+        o = self.out if out is None else out
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        st = self._fn(q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(),
+                      context_lens.data_ptr(), scale, o.data_ptr(), self._shape_ref, self._opts_ref, self._ws_ptr,
+                      self.wsb, stream.cuda_stream)
+        if st:
+            raise PdaError(st, "paged_decode_attention")
+        return o
 
 
 def paged_decode_attention_gather(q, k_cache, v_cache, block_tables, context_lens, scale, out_peers,

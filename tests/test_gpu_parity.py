@@ -792,3 +792,15 @@ def test_cluster_merge_full_size_c3(pda, oracle_mod):
     assert torch.equal(a, b)
     seqs = [0, 127]
     assert max_err(a[seqs], oracle_out(oracle_mod, synth.sample_rows(inp, seqs))) <= TOL
+
+
+def test_prepared_decode_matches_wrapper(pda):
+    for cfg, kw in ((SHAPES[2], dict(partition_tokens=64)), (SHAPES[0], dict(kernel="paper")),
+                    (SHAPES[3], dict(kernel="balanced"))):
+        dev = to_dev(synth.make_inputs(cfg, seed=29))
+        step = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], **kw)
+        a = step(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"], dev["scale"])
+        b = gpu(pda, dev, **kw)
+        assert torch.equal(a, b)
+        with pytest.raises(ValueError):
+            step(dev["q"][:1], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"], dev["scale"])
