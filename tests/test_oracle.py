@@ -583,3 +583,63 @@ def test_attention_after_append_is_attention_over_concatenation(oracle_mod):
             w = np.exp(s - s.max())
             w /= w.sum()
             assert np.abs(out[b, h] - w @ V).max() < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# Property-based pins (hypothesis): random shapes, lengths, placements, scales
+# ---------------------------------------------------------------------------
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=30, deadline=None)
+@given(B=st.integers(1, 3), Hkv=st.integers(1, 2), g=st.sampled_from([1, 2, 4]), D=st.sampled_from([16, 64]),
+       lens=st.lists(st.integers(0, 70), min_size=3, max_size=3), dtype=st.sampled_from(["fp16", "bf16"]),
+       seed=st.integers(0, 10_000), scale=st.sampled_from([None, 1.0, 0.3]))
+def test_property_oracle_equals_contiguous_softmax(oracle_mod, B, Hkv, g, D, lens, dtype, seed, scale):
+    cfg = synth.Config("prop", B, Hkv * g, Hkv, D, tuple(lens[:B]), dtype, poison_blocks=2)
+    inp = synth.make_inputs(cfg, seed=seed)
+    if scale is not None:
+        inp["scale"] = scale
+    out = run_oracle(oracle_mod, inp)
+    for b in range(B):
+        for h in range(Hkv * g):
+            np.testing.assert_allclose(out[b, h], contiguous_reference(inp, b, h), rtol=0, atol=1e-12)
+
+
+@settings(max_examples=20, deadline=None)
+@given(lens=st.lists(st.integers(0, 60), min_size=2, max_size=2), q_len=st.integers(1, 4),
+       seed=st.integers(0, 10_000))
+def test_property_append_then_attend(oracle_mod, lens, q_len, seed):
+    """Append q_len rows then multi-token attend == causal attention over the
+    old rows with the new rows spliced in at positions L - q_len + i."""
+    cfg = synth.Config("prop_app", 2, 4, 2, 16, tuple(max(l, 1) for l in lens), "fp16", poison_blocks=1)
+    inp = synth.with_query_tokens(synth.make_inputs(cfg, seed=seed), q_len)
+    kn, vn = synth.new_kv_rows(inp, q_len, seed=seed)
+    kc, vc = oracle_mod.kv_append(kn, vn, inp["k_cache"], inp["v_cache"], inp["block_tables"], inp["context_lens"])
+    kt = torch.from_numpy(kc.view(np.int16)).view(torch.float16)
+    vt = torch.from_numpy(vc.view(np.int16)).view(torch.float16)
+    out = oracle_mod.paged_attention_mq(inp["q"], kt, vt, inp["block_tables"], inp["context_lens"], inp["scale"],
+                                        "fp16")
+    bt = inp["block_tables"].numpy()
+    for b in range(2):
+        L = int(inp["context_lens"][b])
+        for i in range(q_len):
+            Li = L - q_len + i + 1
+            for h in range(4):
+                kvh = h // 2
+                if Li <= 0:
+                    assert (out[b, i, h] == 0).all()
+                    continue
+                rows_k, rows_v = [], []
+                for t in range(Li):
+                    j = t - (L - q_len)  # index among the new rows, if this is one
+                    if 0 <= j < q_len:
+                        rows_k.append(kn[b, j, kvh].double().numpy())
+                        rows_v.append(vn[b, j, kvh].double().numpy())
+                    else:
+                        rows_k.append(inp["k_cache"][bt[b, t // 16], kvh, t % 16].double().numpy())
+                        rows_v.append(inp["v_cache"][bt[b, t // 16], kvh, t % 16].double().numpy())
+                K, V = np.stack(rows_k), np.stack(rows_v)
+                s = inp["scale"] * (K @ inp["q"][b, i, h].double().numpy())
+                w = np.exp(s - s.max())
+                np.testing.assert_allclose(out[b, i, h], (w / w.sum()) @ V, rtol=0, atol=1e-12)
