@@ -292,3 +292,18 @@ def test_cluster_merge_planning():
     assert pda.lib().pda_plan(ctypes.byref(s), ctypes.byref(opts(partition_tokens=32, merge=2)),
                               ctypes.byref(info)) == 3  # 32 partitions do not fit a cluster
     assert pda.plan(s, opts(partition_tokens=1024))["cluster"] == 0  # single partition
+
+
+@pytest.mark.parametrize("B,ctx,P,p_max,cluster", [
+    (1, 512, 128, 4, 4),      # tiny grid: down to 128-token partitions, merged in clusters
+    (4, 512, 128, 4, 4),
+    (16, 512, 512, 1, 0),     # 128 units at 512: no split
+    (1, 4096, 512, 8, 8),     # 64 units, one wave: cluster merge
+    (16, 4096, 1024, 4, 0),   # 512 units > one wave (444): combine kernel
+    (1, 32768, 1024, 32, 0),  # > 8 partitions: combine kernel
+])
+def test_planner_partitions_and_merge(B, ctx, P, p_max, cluster):
+    s = shape(num_seqs=B, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=100000,
+              max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1)
+    p = pda.plan(s, opts(kernel=2))
+    assert (p["partition_tokens"], p["p_max"], p["cluster"]) == (P, p_max, cluster)
