@@ -2,11 +2,13 @@
 // context partitions) and its combine kernel.
 //
 // One CTA per unit (partition p, kv head, sequence b); grid (P_max, Hkv, B).
-//  * Producer warp (warp 4): walks the unit's block-table slice (S1, Alg. 1
-//    line 3 "Lookup bt[block_idx]"), issues TMA tensor loads of the K
-//    and V slabs of each 16-token block into an S-stage shared-memory ring
-//    (S3, "Load K Block"), and -- the paper's method -- while issuing
-//    block j prefetches the K and V slabs of block j + d into L2 with
+//  * Ring refill (S1-S3): by default each of the 4 consumer warps refills the
+//    shared-memory ring stages it owns (self-issue); alternatively a producer
+//    warp (warp 4) does it.  The issuer walks the unit's block-table slice
+//    (S1, Alg. 1 line 3 "Lookup bt[block_idx]"), issues TMA tensor
+//    loads of the K and V slabs of each 16-token block into an S-stage ring
+//    (S3, "Load K Block"), and -- the paper's method, when prefetch is
+//    on -- prefetches the K and V slabs of block j + d into L2 with
 //    cp.async.bulk.prefetch.L2 iff j + d < e (S2, Alg. 1 lines 5-7,
 //    P:132-135; V blocks likewise).
 //  * 4 consumer warps take ring stages round-robin and compute, per block,
@@ -16,8 +18,12 @@
 //    accumulation.  Q stays in registers for the whole unit.
 //  * Epilogue (S7): the 4 warps' (m, l, acc) are merged through shared
 //    memory; a sequence with a single partition writes `out` directly,
-//    otherwise the normalised partial and its log2-sum-exp go to the
-//    workspace and combine_kernel (S8) merges partitions in fixed order.
+//    otherwise the normalised partial and its log2-sum-exp either go to the
+//    workspace for combine_kernel (S8, fixed partition order) or, when the
+//    grid was launched as clusters of the P_max partitions of a row, stay in
+//    shared memory and are merged over DSMEM by the cluster (same order).
+//  * Optional fused KV append: the new tokens' K/V rows are written by the
+//    warp that issues their block's load, before it does.
 #include "block_math.cuh"
 #include "kv_append.cuh"
 
