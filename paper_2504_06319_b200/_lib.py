@@ -353,6 +353,39 @@ class PreparedDecode:
         return o
 
 
+class GraphedDecode:
+    """A decode step captured once into a CUDA graph: replay() re-runs the
+    kernels on the static input buffers (q, block_tables, context_lens --
+    update them in place) for a few microseconds of host time, whatever the
+    step's size.  The caches stay the caller's tensors.
+
+    g = GraphedDecode(PreparedDecode(q, k_cache, bt), q, k_cache, v_cache, bt, lens, scale)
+    g.q.copy_(q_next); g.context_lens.add_(1); out = g.replay()
+    """
+
+    def __init__(self, prepared, q, k_cache, v_cache, block_tables, context_lens, scale, warmup=2):
+        import torch
+        self.prepared = prepared
+        self.q, self.block_tables, self.context_lens = q.clone(), block_tables.clone(), context_lens.clone()
+        self.k, self.v, self.scale = k_cache, v_cache, float(scale)
+        side = torch.cuda.Stream(device=q.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm up (module load, attributes) outside the capture
+            for _ in range(warmup):
+                self._step()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = self._step()
+
+    def _step(self):
+        return self.prepared(self.q, self.k, self.v, self.block_tables, self.context_lens, self.scale)
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+
 def paged_decode_attention_gather(q, k_cache, v_cache, block_tables, context_lens, scale, out_peers,
                                   head_offset, total_q_heads, *, out_dtype=None, workspace=None, stream=None,
                                   **opt_kw):

@@ -804,3 +804,19 @@ def test_prepared_decode_matches_wrapper(pda):
         assert torch.equal(a, b)
         with pytest.raises(ValueError):
             step(dev["q"][:1], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"], dev["scale"])
+
+
+def test_graphed_decode_replays_with_updated_inputs(pda, oracle_mod):
+    cfg = synth.Config("graphed", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
+    a_in, b_in = synth.make_inputs(cfg, seed=30), synth.make_inputs(cfg, seed=31)
+    dev = to_dev(a_in)
+    prep = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], partition_tokens=64)
+    g = pda.GraphedDecode(prep, dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"],
+                          dev["scale"])
+    out = g.replay().clone()
+    assert torch.equal(out, gpu(pda, dev, partition_tokens=64))
+    g.q.copy_(b_in["q"].cuda())                      # new queries, same cache
+    g.context_lens.copy_(torch.tensor([299, 16, 1], dtype=torch.int32))
+    out2 = g.replay().clone()
+    ref_in = dict(a_in, q=b_in["q"], context_lens=torch.tensor([299, 16, 1], dtype=torch.int32))
+    assert max_err(out2, oracle_out(oracle_mod, ref_in)) <= TOL
