@@ -133,6 +133,15 @@ cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace,
                           dim3 grid, cudaStream_t stream, bool kv8 = false, bool self_issue = false);
 size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8 = false);
+// per-MODE instantiation sets (decode_splitk_m{0,1,2}.cu): plain, debug trace, cluster-launched
+#define PDA_SPLITK_MODE_DECL(M)                                                                          \
+    cudaError_t launch_splitk_m##M(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p, \
+                                   bool bf16, int head_dim, int n_tiles, int stages, dim3 grid,          \
+                                   cudaStream_t stream, bool kv8, bool self_issue);
+PDA_SPLITK_MODE_DECL(0)
+PDA_SPLITK_MODE_DECL(1)
+PDA_SPLITK_MODE_DECL(2)
+#undef PDA_SPLITK_MODE_DECL
 int splitk_threads(bool self_issue = false);
 
 cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,
