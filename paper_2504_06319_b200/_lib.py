@@ -316,7 +316,9 @@ class PreparedDecode:
     fixed at construction: a call only marshals the data pointers (the
     per-call Python checks of paged_decode_attention cost ~13 us of host time,
     more than a small step's GPU time).  Calls must use tensors of the shapes
-    and dtypes given here (checked cheaply: q shape, cache shape).
+    and dtypes given here (checked cheaply: q shape, cache shape).  One
+    workspace and one default output per object: calls on several streams at
+    once need one object per stream.
 
     step = PreparedDecode(q, k_cache, block_tables, **options)
     out = step(q, k_cache, v_cache, block_tables, context_lens, scale)
