@@ -195,9 +195,24 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         // tiny grids that would stay under one CTA per SM even with 128-token
         // partitions go down to 128 (B=1-4, ctx 512: 12.3-14.3 us vs 16.4 us)
         const int64_t min_part = units0 * ceil_div(max_tokens, 128) <= sms ? 128 : 512;
-        while (units0 * split < 4 * conc &&
-               max_tokens / (split * 2) >= (units0 * split * 2 > 256 ? 1024 : min_part))
-            split *= 2;
+        // a single, well-filled wave (>= 0.4 of the resident CTA slots) of
+        // 512-8192-token partitions beats 1-4 ragged waves: take the smallest
+        // split that reaches it (measured: B=4 ctx 32k 88 vs 100 us, B=16 ctx
+        // 4k 49 vs 53, C2 at TP 8 94 vs 100; longer partitions prefer many
+        // waves: B=16 ctx 32k 280 vs 285)
+        int64_t one_wave = 0;
+        for (int64_t sp = 1; units0 * sp <= conc && max_tokens / sp >= 512; sp *= 2)
+            if (units0 * sp * 5 >= conc * 2 && max_tokens / sp <= 8192) {
+                one_wave = sp;
+                break;
+            }
+        if (one_wave) {
+            split = one_wave;
+        } else {
+            while (units0 * split < 4 * conc &&
+                   max_tokens / (split * 2) >= (units0 * split * 2 > 256 ? 1024 : min_part))
+                split *= 2;
+        }
         P = ceil_div(ceil_div(max_tokens, split), s->block_size) * s->block_size;
     }
     const int64_t p_max = ceil_div(max_tokens, P);

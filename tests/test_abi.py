@@ -299,7 +299,9 @@ def test_cluster_merge_planning():
     (4, 512, 128, 4, 4),
     (16, 512, 512, 1, 0),     # 128 units at 512: no split
     (1, 4096, 512, 8, 8),     # 64 units, one wave: cluster merge
-    (16, 4096, 1024, 4, 0),   # 512 units > one wave (444): combine kernel
+    (16, 4096, 2048, 2, 2),   # 256 units: one well-filled wave of 2048-token partitions
+    (64, 4096, 1024, 4, 0),   # 512 rows: four waves of 1024-token partitions, combine kernel
+    (16, 32768, 2048, 16, 0),  # long partitions prefer many waves
     (1, 32768, 1024, 32, 0),  # > 8 partitions: combine kernel
 ])
 def test_planner_partitions_and_merge(B, ctx, P, p_max, cluster):
