@@ -39,6 +39,24 @@ KERNEL_NAMES = {1: "paper_kernel", 2: "splitk_kernel", 3: "stream_kernel", 4: "b
 L2_BYTES = 126 * 1024 * 1024  # B200 L2
 
 
+class L2Flush:
+    """Evict L2 between timed steps without leaving it dirty: write 512 MiB
+    (every line of the previous step evicted), then read 256 MiB of another
+    buffer, so the lines the write left dirty are written back here, outside
+    the timed span, and not by the next step's loads (a write-only flush
+    charged the next step up to 126 MB of write-back, ~17 us)."""
+
+    def __init__(self, torch):
+        self.w = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(128 << 20, dtype=torch.float16, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
+        self.torch = torch
+
+    def __call__(self):
+        self.w.zero_()
+        self.torch.sum(self.r, dim=0, dtype=self.torch.float32, out=self.sink)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -304,8 +322,7 @@ def main():
 
     # steps whose KV fits in a few L2s would hit in L2 across back-to-back
     # steps: flush it between timed steps (outside the timed spans)
-    flush_buf = (torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-                 if local_cfg.kv_bytes() < 4 * L2_BYTES else None)
+    flush_buf = L2Flush(torch) if local_cfg.kv_bytes() < 4 * L2_BYTES else None
 
     def time_steps(fn, steps, warmup, join=None):
         for _ in range(warmup):
@@ -318,7 +335,7 @@ def main():
         if flush_buf is not None:
             spans = []
             for _ in range(steps):
-                flush_buf.zero_()
+                flush_buf()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 fn(q, bt, lens, scale)
@@ -373,7 +390,7 @@ def main():
             for _ in range(n_rep):
                 for k, fn in arms.items():
                     if flush_buf is not None:
-                        flush_buf.zero_()
+                        flush_buf()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn(q, bt, lens, scale)
@@ -440,7 +457,7 @@ def main():
             for _ in range(max(10, args.steps // 4)):
                 for k, fn in app_arms.items():
                     if flush_buf is not None:
-                        flush_buf.zero_()
+                        flush_buf()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn()
@@ -530,7 +547,7 @@ def main():
             "p_max": pl["p_max"],
             "l2": (f"no flush: inputs larger than L2 ({local_cfg.kv_bytes() / 1e9:.2f} GB KV per step vs 126 MB L2)"
                    if flush_buf is None else
-                   "L2 flushed between timed steps (512 MiB write outside the per-step CUDA-event spans)"),
+                   "L2 flushed between timed steps (512 MiB write + 256 MiB read, outside the per-step CUDA-event spans)"),
             "bytes_per_step": total_bytes,
         },
         "roofline": {

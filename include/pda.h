@@ -222,6 +222,23 @@ pda_status paged_decode_attention_trace(const void* q, const void* k_cache, cons
                                         void* workspace, size_t workspace_bytes, int32_t* trace,
                                         size_t trace_words, void* stream);
 
+/* Measurement only: paged_decode_attention_trace (split-K kernel; other
+ * kernels return PDA_ERR_UNSUPPORTED) that additionally writes, per unit u of
+ * the trace (u = (b * Hkv + kvh) * P_max + p), the unit CTA's timeline to the
+ * device buffer `stamps` (uint64, >= 3 * plan.trace_records words):
+ *   stamps[3u] = %globaltimer (ns) at CTA entry, stamps[3u+1] = at its exit,
+ *   stamps[3u+2] = the SM it ran on.
+ * Used to see the grid's ramp, drain and per-CTA stream rate (tools/timeline.py);
+ * the trace instantiation runs a few percent slower than the product kernel.
+ * NULL trace or stamps: PDA_ERR_NULL; short stamp buffer: PDA_ERR_SHAPE. */
+pda_status paged_decode_attention_timeline(const void* q, const void* k_cache, const void* v_cache,
+                                           const int32_t* block_tables,
+                                           const int32_t* context_lens, float scale, void* out,
+                                           const pda_shape* shape, const pda_options* opt,
+                                           void* workspace, size_t workspace_bytes, int32_t* trace,
+                                           size_t trace_words, uint64_t* stamps,
+                                           size_t stamp_words, void* stream);
+
 /* The decode step with the tensor-parallel output all-gather fused into its
  * stores (S9 fused): every output element this rank
  * computes is written directly into the output buffer of each of the n_peers
@@ -326,7 +343,7 @@ pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* st
 const char* pda_status_string(pda_status status);
 
 /* ABI version (bumped on any signature change). */
-int32_t pda_abi_version(void);  /* 12: cluster merge (options.merge, plan.cluster); 11: pda_decode_step_host_async; 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
+int32_t pda_abi_version(void);  /* 13: paged_decode_attention_timeline; 12: cluster merge (options.merge, plan.cluster); 11: pda_decode_step_host_async; 10: KV append + validate entries; 9: _gather entry; 8: q_len; 7: issue_mode; 6: e4m3 KV */
 
 #ifdef __cplusplus
 }

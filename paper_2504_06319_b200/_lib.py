@@ -87,6 +87,8 @@ def lib():
             L.paged_decode_attention.restype = i32
             L.paged_decode_attention_trace.argtypes = [p, p, p, p, p, f32, p, ps, po, p, sz, p, sz, p]
             L.paged_decode_attention_trace.restype = i32
+            L.paged_decode_attention_timeline.argtypes = [p, p, p, p, p, f32, p, ps, po, p, sz, p, sz, p, sz, p]
+            L.paged_decode_attention_timeline.restype = i32
             L.paged_decode_attention_gather.argtypes = [p, p, p, p, p, f32, p, i32, i32, i32, ps, po, p, sz, p]
             L.paged_decode_attention_gather.restype = i32
             L.pda_decode_step_host.argtypes = [p, p, p, p, p, p, p, p, p, p, f32, ps, po, p, sz, p]
@@ -202,7 +204,7 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
                            partition_tokens=0, smem_stages=0, kernel="auto", stream_warps=0,
                            num_sms=0, eviction=DEFAULT_EVICTION, k_scale=0.0, v_scale=0.0,
                            issue_mode=0, merge="auto", workspace=None, stream=None, trace=False, k_new=None,
-                           v_new=None):
+                           v_new=None, timeline=False):
     """Decode attention over a paged KV cache (see include/pda.h).
 
     q [B, Hq, D], k_cache/v_cache [num_blocks, Hkv, 16, D] (fp16/bf16 like q, or
@@ -210,7 +212,9 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     block_tables [B, max_blocks] int32, context_lens [B] int32, all CUDA.
     k_new/v_new [B, (q_len,) Hkv, D]: append the step's new tokens to the
     caches first (paged_decode_attention_append; fused in the split-K kernel).
-    Returns out [B, Hq, D] (and the int32 bookkeeping trace if trace=True).
+    Returns out [B, Hq, D] (and the int32 bookkeeping trace if trace=True;
+    timeline=True, split-K only, also returns the per-unit {start ns, end ns,
+    SM} uint64 stamps as an int64 tensor [units, 3] -- a measurement export).
     """
     import torch
     _require_cuda(q, k_cache, v_cache, block_tables, context_lens)
@@ -218,7 +222,7 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
         raise ValueError("k_new and v_new go together")
     if k_new is not None:
         _require_cuda(k_new, v_new)
-        if trace:
+        if trace or timeline:
             raise ValueError("trace and append are separate calls")
         if k_new.dtype != q.dtype or v_new.dtype != q.dtype:
             raise TypeError("k_new / v_new must have q's dtype")
@@ -249,6 +253,16 @@ def paged_decode_attention(q, k_cache, v_cache, block_tables, context_lens, scal
     ws_ptr = workspace.data_ptr() if (workspace is not None and wsb) else None
     s = _stream_handle(stream)
     L = lib()
+    if timeline:
+        words = info["trace_records"] * info["trace_rec_len"]
+        tr = torch.empty(max(1, words), dtype=torch.int32, device=q.device)
+        stamps = torch.zeros((max(1, info["trace_records"]), 3), dtype=torch.int64, device=q.device)
+        st = L.paged_decode_attention_timeline(
+            q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_tables.data_ptr(),
+            context_lens.data_ptr(), float(scale), out.data_ptr(), ctypes.byref(shape),
+            ctypes.byref(opts), ws_ptr, wsb, tr.data_ptr(), words, stamps.data_ptr(), stamps.numel(), s)
+        _check(st, "paged_decode_attention_timeline")
+        return out, tr, info, stamps
     if trace:
         words = info["trace_records"] * info["trace_rec_len"]
         tr = torch.empty(max(1, words), dtype=torch.int32, device=q.device)

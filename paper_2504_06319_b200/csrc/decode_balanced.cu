@@ -374,14 +374,8 @@ cudaError_t launch_b_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const B
                          int grid, cudaStream_t stream) {
     auto kern = balanced_kernel<BF16, D, NT, S, TRACE>;
     constexpr size_t smem = BLayout<D, NT, S>::kBytes;
-    static int configured_device = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_device != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured_device = dev;
-    }
+    static std::atomic<uint64_t> smem_set{0};
+    if (cudaError_t e = ensure_smem_limit(kern, smem, smem_set); e != cudaSuccess) return e;
     kern<<<grid, (kConsumerWarps + 1) * 32, smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();
 }

@@ -334,14 +334,8 @@ cudaError_t launch_stream_one(const CUtensorMap& tmK, const CUtensorMap& tmV, co
                               int grid, cudaStream_t stream) {
     auto kern = stream_kernel<BF16, D, NT, S, W, TRACE>;
     constexpr size_t smem = stream_smem_for<D, S, W>();
-    static int configured_device = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_device != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured_device = dev;
-    }
+    static std::atomic<uint64_t> smem_set{0};
+    if (cudaError_t e = ensure_smem_limit(kern, smem, smem_set); e != cudaSuccess) return e;
     kern<<<grid, W * 32, smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();
 }

@@ -4,9 +4,25 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace pda {
+
+// Raise a kernel's dynamic shared-memory limit once per device.  Thread-safe
+// (the library promises stateless, thread-safe calls): the per-device "done"
+// bits are atomic, and a concurrent duplicate cudaFuncSetAttribute is harmless.
+template <typename Kern>
+inline cudaError_t ensure_smem_limit(Kern kern, size_t smem, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
 
 constexpr int kBlockSize = 16;     // tokens per KV block
 constexpr int kConsumerWarps = 4;  // split-K kernel consumer warps
@@ -50,6 +66,7 @@ struct SplitKParams {
     float* ws_o;          // [B, Hq, P_max, D]   split-K partial outputs (normalised)
     float* ws_lse;        // [B, Hq, P_max]      log2-sum-exp of each partition
     int32_t* trace;       // debug trace (TRACE instantiation only)
+    uint64_t* stamps;     // TRACE only, optional: per unit {start ns, end ns, SM id} (timeline)
     int B, Hq, Hkv, g, max_blocks, part_tokens, p_max;
     int q_len;  // query tokens per sequence (multi-token decode); columns = q_len * g <= 16
     int out_dtype;

@@ -180,8 +180,8 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // partition keeps >= 512 tokens (32 blocks) to amortise pipeline fill.
     const int n_tiles = q_tokens(s) * (Hq / Hkv) <= 8 ? 1 : 2;
     // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
-    const int stages = o->smem_stages ? o->smem_stages
-                                      : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
+    int stages = o->smem_stages ? o->smem_stages
+                                : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
     const int sms = o->num_sms ? o->num_sms : kDefaultSms;
     int64_t P;
     if (o->partition_tokens > 0) {
@@ -216,6 +216,18 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         P = ceil_div(ceil_div(max_tokens, split), s->block_size) * s->block_size;
     }
     const int64_t p_max = ceil_div(max_tokens, P);
+    if (o->smem_stages == 0 && s->kv_dtype != PDA_E4M3 && n_tiles == 1) {
+        // A grid just past one wave at 3 CTAs/SM (8-stage rings) but within two
+        // waves at 4 CTAs/SM (4-stage rings, 34 KiB of shared memory; 127
+        // registers x 128 threads still fit 4): the shallower ring loses less to
+        // wave quantisation than to bytes in flight (measured, L2 flushed: B=64
+        // ctx 512 28.7 vs 32.8 us, B=64 ctx 1024 47.1 vs 51.2, B=128 ctx 512
+        // 45.1 vs 49.2; past two waves the 8-stage ring wins again: B=256 ctx
+        // 1024 133 vs 129, and one-wave grids keep their depth: B=32 ctx 512
+        // 22.5 vs 20.5)
+        const int64_t units = (int64_t)B * Hkv * p_max;
+        if (units > (int64_t)sms * 3 && units <= (int64_t)sms * 4 * 2) stages = 4;
+    }
     pl->kernel = PDA_KERNEL_SPLITK;
     pl->partition_tokens = (int32_t)(P < max_tokens ? P : ceil_div(max_tokens, s->block_size) * s->block_size);
     pl->p_max = (int32_t)p_max;
@@ -311,7 +323,8 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
                const int32_t* lens, float scale, void* out, const pda_shape* s,
                const pda_options* o, void* ws, size_t ws_bytes, int32_t* trace, size_t trace_words,
                cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0, int head_off = 0,
-               int hq_out = 0, const pda::AppendParams* app = nullptr) {
+               int hq_out = 0, const pda::AppendParams* app = nullptr, uint64_t* stamps = nullptr,
+               size_t stamp_words = 0) {
     pda_plan_info pl;
     pda_status st = plan(s, o, &pl);
     if (st != PDA_OK) return st;
@@ -321,6 +334,8 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         return PDA_ERR_ALIGN;
     if (pl.workspace_bytes > 0 && (!ws || ws_bytes < pl.workspace_bytes)) return PDA_ERR_WORKSPACE;
     if (trace && trace_words < (size_t)pl.trace_records * pl.trace_rec_len) return PDA_ERR_SHAPE;
+    if (stamps && (pl.kernel != PDA_KERNEL_SPLITK || !trace)) return PDA_ERR_UNSUPPORTED;
+    if (stamps && stamp_words < (size_t)pl.trace_records * 3) return PDA_ERR_SHAPE;
     if (s->num_seqs == 0) return PDA_OK;
     st = use_device_of(out);
     if (st != PDA_OK) return st;
@@ -451,6 +466,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.ws_lse = via_ws ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
     p.cluster = pl.cluster;
     p.trace = trace;
+    p.stamps = stamps;
     p.B = s->num_seqs;
     p.Hq = s->num_q_heads;
     p.Hkv = s->num_kv_heads;
@@ -530,6 +546,18 @@ pda_status paged_decode_attention_trace(const void* q, const void* k_cache, cons
     if (!trace) return PDA_ERR_NULL;
     return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
                workspace_bytes, trace, trace_words, static_cast<cudaStream_t>(stream));
+}
+
+pda_status paged_decode_attention_timeline(const void* q, const void* k_cache, const void* v_cache,
+                                           const int32_t* block_tables, const int32_t* context_lens,
+                                           float scale, void* out, const pda_shape* shape,
+                                           const pda_options* opt, void* workspace, size_t workspace_bytes,
+                                           int32_t* trace, size_t trace_words, uint64_t* stamps,
+                                           size_t stamp_words, void* stream) {
+    if (!trace || !stamps) return PDA_ERR_NULL;
+    return run(q, k_cache, v_cache, block_tables, context_lens, scale, out, shape, opt, workspace,
+               workspace_bytes, trace, trace_words, static_cast<cudaStream_t>(stream), nullptr, 0, 0, 0,
+               nullptr, stamps, stamp_words);
 }
 
 pda_status paged_decode_attention_gather(const void* q, const void* k_cache, const void* v_cache,
@@ -700,6 +728,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 12; }
+int32_t pda_abi_version(void) { return 13; }
 
 }  // extern "C"

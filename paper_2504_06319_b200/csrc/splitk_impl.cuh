@@ -105,9 +105,21 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
     const int e_tok = (part + 1) * P < L ? (part + 1) * P : L;
 
     int32_t* rec = nullptr;
+    uint64_t t_start = 0;
     if constexpr (TRACE) {
         rec = p.trace + ((size_t)(b * p.Hkv + kvh) * p.p_max + part) * p.trace_rec_len;
+        if (threadIdx.x == 0) t_start = globaltimer_ns();
     }
+    auto stamp_end = [&]() {  // timeline export (measurement only): thread 0
+        if constexpr (TRACE) {
+            if (p.stamps != nullptr && threadIdx.x == 0) {
+                uint64_t* st = p.stamps + ((size_t)(b * p.Hkv + kvh) * p.p_max + part) * 3;
+                st[0] = t_start;
+                st[1] = globaltimer_ns();
+                st[2] = sm_id();
+            }
+        }
+    };
 
     const int n_parts = (L + P - 1) / P;
 
@@ -152,6 +164,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         }
         if (clustered) {  // still merges its slice of the row
             cluster_merge();
+            stamp_end();
             return;
         }
         if (part == 0 && L <= 0) {  // context_len == 0 => zero rows (reading R6), every query token
@@ -161,6 +174,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
                 store_out_peers(p.outs, row, p.Hq, D, dd, 0.f, p.out_dtype);
             }
         }
+        stamp_end();
         return;
     }
     const int sb = s_tok / kBlockSize;
@@ -436,6 +450,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         }
     }
     if (clustered) cluster_merge();
+    stamp_end();
 }
 
 template <int D, int NT, int STAGES, bool KV8 = false>
@@ -451,14 +466,8 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
                        dim3 grid, cudaStream_t stream) {
     auto kern = splitk_kernel<BF16, D, NT, STAGES, MODE, KV8, SELF>;
     constexpr size_t smem = smem_bytes_for<D, NT, STAGES, KV8>();
-    static int configured_device = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_device != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured_device = dev;
-    }
+    static std::atomic<uint64_t> smem_set{0};
+    if (cudaError_t e = ensure_smem_limit(kern, smem, smem_set); e != cudaSuccess) return e;
     if (p.cluster > 1) {
         // one cluster per (seq, kv head) row: its P_max partition CTAs (grid.x == P_max)
         if (p.cluster > 8) {

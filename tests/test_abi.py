@@ -230,7 +230,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 12
+    assert pda.lib().pda_abi_version() == 13
 
 
 def test_product_never_imports_oracle():
@@ -309,3 +309,22 @@ def test_planner_partitions_and_merge(B, ctx, P, p_max, cluster):
               max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1)
     p = pda.plan(s, opts(kernel=2))
     assert (p["partition_tokens"], p["p_max"], p["cluster"]) == (P, p_max, cluster)
+
+
+@pytest.mark.parametrize("B, ctx, stages", [
+    (64, 512, 4),     # 512 units: past one wave at 3 CTAs/SM (444), one wave at 4 (592)
+    (128, 512, 4),    # 1024 units: within two waves at 4 CTAs/SM
+    (64, 1024, 4),
+    (32, 512, 8),     # 256 units: one wave either way, keep the deeper ring
+    (256, 512, 8),    # 2048 units: many waves, deeper ring wins
+    (256, 1024, 8),
+    (64, 4096, 8),    # split to 2048 units of 1024 tokens
+])
+def test_planner_ring_depth(B, ctx, stages):
+    s = shape(num_seqs=B, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=100000,
+              max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1)
+    assert pda.plan(s, opts(kernel=2))["smem_stages"] == stages
+    assert pda.plan(s, opts(kernel=2, smem_stages=12))["smem_stages"] == 12  # explicit depth wins
+    kv8 = shape(num_seqs=B, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=100000,
+                max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1, kv_dtype=3)
+    assert pda.plan(kv8, opts(kernel=2))["smem_stages"] == 16  # e4m3 keeps its own default

@@ -189,6 +189,24 @@ def test_trace_splitk_matches_oracle_plan(pda, oracle_mod, issue):
             assert np.array_equal(got, ref), (P, mode, d)
 
 
+def test_timeline_export_is_consistent(pda, oracle_mod):
+    """paged_decode_attention_timeline: same output and trace as the trace
+    call, one {start, end, SM} stamp per unit, end >= start, SM ids on chip."""
+    cfg = synth.Config("timeline", 3, 8, 2, 64, (37, 256, 0), "fp16", poison_blocks=3)
+    dev = to_dev(synth.make_inputs(cfg, seed=1))
+    for P in (64, 0):
+        out, tr, info = gpu(pda, dev, kernel="splitk", partition_tokens=P, trace=True)
+        out2, tr2, info2, st = gpu(pda, dev, kernel="splitk", partition_tokens=P, timeline=True)
+        assert torch.equal(out, out2) and torch.equal(tr, tr2)
+        st = st.cpu()
+        assert st.shape == (info["trace_records"], 3)
+        assert (st[:, 0] > 0).all() and (st[:, 1] >= st[:, 0]).all()
+        nsm = torch.cuda.get_device_properties(0).multi_processor_count
+        assert ((st[:, 2] >= 0) & (st[:, 2] < nsm)).all()
+    with pytest.raises(RuntimeError):
+        gpu(pda, dev, kernel="paper", timeline=True)
+
+
 def test_trace_paper_matches_alg1(pda, oracle_mod):
     cfg = synth.Config("trace_p", 3, 4, 2, 128, (16, 128, 300), "fp16", poison_blocks=3)
     dev = to_dev(synth.make_inputs(cfg, seed=2))

@@ -17,7 +17,7 @@ from cuda.bindings import runtime as rt
 
 import paper_2504_06319_b200 as pda
 import synth
-from bench import workload_config
+from bench import L2Flush, workload_config
 
 
 def check(err):
@@ -45,7 +45,7 @@ def main():
     err, max_persist = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrMaxPersistingL2CacheSize, dev)
     err2, max_window = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrMaxAccessPolicyWindowSize, dev)
     check(rt.cudaDeviceSetLimit(rt.cudaLimit.cudaLimitPersistingL2CacheSize, max_persist))
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(torch)
     for name in sys.argv[1:]:
         cfg = workload_config(name)
         inp = synth.make_inputs(cfg, seed=0, device="cuda")
@@ -69,7 +69,7 @@ def main():
                         step()
                     for _ in range(20):
                         if flushed:
-                            flush.zero_()
+                            flush()
                         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         a.record(stream)
                         step()

@@ -9,7 +9,7 @@ import torch
 
 import paper_2504_06319_b200 as pda
 import synth
-from bench import workload_config
+from bench import L2Flush, workload_config
 
 cfg = workload_config(sys.argv[1])
 variants = eval(sys.argv[2])
@@ -22,7 +22,7 @@ if kv8:
     inp = synth.quantize_kv_e4m3(inp)
     variants = [dict(v, k_scale=inp["k_scale"], v_scale=inp["v_scale"]) for v in variants]
 ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
-flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush = L2Flush(torch)
 res = {}
 graphs = {}
 outs = {}
@@ -39,7 +39,7 @@ for rnd in range(5):
     for i in graphs:
         spans = []
         for _ in range(3):  # all reps queued, one sync: no host gaps inside a span
-            flush.zero_()
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); graphs[i].replay(); e1.record()
             spans.append((e0, e1))

@@ -5,7 +5,8 @@ ring depth x prefetch mode/distance, on one B200.
 
 Every variant of a cell runs on the same inputs; variants are interleaved in
 rounds (ABAB...) and each timed iteration is preceded by an L2 flush (a
-512 MiB memset, untimed) so small cells do not run out of L2.  Times are
+512 MiB memset, then a 256 MiB read so no dirty lines are left for the step
+to write back; untimed) so small cells do not run out of L2.  Times are
 CUDA-event medians per iteration.  One JSON line per (cell, variant).
 """
 import argparse
@@ -83,8 +84,9 @@ def main():
 
     import paper_2504_06319_b200 as pda
     import synth
+    from bench import L2Flush
     pda.lib()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(torch)
     keep = set(filter(None, a.cells.split(",")))
     f = open(a.out, "a")
     for cfg in cells(a.quick):
@@ -127,7 +129,7 @@ def main():
                         graphs[i] = g
                 spans = []
                 for _ in range(a.reps):  # all reps queued, one sync: no host gaps inside a span
-                    flush.zero_()
+                    flush()
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record()
