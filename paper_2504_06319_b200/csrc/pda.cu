@@ -75,7 +75,8 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
             return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (s->kv_dtype == PDA_E4M3) {
-        if (o->smem_stages != 0 && o->smem_stages != 8 && o->smem_stages != 16 && o->smem_stages != 24)
+        if (o->smem_stages != 0 && o->smem_stages != 8 && o->smem_stages != 12 && o->smem_stages != 16 &&
+            o->smem_stages != 24)
             return PDA_ERR_UNSUPPORTED;
         if (o->prefetch != PDA_PF_OFF && o->prefetch_distance > 32) return PDA_ERR_UNSUPPORTED;
     } else if (o->smem_stages != 0 && o->smem_stages != 4 && o->smem_stages != 8 &&
@@ -182,6 +183,14 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
     int stages = o->smem_stages ? o->smem_stages
                                 : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
+    if (o->smem_stages == 0 && s->kv_dtype == PDA_E4M3 && n_tiles == 1 &&
+        2.0 * B * (double)max_tokens * Hkv * D <= 1073741824.0) {
+        // e4m3 steps up to 1 GiB of KV: 12 stages consumed one block at a time
+        // at 4 CTAs/SM beat 16 stages in pairs at 3 (B=64 ctx 4k 81.9 vs 84.0 us,
+        // B=64 ctx 512 22.6 vs 28.7, B=4 ctx 4k 20.5 vs 24.6); multi-GB steps keep
+        // 16 (C2 321.5 vs 323.7, C5 1268.7 vs 1273.9; profiles/r01_ab_kv8_s12.log)
+        stages = 12;
+    }
     const int sms = o->num_sms ? o->num_sms : kDefaultSms;
     int64_t P;
     if (o->partition_tokens > 0) {

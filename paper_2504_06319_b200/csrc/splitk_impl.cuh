@@ -64,8 +64,13 @@ constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) 
 // MODE: 0 = plain, 1 = debug trace (+ runtime cluster support), 2 = launched
 // as clusters (merge over DSMEM).  The plain instantiation carries no cluster
 // code at all (it cost 4 registers and 1-2 us on small steps).
+// e4m3 with a 12-stage ring: blocks one at a time (no pairs), 4 CTAs per SM
+// (16 warps, 4 x 48 KiB in flight) instead of 3 x 16 stages consumed in pairs.
+template <bool KV8, int STAGES, int NT>
+constexpr int splitk_min_blocks() { return (KV8 && STAGES == 12 && NT == 1) ? 4 : (NT == 1 ? 3 : 2); }
+
 template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF>
-__global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
+__global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_blocks<KV8, STAGES, NT>())
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
     constexpr bool TRACE = MODE == 1;
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), NT == 1 ? 3 : 2)
         // stages it just read: it owns every stage s with (s / PAIR) % 4 == w, so
         // no empty barriers are needed and a parity wait always refers to the
         // warp's own previous fill.
-        constexpr int PAIR = KV8 ? 2 : 1;
+        constexpr int PAIR = (KV8 && STAGES % 8 == 0) ? 2 : 1;
         static_assert(STAGES % (PAIR * kConsumerWarps) == 0, "stages must split evenly over the warps");
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;  // <= 32 (validated)
@@ -506,9 +511,10 @@ cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, cons
 template <bool BF16, int NT, int MODE>
 cudaError_t dispatch_stages_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                                 int stages, dim3 grid, cudaStream_t s) {
-    // 4 KiB stages, consumed in pairs: depth a multiple of 8
+    // 4 KiB stages, consumed in pairs (depth a multiple of 8) or singly (12)
     switch (stages) {
         case 8: return launch_one<BF16, 128, NT, 8, MODE, true, true>(tmK, tmV, p, grid, s);
+        case 12: return launch_one<BF16, 128, NT, 12, MODE, true, true>(tmK, tmV, p, grid, s);
         case 16: return launch_one<BF16, 128, NT, 16, MODE, true, true>(tmK, tmV, p, grid, s);
         case 24: return launch_one<BF16, 128, NT, 24, MODE, true, true>(tmK, tmV, p, grid, s);
         default: return cudaErrorInvalidValue;

@@ -327,4 +327,8 @@ def test_planner_ring_depth(B, ctx, stages):
     assert pda.plan(s, opts(kernel=2, smem_stages=12))["smem_stages"] == 12  # explicit depth wins
     kv8 = shape(num_seqs=B, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=100000,
                 max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1, kv_dtype=3)
-    assert pda.plan(kv8, opts(kernel=2))["smem_stages"] == 16  # e4m3 keeps its own default
+    # e4m3: 12 single-block stages at 4 CTAs/SM up to 1 GiB of e4m3 KV, else 16 in pairs
+    assert pda.plan(kv8, opts(kernel=2))["smem_stages"] == (12 if 2 * B * ctx * 8 * 128 <= 1 << 30 else 16)
+    big8 = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
+                 max_blocks_per_seq=256, kv_dtype=3)  # C2 in e4m3: 2.1 GB
+    assert pda.plan(big8, opts(kernel=2))["smem_stages"] == 16

@@ -398,6 +398,7 @@ KV8_SHAPES = [
 @pytest.mark.parametrize("cfg", KV8_SHAPES, ids=lambda c: c.name)
 @pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=64), dict(smem_stages=8),
                                 dict(smem_stages=16, partition_tokens=256), dict(smem_stages=24),
+                                dict(smem_stages=12), dict(smem_stages=12, partition_tokens=48),
                                 dict(partition_tokens=16), dict(partition_tokens=48)],
                          ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
 def test_kv8_parity_vs_oracle(pda, oracle_mod, cfg, kw):
@@ -431,8 +432,9 @@ def test_kv8_context_one_is_scaled_v_row(pda):
 def test_kv8_trace_matches_oracle_plan(pda, oracle_mod):
     cfg = synth.Config("kv8_trace", 3, 8, 2, 128, (37, 256, 0), "fp16", poison_blocks=3)
     dev = to_dev(kv8(synth.make_inputs(cfg, seed=1)))
-    for P in (16, 64, 0):
-        _, tr, info = gpu_kv8(pda, dev, partition_tokens=P, prefetch="line", prefetch_distance=3, trace=True)
+    for P, st in ((16, 0), (64, 0), (0, 0), (48, 12), (0, 12)):
+        _, tr, info = gpu_kv8(pda, dev, partition_tokens=P, prefetch="line", prefetch_distance=3, trace=True,
+                              smem_stages=st)
         ref = oracle_mod.plan_splitk(dev["block_tables"], dev["context_lens"], 2, 16, info["partition_tokens"],
                                      info["p_max"], 3)
         assert np.array_equal(tr.cpu().numpy().reshape(ref.shape), ref)

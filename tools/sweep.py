@@ -23,6 +23,7 @@ def variants(quick):
     vs = []
     stages = [4, 8] if quick else [4, 8, 12]
     dists = [2, 8] if quick else [1, 2, 4, 8, 16, 32]
+    vs.append(dict(kernel="splitk", prefetch="off"))  # the library default (planner-chosen ring depth)
     for s in stages:
         vs.append(dict(kernel="splitk", smem_stages=s, prefetch="off"))
         for d in dists:

@@ -34,25 +34,27 @@ def main():
     x = lambda r: f"{r['speedup_vs_off']:.3f}" if r else "-"
     us = lambda r: f"{r['us_median']:.1f}" if r else "-"
     print(f"# Sweep report ({path.split('/')[-1]})\n")
-    print("One B200; per cell all variants on the same inputs, 3 interleaved rounds x 7 reps, 512 MiB L2 "
-          "flush before each iteration, CUDA-event median of a CUDA-graph replay.  Every prefetch / eviction "
+    print("One B200; per cell all variants on the same inputs, interleaved rounds of graph replays, an L2 "
+          "flush before each iteration (512 MiB write + 256 MiB read in the newer sweeps, write only in the "
+          "older ones, which then charge the step up to 126 MB of dirty-line write-back), CUDA-event median of a CUDA-graph replay.  Every prefetch / eviction "
           f"variant's output is bitwise equal to the same kernel with prefetch off ({len(rows)} lines, asserted). "
           "GB/s = algorithmic bytes (KV + q + out + block tables; e4m3 KV counts 1 B/element) / time.\n")
     print("## Kernels\n")
-    print("| cell | B | ctx | KV GB | default: split-K self-issue S8 µs | GB/s | split-K producer-warp µs | "
+    print("| cell | B | ctx | KV GB | library default µs | GB/s | split-K self-issue S8 µs | split-K producer-warp µs | "
           "best split-K variant | balanced best µs | stream best µs | paper kernel µs | e4m3 KV µs (S16) | "
           "e4m3 speedup |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for c in cells:
         rs = [r for r in rows if r["cell"] == c]
-        d = get(c, kernel="splitk", smem_stages=8, prefetch="off")
+        d8 = get(c, kernel="splitk", smem_stages=8, prefetch="off")
+        d = get(c, kernel="splitk", smem_stages=None, prefetch="off") or d8
         pr = get(c, kernel="splitk", smem_stages=8, prefetch="off", issue_mode="producer")
         sk = min([r for r in rs if r["kernel"] == "splitk" and not r.get("kv")], key=lambda r: r["us_median"])
         bal = min([r for r in rs if r["kernel"] == "balanced"], key=lambda r: r["us_median"])
         st = min([r for r in rs if r["kernel"] == "stream"], key=lambda r: r["us_median"])
         pp = get(c, kernel="paper", prefetch="off")
         e8 = get(c, kernel="splitk", smem_stages=16, prefetch="off", kv="e4m3")
-        print(f"| {c} | {d['batch']} | {d['ctx']} | {d['kv_bytes'] / 1e9:.3f} | {us(d)} | {d['gbs']:.0f} | "
+        print(f"| {c} | {d['batch']} | {d['ctx']} | {d['kv_bytes'] / 1e9:.3f} | {us(d)} | {d['gbs']:.0f} | {us(d8)} | "
               f"{us(pr)} | {name(sk)}: {us(sk)} | {us(bal)} | {us(st)} | {us(pp)} | {us(e8)} | "
               f"{(d['us_median'] / e8['us_median']) if e8 else 0:.2f}x |")
     print("\n## Prefetch and eviction priority (speedup vs the same configuration with prefetch off)\n")
