@@ -484,6 +484,20 @@ def main():
             torch.cuda.synchronize()
             extras["read_roofline_gbs"] = buf.numel() * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
             del buf
+            # Eq. 1-2 and the L2 residency bound re-derived for this device (DESIGN 7.5)
+            l2 = getattr(torch.cuda.get_device_properties(dev_index), "L2_cache_size", L2_BYTES)
+            m_block = 16 * cfg.head_dim * 2  # Eq. 1: b * d_h * T_block
+            m_total_b1 = m_block * (128 // 32) * cfg.num_q_heads  # Eq. 2 at B=1 (paper kernel, K blocks)
+            plan = step_main.plan
+            sms = torch.cuda.get_device_properties(dev_index).multi_processor_count
+            resident = sms * (3 if plan["smem_stages"] >= 8 else 4)
+            extras["l2_capacity"] = {
+                "l2_bytes": l2, "m_block_bytes": m_block, "paper_kernel_m_total_b1_bytes": m_total_b1,
+                "residency_bound_batches": l2 // m_total_b1,
+                "splitk_prefetch_lookahead_bytes_per_block_of_distance": resident * 2 * m_block,
+                "splitk_distance_filling_l2": l2 // (resident * 2 * m_block),
+                "desc": "paper: 60 MB L2 / 512 KiB = 120 batches (P:180); split-K: resident CTAs x d x "
+                        "(K+V) M_block of L2 lookahead beyond the smem ring"}
 
     # the dominant kernel's own launch time (attention call alone, no gather)
     def attn_only(q_, bt_, lens_, scale_):

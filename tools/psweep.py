@@ -15,7 +15,8 @@ cfg = workload_config(sys.argv[1])
 variants = eval(sys.argv[2])
 kv8 = len(sys.argv) > 3 and sys.argv[3] == "kv8"
 q_len = int(sys.argv[4]) if len(sys.argv) > 4 else 1
-inp = synth.make_inputs(cfg, seed=0, device="cuda")
+# PSWEEP_CONTIGUOUS=1: identity block placement (sequential KV) instead of the shuffled pool
+inp = synth.make_inputs(cfg, seed=0, device="cuda", shuffle=os.environ.get("PSWEEP_CONTIGUOUS") != "1")
 if q_len > 1:
     inp = synth.with_query_tokens(inp, q_len)
 if kv8:
