@@ -183,14 +183,22 @@ struct BlockMath {
     // One block: K slab at kbase, V slab at vbase (shared addresses); vq =
     // L - (first token of the block): rows >= vq are outside the context (V
     // zeroed), and column c additionally masks rows >= vq - qoff[c].
+    // TAIL = false: the caller guarantees no masking is needed
+    // (needs_mask(vq) is false), so the masking code is not even issued
+    // (predicated-off masks still cost issue slots every block).
+    template <bool TAIL = true>
     __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk(kbase, lane, s, s2);
         uint32_t pb[NT][2], pb_lo[NT][2];
-        softmax(s, s2, vq, scale_log2, lane, pb, pb_lo);
-        pv(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb, pb_lo);
+        softmax<TAIL>(s, s2, vq, scale_log2, lane, pb, pb_lo);
+        pv<TAIL>(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb, pb_lo);
     }
+
+    // Does a block starting vq tokens before the context end need masking
+    // (some column's limit, or the context end, inside the block)?
+    __device__ __forceinline__ bool needs_mask(int vq) const { return vq - qm1 < kBlockSize; }
 
     // Mask the scores of rows outside each column's context (select, never
     // arithmetic: masked K rows may hold NaN).
@@ -231,6 +239,7 @@ struct BlockMath {
 
     // ---- S5: scale (fp32), mask t >= valid, online softmax per head column;
     // P leaves as PV B fragments (transposed in registers with movmatrix)
+    template <bool TAIL = true>
     __device__ __forceinline__ void softmax(float (&s)[NT][4], const float (&s2)[NT][4], int vq,
                                             float scale_log2, int lane, uint32_t (&pb)[NT][2],
                                             uint32_t (&pb_lo)[NT][2]) {
@@ -238,7 +247,7 @@ struct BlockMath {
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) s[nt][r] = (s[nt][r] + s2[nt][r]) * scale_log2;
-        mask_scores(s, vq, lane);
+        if constexpr (TAIL) mask_scores(s, vq, lane);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             float pr[4];
@@ -289,6 +298,7 @@ struct BlockMath {
     }
 
     // ---- S6: O^T[d][h] += sum_t V^T[d][t] P[t][h]
+    template <bool TAIL = true>
     __device__ __forceinline__ void pv(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2],
                                        const uint32_t (&pb_lo)[NT][2]) {
         const int v_t = (lane & 7) + (lane >> 4) * 8;
@@ -297,7 +307,7 @@ struct BlockMath {
         for (int i = 0; i < MT; ++i) {
             uint32_t a[4];
             ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
-            if (valid < kBlockSize) mask_v(a, valid, lane);
+            if (TAIL && valid < kBlockSize) mask_v(a, valid, lane);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 mma_16816<BF16>(acc[i][nt], a, pb[nt][0], pb[nt][1]);
@@ -403,6 +413,7 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
     }
 
     // ---- S6 on e4m3 V
+    template <bool TAIL = true>
     __device__ __forceinline__ void pv8(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2]) {
         const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
@@ -417,7 +428,7 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
                 cvt_e4m3x4(r[2 * c2 + 1], x1, y1);  // tokens 8-15
                 uint32_t a[4] = {movmatrix_trans(x0), movmatrix_trans(y0), movmatrix_trans(x1),
                                  movmatrix_trans(y1)};
-                if (valid < kBlockSize) Base::mask_v(a, valid, lane);
+                if (TAIL && valid < kBlockSize) Base::mask_v(a, valid, lane);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
                     mma_16816<false>(this->acc[2 * ip + c2][nt], a, pb[nt][0], pb[nt][1]);
@@ -425,18 +436,20 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         }
     }
 
+    template <bool TAIL = true>
     __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk8(kbase, lane, s, s2);
         uint32_t pb[NT][2], pb_lo[NT][2];
-        this->softmax(s, s2, vq, scale_log2, lane, pb, pb_lo);
-        pv8(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb);
+        this->template softmax<TAIL>(s, s2, vq, scale_log2, lane, pb, pb_lo);
+        pv8<TAIL>(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb);
     }
 
     // Two blocks (32 tokens) per step: independent QK chains, ONE online-softmax
     // update (shared max / rescale), two PV tiles -- halves the per-block
     // latency chain, which bounds the e4m3 path (half the bytes per block).
+    template <bool TAIL = true>
     __device__ __forceinline__ void block2(uint32_t kb0, uint32_t vb0, int vq0, uint32_t kb1, uint32_t vb1,
                                            int vq1, float scale_log2, int lane) {
         float sa[NT][4], sa2[NT][4], sb[NT][4], sb2[NT][4];
@@ -450,8 +463,10 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
                 sa[nt][r] = (sa[nt][r] + sa2[nt][r]) * scale_log2;
                 sb[nt][r] = (sb[nt][r] + sb2[nt][r]) * scale_log2;
             }
-        this->mask_scores(sa, vq0, lane);
-        this->mask_scores(sb, vq1, lane);
+        if constexpr (TAIL) {
+            this->mask_scores(sa, vq0, lane);
+            this->mask_scores(sb, vq1, lane);
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             float pra[4], prb[4];
@@ -481,8 +496,8 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
             pbb[nt][0] = movmatrix_trans(pack2<false>(prb[0], prb[1]));
             pbb[nt][1] = movmatrix_trans(pack2<false>(prb[2], prb[3]));
         }
-        pv8(vb0, vq0 < kBlockSize ? vq0 : kBlockSize, lane, pa);
-        pv8(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
+        pv8<TAIL>(vb0, vq0 < kBlockSize ? vq0 : kBlockSize, lane, pa);
+        pv8<TAIL>(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
     }
 
     // Output column d held by accumulator acc[i][*][r]: rows 0-7 of a tile are

@@ -358,15 +358,25 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
             if (two) mbar_wait(&full[st1], ((j + 1) / STAGES) & 1);
             const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
             const int v0 = L - (sb + j) * kBlockSize;  // tokens of the context from this block on
+            // masking only where a context / causal limit falls inside the block(s):
+            // a warp-uniform branch, so full blocks issue no mask instructions
             if constexpr (PAIR == 2) {
                 if (two) {
                     const int v1 = L - (sb + j + 1) * kBlockSize;
-                    bm.block2(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2, lane);
+                    if (bm.needs_mask(v1))
+                        bm.template block2<true>(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2,
+                                                 lane);
+                    else
+                        bm.template block2<false>(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2,
+                                                  lane);
                 } else {
-                    bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                    bm.template block<true>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
                 }
             } else {
-                bm.block(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                if (bm.needs_mask(v0))
+                    bm.template block<true>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                else
+                    bm.template block<false>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
             }
             mine += two ? 2 : 1;
             // our ldmatrix reads of the stages are complete (their registers fed the
@@ -388,7 +398,11 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
             const uint32_t round = j / STAGES;
             mbar_wait(&full[stage], round & 1);
             const uint32_t kbase = smem_u32(ring + stage * G::kStage);
-            bm.block(kbase, kbase + G::kSlab, L - (sb + j) * kBlockSize, p.scale_log2, lane);
+            const int vq = L - (sb + j) * kBlockSize;
+            if (bm.needs_mask(vq))
+                bm.template block<true>(kbase, kbase + G::kSlab, vq, p.scale_log2, lane);
+            else
+                bm.template block<false>(kbase, kbase + G::kSlab, vq, p.scale_log2, lane);
             mbar_arrive(&empty[stage]);  // ring slot free for the producer (32 lane arrivals)
         }
     }

@@ -357,6 +357,31 @@ def test_full_size_sampled(pda, oracle_mod, cfg):
     sampled_check(pda, oracle_mod, cfg, [1, B - 2], prefetch="off")
 
 
+@pytest.mark.parametrize("batch,ctx", [(64, 512), (128, 512), (64, 1024)])
+def test_sweep_cell_four_ctas_per_sm_sampled(pda, oracle_mod, batch, ctx):
+    """Sweep cells where the planner picks 4-stage rings at 4 CTAs/SM (DESIGN 6)."""
+    cfg = synth.sweep_cell(batch, ctx, seed=batch + ctx)
+    s = pda.make_shape(torch.empty((batch, 32, 128), dtype=torch.bfloat16, device="meta"),
+                       torch.empty((cfg.num_blocks, 8, 16, 128), dtype=torch.bfloat16, device="meta"),
+                       torch.empty((batch, cfg.max_blocks_per_seq), dtype=torch.int32, device="meta"))
+    assert pda.plan(s, pda.make_options())["smem_stages"] == 4
+    sampled_check(pda, oracle_mod, cfg, [0, batch // 2, batch - 1])
+
+
+@pytest.mark.parametrize("batch,ctx", [(64, 4096), (4, 4096)])
+def test_kv8_sweep_cell_twelve_stages_sampled(pda, oracle_mod, batch, ctx):
+    """e4m3 steps <= 1 GiB run 12 single-block stages at 4 CTAs/SM (DESIGN 6)."""
+    cfg = synth.sweep_cell(batch, ctx, seed=batch + ctx)
+    inp = kv8(synth.make_inputs(cfg, seed=0, device="cuda"))
+    out = gpu_kv8(pda, inp)
+    torch.cuda.synchronize()
+    seqs = [0, batch // 2, batch - 1]
+    sub = synth.sample_rows(inp, seqs)
+    sub.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
+    assert max_err(out[seqs], oracle_kv8(oracle_mod, sub)) <= TOL
+    assert torch.isfinite(out).all()
+
+
 def test_full_size_c5_tp8_shard(pda, oracle_mod):
     """Llama-3-70B shape, one TP=8 rank's shard (1 KV head, 8 q heads)."""
     cfg = synth.C5_LLAMA3_70B.with_heads(8, 1, name="c5_tp8_rank")
