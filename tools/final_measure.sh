@@ -9,3 +9,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:splitk_kernel -s 2 -c 1 \
     -o gpurun_out/end_prof_c2 python tools/one_step.py c2 > /dev/null 2>&1
 ls -la gpurun_out
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/end_bench_reference.json 2> gpurun_out/end_bench_reference.err
+ncu --set full --clock-control none --import-source on -k regex:splitk_kernel -s 2 -c 1 \
+    -o gpurun_out/end_prof_c2_kv8 python tools/one_step.py c2 "{}" kv8 > /dev/null 2>&1
+python tools/timeline.py c2 > gpurun_out/end_timeline.jsonl 2>/dev/null
+python tools/timeline.py c2 "{}" kv8 >> gpurun_out/end_timeline.jsonl 2>/dev/null
+python tools/timeline.py c4_b64_ctx4096 >> gpurun_out/end_timeline.jsonl 2>/dev/null
