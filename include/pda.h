@@ -129,9 +129,11 @@ typedef struct {
                                   stream / balanced kernels and e4m3 caches: d <= 32 */
     int32_t partition_tokens;  /* split-K partition size P in tokens; 0 = planner's choice;
                                   otherwise a positive multiple of block_size */
-    int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = default.
-                                  split-K: 4, 8 (default), 12 (per CTA); e4m3 cache: 8,
-                                  16 (default), 24 (blocks are consumed in pairs);
+    int32_t smem_stages;       /* shared-memory ring depth in blocks; 0 = planner's choice.
+                                  split-K: 4, 8, 12 per CTA (auto: 8, or 4 when the grid fits two
+                                  waves at 4 CTAs/SM but not one at 3); e4m3 cache: 8, 16, 24
+                                  (blocks consumed in pairs) or 12 (one at a time, 4 CTAs/SM)
+                                  (auto: 12 up to 1 GiB of e4m3 KV, else 16);
                                   balanced: 4, 8 (default), 12 (per CTA; multiples of the 4 consumer warps);
                                   stream: per warp, with stream_warps: (8,1), (4,2), (6,2) default, (4,4) */
     int32_t kernel;            /* pda_kernel */

@@ -332,3 +332,25 @@ def test_planner_ring_depth(B, ctx, stages):
     big8 = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
                  max_blocks_per_seq=256, kv_dtype=3)  # C2 in e4m3: 2.1 GB
     assert pda.plan(big8, opts(kernel=2))["smem_stages"] == 16
+
+
+def _build_c_example(tmp_path):
+    """examples/decode_step.c compiled and linked as plain C11 against the
+    header and libpda.so (the boundary needs no C++ and no PyTorch)."""
+    exe = tmp_path / "decode_step"
+    cmd = ["gcc", "-std=c11", "-pedantic", "-Wall", "-Wextra", "-Werror", f"-I{ROOT}/include",
+           "-I/usr/local/cuda/include", f"{ROOT}/examples/decode_step.c", f"-L{os.path.dirname(_lib.LIB_PATH)}",
+           "-lpda", "-L/usr/local/cuda/lib64", "-lcudart", "-lm",
+           f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_header_is_c99_and_c_example_links(tmp_path):
+    src = tmp_path / "h.c"
+    src.write_text('#include "pda.h"\nint main(void) { return pda_abi_version() > 0 ? 0 : 1; }\n')
+    r = subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", f"-I{ROOT}/include",
+                        "-fsyntax-only", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert _build_c_example(tmp_path).exists()

@@ -865,3 +865,14 @@ def test_graphed_decode_replays_with_updated_inputs(pda, oracle_mod):
     out2 = g.replay().clone()
     ref_in = dict(a_in, q=b_in["q"], context_lens=torch.tensor([299, 16, 1], dtype=torch.int32))
     assert max_err(out2, oracle_out(oracle_mod, ref_in)) <= TOL
+
+
+def test_c_example_runs(tmp_path):
+    """examples/decode_step.c: one decode step from plain C through the C ABI,
+    self-checked against the constant-V closed form (exit code 0)."""
+    import subprocess
+    from test_abi import _build_c_example
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 of 512 outputs off the closed form" in r.stdout
