@@ -104,8 +104,17 @@ __device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint1
                                           off * 2, pf_mode, lane, eviction, pol_last);
 }
 
-template <bool BF16, int D, int NT>
+// TOKPERM: MMA row m of S^T holds token tok_of_row(m) (the e4m3 path loads K
+// rows in that order so that its V^T fragments come straight from a
+// transposing byte ldmatrix, see BlockMathKV8); the contraction over tokens
+// is order-free, only the masks need the mapping.
+template <bool BF16, int D, int NT, bool TOKPERM = false>
 struct BlockMath {
+    // rows m = 2c + e -> token 4c + e, rows 8 + 2c + e -> token 4c + 2 + e
+    static __device__ __forceinline__ int tok_of_row(int m) {
+        return TOKPERM ? 4 * ((m & 7) >> 1) + (m & 1) + ((m >> 3) << 1) : m;
+    }
+
     static constexpr int KSTEPS = D / 16;
     static constexpr int MT = D / 16;
     static constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1
@@ -204,14 +213,14 @@ struct BlockMath {
     // arithmetic: masked K rows may hold NaN).
     __device__ __forceinline__ void mask_scores(float (&s)[NT][4], int vq, int lane) const {
         if (vq - qm1 >= kBlockSize) return;  // no column reaches into this block's end
-        const int r0 = lane >> 2;
+        const int t0 = tok_of_row(lane >> 2), t1 = tok_of_row((lane >> 2) + 8);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int lim = vq - qoff[nt][c];
-                if (r0 >= lim) s[nt][c] = -INFINITY;
-                if (r0 + 8 >= lim) s[nt][c + 2] = -INFINITY;
+                if (t0 >= lim) s[nt][c] = -INFINITY;
+                if (t1 >= lim) s[nt][c + 2] = -INFINITY;
             }
     }
 
@@ -343,9 +352,10 @@ struct BlockMath {
 //    a token; converted pairwise to f16x2 they fill the A fragment with the
 //    contraction index d permuted within each 16-column k-step -- Q's B
 //    fragment is loaded with the same permutation, so q.k is unchanged.
-//  * PV: V bytes are loaded per token row, converted to f16x2 and transposed
-//    in registers with movmatrix into V^T fragments; the output rows d come
-//    out permuted within each 16-row tile (dcol() gives the mapping).
+//  * PV: V^T fragments come straight from ldmatrix.m16n16.x2.trans.b8 (lane
+//    (g, c): tokens 4c..4c+3 of columns g, g + 8) -- the K rows of QK^T are
+//    loaded in the matching token order (tok_of_row), so P's k index lines
+//    up; no movmatrix on V, output rows d in natural order.
 // Q_BF16 only selects how q is read (bf16 q is converted to fp16).
 __device__ __forceinline__ void cvt_e4m3x4(uint32_t w, uint32_t& lo, uint32_t& hi) {
     asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
@@ -355,8 +365,8 @@ __device__ __forceinline__ void cvt_e4m3x4(uint32_t w, uint32_t& lo, uint32_t& h
 }
 
 template <bool Q_BF16, int NT>
-struct BlockMathKV8 : BlockMath<false, 128, NT> {
-    using Base = BlockMath<false, 128, NT>;
+struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
+    using Base = BlockMath<false, 128, NT, true>;
     static constexpr int D = 128;
     static constexpr int MT = D / 16;
     static constexpr int kSlab = kBlockSize * D;  // 1 byte per element
@@ -393,7 +403,8 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) s[nt][r] = s2[nt][r] = 0.f;
-        const int kr = (lane & 7) + ((lane >> 3) & 1) * 8;
+        // MMA row m = (lane & 7) + ((lane >> 3) & 1) * 8 is loaded from token tok_of_row(m)
+        const int kr = Base::tok_of_row((lane & 7) + ((lane >> 3) & 1) * 8);
 #pragma unroll
         for (int j = 0; j < D / 32; ++j) {
             const int unit = 2 * j + (lane >> 4);
@@ -412,23 +423,34 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         }
     }
 
-    // ---- S6 on e4m3 V
+    // ---- S6 on e4m3 V: V^T fragments straight from a transposing byte
+    // ldmatrix -- lane (g, c) gets tokens 4c..4c+3 of columns d = g and g + 8,
+    // which is the A fragment of O^T += V^T P for the token order
+    // tok_of_row() gave the rows of S^T (hence of P's k index); no movmatrix.
+    static __device__ __forceinline__ void mask_v8(uint32_t (&a)[4], int valid, int lane) {
+        const int t0 = 4 * (lane & 3);
+        const uint32_t m0 = (t0 < valid ? 0xffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+        const uint32_t m1 = (t0 + 2 < valid ? 0xffffu : 0u) | (t0 + 3 < valid ? 0xffff0000u : 0u);
+        a[0] &= m0;
+        a[1] &= m0;
+        a[2] &= m1;
+        a[3] &= m1;
+    }
+
     template <bool TAIL = true>
     __device__ __forceinline__ void pv8(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2]) {
-        const int vr = (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int vr = lane & 15;
 #pragma unroll
         for (int ip = 0; ip < MT / 2; ++ip) {
-            const int unit = 2 * ip + (lane >> 4);
+            const int unit = 2 * ip + (lane >> 4);  // 16 d columns per matrix: tiles 2 ip, 2 ip + 1
             uint32_t r[4];
-            ldsm_x4(vbase + vr * 128 + ((unit ^ (vr & 7)) << 4), r[0], r[1], r[2], r[3]);
+            ldsm_x2_trans_b8(vbase + vr * 128 + ((unit ^ (vr & 7)) << 4), r[0], r[1], r[2], r[3]);
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) {
-                uint32_t x0, y0, x1, y1;
-                cvt_e4m3x4(r[2 * c2], x0, y0);      // tokens 0-7
-                cvt_e4m3x4(r[2 * c2 + 1], x1, y1);  // tokens 8-15
-                uint32_t a[4] = {movmatrix_trans(x0), movmatrix_trans(y0), movmatrix_trans(x1),
-                                 movmatrix_trans(y1)};
-                if (TAIL && valid < kBlockSize) Base::mask_v(a, valid, lane);
+                uint32_t a[4];
+                cvt_e4m3x4(r[2 * c2], a[0], a[2]);      // d = g: tokens (4c, 4c+1) | (4c+2, 4c+3)
+                cvt_e4m3x4(r[2 * c2 + 1], a[1], a[3]);  // d = g + 8
+                if (TAIL && valid < kBlockSize) mask_v8(a, valid, lane);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
                     mma_16816<false>(this->acc[2 * ip + c2][nt], a, pb[nt][0], pb[nt][1]);
@@ -500,12 +522,6 @@ struct BlockMathKV8 : BlockMath<false, 128, NT> {
         pv8<TAIL>(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
     }
 
-    // Output column d held by accumulator acc[i][*][r]: rows 0-7 of a tile are
-    // the even-pair columns {0,1,4,5,8,9,12,13}, rows 8-15 the odd pairs.
-    static __device__ __forceinline__ int dcol(int i, int lane, int r) {
-        const int m = lane >> 2;
-        return i * 16 + 4 * (m >> 1) + (m & 1) + 2 * (r >> 1);
-    }
 };
 
 }  // namespace pda

@@ -157,6 +157,17 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint3
                  : "r"(addr));
 }
 
+// Two transposed 16x16 byte matrices (rows addressed by lanes 0-15 and 16-31).
+// Measured layout on sm_100a (tools/probes/ldsm_b8.cu): lane 4g + c receives
+// r0 = rows 4c..4c+3 of column g, r1 = the same rows of column g + 8 (matrix
+// 0; r2, r3 likewise from matrix 1), row 4c in the lowest byte.
+__device__ __forceinline__ void ldsm_x2_trans_b8(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                                 uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
 // Transpose an 8x8 b16 matrix held in mma fragment layout (MOVM).
 __device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
     uint32_t d;
