@@ -301,19 +301,29 @@ def main():
     if (world > 1 or check_fused_1) and not share and not args.fused_gather and not args.nccl_gather:
         # fused output all-gather when it works here: its first
         # step must equal the NCCL step bit for bit on every rank, else NCCL
+        def all_ok(ok):  # every rank agrees before anyone enters a cross-rank device barrier
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            return int(flag.item()) == 1
+
         ok = 1
         try:
             step_fused = make_step(**opt_kw, fused_gather=True)
-            ref = step_main(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
-            got = step_fused(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
-            torch.cuda.synchronize()
-            ok = int(torch.equal(ref.view(torch.int16), got.view(torch.int16)))
         except Exception as e:  # noqa: BLE001 -- any failure selects the NCCL path
             print(f"[bench rank {rank}] fused gather unavailable: {e}", file=sys.stderr)
             ok = 0
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 1:
+        if all_ok(ok):
+            try:
+                ref = step_main(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
+                got = step_fused(q, bt, lens, scale).reshape(local_cfg.num_seqs, -1, cfg.head_dim).clone()
+                torch.cuda.synchronize()
+                ok = int(torch.equal(ref.view(torch.int16), got.view(torch.int16)))
+            except Exception as e:  # noqa: BLE001
+                print(f"[bench rank {rank}] fused gather failed: {e}", file=sys.stderr)
+                ok = 0
+        else:
+            ok = 0
+        if all_ok(ok):
             step_nccl, step_main, tp_gather = step_main, step_fused, "fused"
 
     def barrier():
