@@ -209,9 +209,12 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         // split that reaches it (measured: B=4 ctx 32k 88 vs 100 us, B=16 ctx
         // 4k 49 vs 53, C2 at TP 8 94 vs 100; longer partitions prefer many
         // waves: B=16 ctx 32k 280 vs 285)
+        // ... and at least one CTA per SM: with two head tiles (2 CTAs/SM) 0.4 of
+        // the slots is fewer CTAs than SMs (g = 16, B=64 ctx 8k: 128 CTAs 135 us
+        // vs 256 CTAs 100 us; B=16 ctx 32k 141 vs 98)
         int64_t one_wave = 0;
         for (int64_t sp = 1; units0 * sp <= conc && max_tokens / sp >= 512; sp *= 2)
-            if (units0 * sp * 5 >= conc * 2 && max_tokens / sp <= 8192) {
+            if (units0 * sp * 5 >= conc * 2 && units0 * sp >= sms && max_tokens / sp <= 8192) {
                 one_wave = sp;
                 break;
             }

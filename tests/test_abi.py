@@ -305,7 +305,19 @@ def test_cluster_merge_planning():
     (1, 32768, 1024, 32, 0),  # > 8 partitions: combine kernel
 ])
 def test_planner_partitions_and_merge(B, ctx, P, p_max, cluster):
-    s = shape(num_seqs=B, num_q_heads=32, num_kv_heads=8, head_dim=128, num_blocks=100000,
+    _check_planner(B, ctx, P, p_max, cluster, 8)
+
+
+@pytest.mark.parametrize("B,ctx,P,p_max,cluster", [
+    (64, 8192, 4096, 2, 2),    # g = 16 (2 CTAs/SM): one wave of >= one CTA per SM, not 128 CTAs
+    (16, 32768, 4096, 8, 8),
+])
+def test_planner_one_wave_fills_every_sm(B, ctx, P, p_max, cluster):
+    _check_planner(B, ctx, P, p_max, cluster, 2)
+
+
+def _check_planner(B, ctx, P, p_max, cluster, hkv):
+    s = shape(num_seqs=B, num_q_heads=32, num_kv_heads=hkv, head_dim=128, num_blocks=100000,
               max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1)
     p = pda.plan(s, opts(kernel=2))
     assert (p["partition_tokens"], p["p_max"], p["cluster"]) == (P, p_max, cluster)
