@@ -64,10 +64,15 @@ constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) 
 // MODE: 0 = plain, 1 = debug trace (+ runtime cluster support), 2 = launched
 // as clusters (merge over DSMEM).  The plain instantiation carries no cluster
 // code at all (it cost 4 registers and 1-2 us on small steps).
-// e4m3 with a 12-stage ring: blocks one at a time (no pairs), 4 CTAs per SM
-// (16 warps, 4 x 48 KiB in flight) instead of 3 x 16 stages consumed in pairs.
+// CTAs per SM the register budget is built for: 3 (<= 170 registers; the
+// two-tile 16-bit kernel fits in 166 without spills); e4m3 with a 12-stage
+// ring: blocks one at a time (no pairs), 4 CTAs per SM (16 warps, 4 x 48 KiB
+// in flight) instead of 3 x 16 stages consumed in pairs; two-tile e4m3: 2
+// (it would spill at 3).
 template <bool KV8, int STAGES, int NT>
-constexpr int splitk_min_blocks() { return (KV8 && STAGES == 12 && NT == 1) ? 4 : (NT == 1 ? 3 : 2); }
+constexpr int splitk_min_blocks() {
+    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 2) : 3;
+}
 
 template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF>
 __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_blocks<KV8, STAGES, NT>())
