@@ -94,9 +94,10 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 }
 
 // Resident split-K CTAs per SM (matches splitk_min_blocks in splitk_impl.cuh):
-// 3, except the two-tile e4m3 kernel (2).
-int splitk_ctas_per_sm(const pda_shape* s, int n_tiles) {
-    return (s->kv_dtype == PDA_E4M3 && n_tiles > 1) ? 2 : 3;
+// 3, except the two-tile e4m3 and two-tile producer-warp kernels (2).
+bool self_issue(const pda_shape* s, const pda_options* o);
+int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
+    return (n_tiles > 1 && (s->kv_dtype == PDA_E4M3 || !self_issue(s, o))) ? 2 : 3;
 }
 
 pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
@@ -203,7 +204,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         P = o->partition_tokens;
     } else {
         const int64_t units0 = (int64_t)B * Hkv;
-        const int64_t conc = (int64_t)sms * splitk_ctas_per_sm(s, n_tiles);
+        const int64_t conc = (int64_t)sms * splitk_ctas_per_sm(s, o, n_tiles);
         int64_t split = 1;
         // partitions of >= 512 tokens; once the grid has >= 256 units, >= 1024
         // (measured: e.g. B=1, ctx 32k: 256 x 1024 tokens 43 us vs 512 x 512 55 us);
@@ -263,7 +264,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // partner (B=16-64, ctx 4k: 14-15 % slower) -- DESIGN.md 7.
     if (p_max > 1 && o->merge != 1) {
         if (o->merge == 2 && p_max > kMaxCluster) return PDA_ERR_UNSUPPORTED;
-        const int64_t conc = (int64_t)sms * splitk_ctas_per_sm(s, n_tiles);
+        const int64_t conc = (int64_t)sms * splitk_ctas_per_sm(s, o, n_tiles);
         const bool one_wave = (int64_t)B * Hkv * p_max <= conc;
         if (o->merge == 2 || (p_max <= kAutoMaxCluster && one_wave)) pl->cluster = (int32_t)p_max;
     }

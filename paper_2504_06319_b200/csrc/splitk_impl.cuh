@@ -71,13 +71,16 @@ constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) 
 // ring: blocks one at a time (no pairs), 4 CTAs per SM (16 warps, 4 x 48 KiB
 // in flight) instead of 3 x 16 stages consumed in pairs; two-tile e4m3: 2
 // (it would spill at 3).
-template <bool KV8, int STAGES, int NT>
+// The producer-warp form (160 threads) keeps 2 CTAs/SM for two tiles (it
+// would spill at 3).
+template <bool KV8, int STAGES, int NT, bool SELF>
 constexpr int splitk_min_blocks() {
-    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 2) : (NT == 1 && STAGES == 4 ? 4 : 3);
+    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 2)
+               : (NT == 1 ? (STAGES == 4 && SELF ? 4 : 3) : (SELF ? 3 : 2));
 }
 
 template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF>
-__global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_blocks<KV8, STAGES, NT>())
+__global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_blocks<KV8, STAGES, NT, SELF>())
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
     constexpr bool TRACE = MODE == 1;

@@ -366,3 +366,18 @@ def test_header_is_c99_and_c_example_links(tmp_path):
                         "-fsyntax-only", str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert _build_c_example(tmp_path).exists()
+
+
+def test_default_split_k_kernels_do_not_spill():
+    """The occupancy each split-K instantiation is built for (its
+    __launch_bounds__ minimum CTAs/SM, which the planner assumes) must not
+    cost spills in the self-issue kernels the library runs by default
+    (ptxas -v report of the plain-MODE translation unit)."""
+    import re
+    rep = os.path.join(os.path.dirname(_lib.LIB_PATH), "_build", "decode_splitk_m0.o.ptxas.txt")
+    text = open(rep).read()
+    blocks = re.findall(r"Function properties for (\S+)\n\s+(\d+) bytes stack frame, (\d+) bytes spill stores", text)
+    self_issue = [(n, int(sp)) for n, _, sp in blocks if "splitk_kernel" in n and n.endswith("ELb1EEEv14CUtensorMap_stS2_NS_12SplitKParamsE")]
+    assert len(self_issue) >= 20, "expected every self-issue instantiation in the ptxas report"
+    spilled = [n for n, sp in self_issue if sp]
+    assert not spilled, spilled
