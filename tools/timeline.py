@@ -87,6 +87,15 @@ def main():
     ideal = total / body_rate if body_rate > 0 else T
     life = (e - s)[work]
     rate = (b[work] / (e - s)[work]) / 1e3  # GB/s per CTA
+    # per-SM load: CTAs sharing an SM (any overlap in time) vs the rate each streamed
+    sm = st[live, 2][work].tolist()
+    from collections import Counter, defaultdict
+    per_sm = Counter(sm)
+    by_load = defaultdict(list)
+    for smi, r in zip(sm, rate.tolist()):
+        by_load[per_sm[smi]].append(r)
+    sm_rates = {f"{k}_ctas_per_sm": dict(n_ctas=len(v), gbs_per_cta=round(statistics.median(v), 2))
+                for k, v in sorted(by_load.items())}
     line = dict(cell=cfg.name + ("_kv8" if kv8 else ""), **{k: v for k, v in kw.items() if not k.endswith("scale")},
                 plan=dict(p_max=info["p_max"], partition_tokens=info["partition_tokens"], cluster=info["cluster"],
                           grid=[info["grid_x"], info["grid_y"], info["grid_z"]]),
@@ -99,7 +108,7 @@ def main():
                                  p90=round(float(life.quantile(0.9)), 1)),
                 cta_gbs=dict(p10=round(float(rate.quantile(0.1)), 2), p50=round(float(rate.median()), 2),
                              p90=round(float(rate.quantile(0.9)), 2)),
-                sms_used=int(st[live, 2].unique().numel()),
+                sms_used=int(st[live, 2].unique().numel()), per_sm_load=sm_rates,
                 residency_1us=[round(float(x), 1) for x in res[:: max(1, nb // 40)]],
                 gbs_1us=[round(float(x) / 1e3) for x in bw[:: max(1, nb // 40)]])
     print(json.dumps(line))
