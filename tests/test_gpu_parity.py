@@ -876,3 +876,25 @@ def test_c_example_runs(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 of 512 outputs off the closed form" in r.stdout
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (28, 4)])
+def test_kernel_gqa_mapping_spec_examples(pda, hq, hkv):
+    """SPEC's kv_head_for_q_head examples on the kernel: with V = 1
+    only in kv head k, exactly the q heads floor(h / (Hq/Hkv)) == k read 1,
+    every other row is exactly 0 -- for each k, default plan and P = 16."""
+    cfg = synth.Config("spec_gqa_gpu", 2, hq, hkv, 128, (20, 300), "bf16", poison_blocks=1)
+    dev = to_dev(synth.make_inputs(cfg, seed=3))
+    g = hq // hkv
+    for k in range(hkv):
+        v = torch.zeros_like(dev["v_cache"])
+        v[:, k] = 1.0
+        for kw in (dict(), dict(partition_tokens=16)):
+            out = pda.paged_decode_attention(dev["q"], dev["k_cache"], v, dev["block_tables"],
+                                             dev["context_lens"], dev["scale"], out_dtype=torch.float32, **kw)
+            for h in range(hq):
+                row = out[:, h].cpu()
+                if h // g == k:
+                    assert (row - 1.0).abs().max().item() <= 2e-3, (k, h)
+                else:
+                    assert torch.count_nonzero(row).item() == 0, (k, h)

@@ -643,3 +643,51 @@ def test_property_append_then_attend(oracle_mod, lens, q_len, seed):
                 s = inp["scale"] * (K @ inp["q"][b, i, h].double().numpy())
                 w = np.exp(s - s.max())
                 np.testing.assert_allclose(out[b, i, h], (w / w.sum()) @ V, rtol=0, atol=1e-12)
+
+
+# ---- SPEC's worked examples (tests/golden/spec_examples.txt), checked through
+# the oracle's own computations, not through a re-typed formula ----
+
+def _spec_examples(kind):
+    path = os.path.join(os.path.dirname(__file__), "golden", "spec_examples.txt")
+    out = []
+    for line in open(path):
+        line = line.split("#")[0].strip()
+        if line.startswith(kind + " "):
+            lhs, rhs = line[len(kind):].split("->")
+            out.append((tuple(int(x) for x in lhs.split()), int(rhs)))
+    assert out, kind
+    return out
+
+
+def test_spec_blocks_per_sequence(oracle_mod):
+    """the number of blocks the oracle's plan visits for a
+    sequence of L tokens in 16-token blocks (one partition covering it)."""
+    for (L, bs), want in _spec_examples("blocks_per_sequence"):
+        bt = np.arange(256, dtype=np.int32)[None, :]
+        recs = oracle_mod.plan_splitk(bt, np.array([L], dtype=np.int32), num_kv_heads=1, block_size=bs,
+                                      partition_tokens=4096, p_max=1, prefetch_distance=0)
+        assert recs[0, 0, 0, 2] == want, (L, bs)
+        assert list(recs[0, 0, 0, 4:4 + want]) == list(range(want))
+
+
+def test_spec_kv_head_for_q_head(oracle_mod):
+    """q head h reads kv head floor(h / (Hq / Hkv)).  Only kv head k
+    carries V = 1 (all others 0), so the oracle's output row of q head h is 1
+    (to rounding) iff h reads kv head k, else exactly 0 -- and every kv head serves exactly Hq/Hkv
+    q heads (the exhaustive check S:159 asks for)."""
+    for (qh, hq, hkv), kvh in _spec_examples("kv_head_for_q_head"):
+        cfg = synth.Config("spec_gqa", 1, hq, hkv, 64, (20,), "fp16", poison_blocks=0)
+        inp = synth.make_inputs(cfg, seed=3, poison=False)
+        readers = {}
+        for k in range(hkv):
+            v = torch.zeros_like(inp["v_cache"])
+            v[:, k] = 1.0
+            out = oracle_mod.paged_attention(inp["q"], inp["k_cache"], v, inp["block_tables"],
+                                             inp["context_lens"], inp["scale"], "fp16")
+            ones = [h for h in range(hq) if np.all(np.abs(out[0, h] - 1.0) <= 1e-12)]  # sum w_t / Z = 1
+            zeros = [h for h in range(hq) if np.all(out[0, h] == 0.0)]
+            assert sorted(ones + zeros) == list(range(hq))
+            readers[k] = ones
+        assert qh in readers[kvh]
+        assert all(len(r) == hq // hkv for r in readers.values())
