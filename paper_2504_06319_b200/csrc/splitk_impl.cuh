@@ -75,7 +75,7 @@ constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) 
 // would spill at 3).
 template <bool KV8, int STAGES, int NT, bool SELF>
 constexpr int splitk_min_blocks() {
-    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 2)
+    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 3)
                : (NT == 1 ? (STAGES == 4 && SELF ? 4 : 3) : (SELF ? 3 : 2));
 }
 

