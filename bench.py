@@ -582,6 +582,11 @@ def main():
                 if pl["kernel"] == 2 and pl["p_max"] > 1 else ""),
             "launch_us": attn_ms * 1e3, "algorithmic_bytes_per_launch": local_bytes,
             "peak_source": peak_src,
+            # the copy peak counts read + write traffic of a copy; a read-only stream runs
+            # faster, so frac > 1 is possible -- context against the spec and the in-run probe:
+            "frac_of_spec_8000_gbs": achieved / 8000.0,
+            "frac_of_read_probe": (achieved / extras["read_roofline_gbs"]) if "read_roofline_gbs" in extras
+            else None,
         },
         "gpu_launches": args.steps * step_main.launches_per_step(),
         "clocks": clk.summary(),
