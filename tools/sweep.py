@@ -45,7 +45,8 @@ def variants(quick):
     # 16-bit split-K with the producer-warp refill (the alternative to self-issue)
     vs.append(dict(kernel="splitk", smem_stages=8, prefetch="off", issue_mode="producer"))
     vs.append(dict(kernel="splitk", smem_stages=8, prefetch="line", prefetch_distance=4, issue_mode="producer"))
-    # e4m3 KV cache (NEXT f3)
+    # e4m3 KV cache (NEXT f3): library default ring (12 single / 16 paired by size), then fixed depths
+    vs.append(dict(kernel="splitk", prefetch="off", kv="e4m3"))
     for st in (8, 16):
         vs.append(dict(kernel="splitk", smem_stages=st, prefetch="off", kv="e4m3"))
         vs.append(dict(kernel="splitk", smem_stages=st, prefetch="line", prefetch_distance=4, kv="e4m3"))
