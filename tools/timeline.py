@@ -87,14 +87,15 @@ def main():
     ideal = total / body_rate if body_rate > 0 else T
     life = (e - s)[work]
     rate = (b[work] / (e - s)[work]) / 1e3  # GB/s per CTA
-    # per-SM load: CTAs sharing an SM (any overlap in time) vs the rate each streamed
+    # per-SM load: how many CTAs ran on the SM over the whole kernel (= CTAs sharing it in a
+    # one-wave grid) vs the rate each streamed
     sm = st[live, 2][work].tolist()
     from collections import Counter, defaultdict
     per_sm = Counter(sm)
     by_load = defaultdict(list)
     for smi, r in zip(sm, rate.tolist()):
         by_load[per_sm[smi]].append(r)
-    sm_rates = {f"{k}_ctas_per_sm": dict(n_ctas=len(v), gbs_per_cta=round(statistics.median(v), 2))
+    sm_rates = {f"{k}_ctas_on_sm": dict(n_ctas=len(v), gbs_per_cta=round(statistics.median(v), 2))
                 for k, v in sorted(by_load.items())}
     line = dict(cell=cfg.name + ("_kv8" if kv8 else ""), **{k: v for k, v in kw.items() if not k.endswith("scale")},
                 plan=dict(p_max=info["p_max"], partition_tokens=info["partition_tokens"], cluster=info["cluster"],
