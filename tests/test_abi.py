@@ -384,3 +384,40 @@ def test_default_split_k_kernels_do_not_spill():
     kv8_two_tile = re.compile(r"ELi128ELi2ELi\d+ELi0ELb1ELb1E")
     spilled = [n for n, sp in self_issue if sp and not (kv8_two_tile.search(n) and sp <= 64)]
     assert not spilled, spilled
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=300, deadline=None)
+@given(B=st.integers(1, 1024), g=st.sampled_from([1, 2, 4, 5, 7, 8, 16]), hkv=st.sampled_from([1, 2, 4, 8, 32]),
+       D=st.sampled_from([64, 128]), max_blocks=st.integers(1, 4096), q_len=st.integers(1, 4),
+       kv8=st.booleans(), dt=st.sampled_from([0, 1]))
+def test_planner_invariants(B, g, hkv, D, max_blocks, q_len, kv8, dt):
+    """Any valid shape: the split-K plan covers every token exactly once with
+    whole blocks, its grid matches (P_max, Hkv, B), the ring depth is one the
+    kernels instantiate, clusters only merge what fits, the workspace is the
+    documented partial size, and the planner is deterministic."""
+    if kv8 and D != 128:
+        return
+    if q_len * g > 16:
+        q_len = max(1, 16 // g)
+    s = shape(num_seqs=B, num_q_heads=g * hkv, num_kv_heads=hkv, head_dim=D, num_blocks=max_blocks + 1,
+              max_blocks_per_seq=max_blocks, dtype=dt, out_dtype=dt, kv_dtype=3 if kv8 else dt, q_len=q_len)
+    p = pda.plan(s, opts(kernel=2, prefetch=0))
+    assert p == pda.plan(s, opts(kernel=2, prefetch=0))
+    max_tokens = max_blocks * 16
+    P, pm = p["partition_tokens"], p["p_max"]
+    assert P % 16 == 0 and P > 0
+    assert pm == -(-max_tokens // P) and (pm - 1) * P < max_tokens <= pm * P
+    assert (p["grid_x"], p["grid_y"], p["grid_z"]) == (pm, hkv, B)
+    assert p["smem_stages"] in ((8, 12, 16, 24) if kv8 else (4, 8, 12))
+    if p["cluster"]:
+        assert p["cluster"] == pm and 1 < pm <= 8 and p["workspace_bytes"] == 0
+    if pm > 1 and not p["cluster"]:
+        rows = B * q_len * g * hkv
+        al = lambda x: (x + 255) // 256 * 256
+        assert p["workspace_bytes"] == al(rows * pm * D * 4) + al(rows * pm * 4)
+    if pm == 1:
+        assert p["workspace_bytes"] == 0
+    assert p["trace_records"] == B * hkv * pm and p["trace_rec_len"] == 4 + 2 * (P // 16)
