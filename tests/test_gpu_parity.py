@@ -898,3 +898,61 @@ def test_kernel_gqa_mapping_spec_examples(pda, hq, hkv):
                     assert (row - 1.0).abs().max().item() <= 2e-3, (k, h)
                 else:
                     assert torch.count_nonzero(row).item() == 0, (k, h)
+
+
+def _fuzz_cases(n=96, seed=2025):
+    import random
+    rng = random.Random(seed)
+    cases = []
+    for i in range(n):
+        kv8_case = i % 4 == 3
+        D = 128 if kv8_case else rng.choice([64, 128])
+        g = rng.choice([1, 2, 4, 7, 8, 16])
+        hkv = rng.choice([1, 2, 4])
+        q_len = 1 if kv8_case else rng.choice([1, 1, 2, 3, 4])
+        q_len = max(1, min(q_len, 16 // g))
+        B = rng.randint(1, 6)
+        lens = tuple(rng.choice([0, 1, 15, 16, 17, rng.randint(2, 700)]) for _ in range(B))
+        if max(lens) < q_len:
+            lens = (q_len,) + lens[1:]
+        lens = tuple(max(L, q_len) if L else 0 for L in lens)  # a row with tokens holds its q_len new ones
+        stages = rng.choice([0, 8, 12, 16, 24] if kv8_case else [0, 4, 8, 12])
+        P = rng.choice([0, 16, 48, 128, 512])
+        merge = rng.choice(["auto", "combine", "cluster"])
+        dt = rng.choice(["fp16", "bf16"])
+        cases.append((i, kv8_case, D, g, hkv, q_len, lens, stages, P, merge, dt))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"fuzz{c[0]}")
+def test_fuzz_parity_vs_oracle(pda, oracle_mod, case):
+    """Seeded random shapes / lengths / ring depths / partition sizes / merge
+    modes (incl. the 4-CTA, two-tile and e4m3 occupancy variants) vs the
+    oracle; every planner-valid combination must match within 2e-3."""
+    i, kv8_case, D, g, hkv, q_len, lens, stages, P, merge, dt = case
+    cfg = synth.Config(f"fuzz{i}", len(lens), g * hkv, hkv, D, lens, dt, poison_blocks=2)
+    inp = synth.make_inputs(cfg, seed=100 + i)
+    kw = dict(smem_stages=stages, partition_tokens=P)
+    if kv8_case:
+        inp = kv8(inp)
+        ref = oracle_kv8(oracle_mod, inp)
+    else:
+        inp = synth.with_query_tokens(inp, q_len, seed=i) if q_len > 1 else inp
+        q4 = inp["q"] if q_len > 1 else inp["q"][:, None]
+        ref = oracle_mod.paged_attention_mq(q4, inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                            inp["context_lens"], inp["scale"], dt)
+        if q_len == 1:
+            ref = ref[:, 0]
+    dev = to_dev(inp)
+    if kv8_case:
+        dev.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
+    # the plan this shape gets; cluster merge only where P_max fits a cluster
+    s = pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"])
+    info = pda.plan(s, pda.make_options(smem_stages=stages, partition_tokens=P, kernel="splitk",
+                                        k_scale=inp.get("k_scale", 0.0), v_scale=inp.get("v_scale", 0.0)))
+    if merge == "cluster" and info["p_max"] > 8:
+        merge = "auto"
+    kw["merge"] = merge
+    out = gpu_kv8(pda, dev, **kw) if kv8_case else gpu(pda, dev, **kw)
+    assert out.shape == tuple(ref.shape)
+    assert max_err(out, ref) <= TOL, kw
