@@ -16,6 +16,10 @@
  *    owned by the caller; the library never allocates, frees or synchronises
  *    them.  Work is enqueued on `stream` (a cudaStream_t passed as void*;
  *    NULL = legacy default stream).  Calls are stateless and thread-safe.
+ *  - The split-K kernels are launched with programmatic stream serialization
+ *    (PDL): they may be scheduled while the previous grid in the stream
+ *    drains and wait for its completion before their first global read, so
+ *    stream order semantics are unchanged.  Environment PDA_PDL=0 disables it.
  *  - Host-side argument errors are returned synchronously before any launch;
  *    launch failures map to PDA_ERR_CUDA.  No C++ exception crosses the ABI.
  *  - Device-resident values (block ids, lengths) are not validated: a block

@@ -35,6 +35,7 @@ namespace {
 template <int D>
 __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
     constexpr int PER = D / 32;
+    pdl_wait();  // the partials come from the split-K grid before this one
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= p.B * p.q_len * p.Hq) return;
@@ -117,6 +118,19 @@ cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t st
     // (a programmatic-dependent-launch variant measured neutral to -2 %)
     const int rows = p.B * p.q_len * p.Hq;
     const dim3 grid((rows + 3) / 4);
+    if (p.pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(128, 1, 1);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return head_dim == 64 ? cudaLaunchKernelEx(&cfg, combine_kernel<64>, p)
+                              : cudaLaunchKernelEx(&cfg, combine_kernel<128>, p);
+    }
     if (head_dim == 64)
         combine_kernel<64><<<grid, 128, 0, stream>>>(p);
     else

@@ -78,6 +78,7 @@ struct SplitKParams {
     AppendParams app;  // fused KV append (app.k_new == nullptr: none)
     int cluster;       // > 1: launched as clusters of P_max CTAs (one per partition of a
                        // (seq, kv head) row) that merge their partials through DSMEM
+    int pdl;           // launched with programmatic stream serialization (PDL)
 };
 
 struct PaperParams {
@@ -136,6 +137,7 @@ struct BalancedParams {
 };
 
 struct CombineParams {
+    int pdl;  // launched with programmatic stream serialization (PDL)
     const float* ws_o;
     const float* ws_lse;
     const int32_t* lens;

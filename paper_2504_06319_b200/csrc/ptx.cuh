@@ -265,4 +265,11 @@ __device__ __forceinline__ uint32_t sm_id() {
     return s;
 }
 
+// Programmatic dependent launch: wait until the grids this one depends on
+// have completed (their memory visible); let the next grid in the stream be
+// scheduled once every CTA of this one has signalled (or exited).  Both are
+// no-ops for a grid launched without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 }  // namespace pda

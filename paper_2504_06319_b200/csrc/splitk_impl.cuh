@@ -112,6 +112,9 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
     const int lane = threadIdx.x & 31;
     const int g = p.g;
 
+    // PDL: everything this grid reads may come from the previous grid in the
+    // stream (q, the tables, the appended KV): wait before the first load
+    pdl_wait();
     const int max_tokens = p.max_blocks * kBlockSize;
     int L = p.lens[b];
     L = L < max_tokens ? L : max_tokens;
@@ -423,6 +426,9 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
             rec[1] = e_tok;
         }
     }
+    // the main loop is done: the next grid may start its prologue (it waits for
+    // this grid's completion before reading anything)
+    pdl_launch_dependents();
     // ---- S7: merge the consumer warps of this unit
     bm.reduce_l();
     const int r0 = lane >> 2;
@@ -497,24 +503,33 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
     constexpr size_t smem = smem_bytes_for<D, NT, STAGES, KV8>();
     static std::atomic<uint64_t> smem_set{0};
     if (cudaError_t e = ensure_smem_limit(kern, smem, smem_set); e != cudaSuccess) return e;
-    if (p.cluster > 1) {
-        // one cluster per (seq, kv head) row: its P_max partition CTAs (grid.x == P_max)
-        if (p.cluster > 8) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
-        }
+    if (p.cluster > 8) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    if (p.cluster > 1 || p.pdl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(splitk_block_threads<SELF>(), 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = (unsigned)p.cluster;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+        cudaLaunchAttribute attr[2];
+        int na = 0;
+        if (p.cluster > 1) {
+            // one cluster per (seq, kv head) row: its P_max partition CTAs (grid.x == P_max)
+            attr[na].id = cudaLaunchAttributeClusterDimension;
+            attr[na].val.clusterDim.x = (unsigned)p.cluster;
+            attr[na].val.clusterDim.y = 1;
+            attr[na].val.clusterDim.z = 1;
+            ++na;
+        }
+        if (p.pdl) {
+            attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[na].val.programmaticStreamSerializationAllowed = 1;
+            ++na;
+        }
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = na;
         return cudaLaunchKernelEx(&cfg, kern, tmK, tmV, p);
     }
     kern<<<grid, splitk_block_threads<SELF>(), smem, stream>>>(tmK, tmV, p);
