@@ -96,7 +96,6 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 
 // Resident split-K CTAs per SM (matches splitk_min_blocks in splitk_impl.cuh):
 // 3, except the two-tile producer-warp kernels (2).
-bool self_issue(const pda_shape* s, const pda_options* o);
 int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
     return (n_tiles > 1 && s->kv_dtype != PDA_E4M3 && !self_issue(s, o)) ? 2 : 3;
 }
