@@ -518,21 +518,41 @@ def main():
 
     # end to end through the public C-ABI host entry (pinned host q/bt/lens in, out back)
     e2e = None
-    if not args.no_extras:
+    if not args.no_extras and world == 1:
         host = pda.HostDecodeStep(inp["k_cache"], inp["v_cache"], local_cfg.num_seqs,
                                   local_cfg.num_q_heads, local_cfg.max_blocks_per_seq, dt, slots=2, **opt_kw)
         qh, bth, lh = q.cpu().pin_memory(), bt.cpu().pin_memory(), lens.cpu().pin_memory()
 
         def e2e_step(*_):
             host(qh, bth, lh, scale)
-            if world > 1:
-                pass  # the gathered output of the TP step is measured on the device path
         e2e_ms = time_steps(e2e_step, max(10, args.steps // 2), 2, join=host.join)
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": host.h2d_bytes() * world,
-               "d2h_bytes_per_step": host.d2h_bytes() * world,
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": host.h2d_bytes(),
+               "d2h_bytes_per_step": host.d2h_bytes(),
                "path": "pda_decode_step_host (H2D q/bt/lens from pinned memory, kernels, D2H out), "
                        "2 staging slots, copies on per-slot copy streams overlapping the previous step's kernels; kernels in order on one stream"}
+    elif not args.no_extras:
+        # N > 1: the TP step end to end -- this rank's q slice, the tables and the
+        # lengths from pinned host memory, the kernels, the output all-gather
+        # (the step's collective), and the gathered [B, Hq, D] output back to the host
+        qh, bth, lh = q.cpu().pin_memory(), bt.cpu().pin_memory(), lens.cpu().pin_memory()
+        qd, btd, ld = torch.empty_like(q), torch.empty_like(bt), torch.empty_like(lens)
+        out_h = torch.empty((cfg.num_seqs, cfg.num_q_heads, cfg.head_dim), dtype=dt).pin_memory()
+
+        def e2e_step(*_):
+            qd.copy_(qh, non_blocking=True)
+            btd.copy_(bth, non_blocking=True)
+            ld.copy_(lh, non_blocking=True)
+            g = step_main(qd, btd, ld, scale)
+            out_h.copy_(g.reshape(out_h.shape), non_blocking=True)
+        e2e_ms = time_steps(e2e_step, max(10, args.steps // 2), 2)
+        h2d = (qh.numel() * qh.element_size() + bth.numel() * 4 + lh.numel() * 4) * world
+        e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": out_h.numel() * out_h.element_size() * world,
+               "path": f"TPDecodeAttention per rank: H2D of the rank's q slice / tables / lengths from pinned "
+                       f"memory, the kernels, the {tp_gather} output all-gather, D2H of the gathered output "
+                       f"(every rank), one stream; max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:

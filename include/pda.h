@@ -18,8 +18,15 @@
  *    NULL = legacy default stream).  Calls are stateless and thread-safe.
  *  - The split-K kernels are launched with programmatic stream serialization
  *    (PDL): they may be scheduled while the previous grid in the stream
- *    drains and wait for its completion before their first global read, so
- *    stream order semantics are unchanged.  Environment PDA_PDL=0 disables it.
+ *    drains and wait for its completion before their first global read.
+ *    The split-K grid releases its dependents (griddepcontrol.launch_dependents)
+ *    after its main loop, BEFORE its epilogue stores `out`, the workspace and
+ *    peer buffers.  For ordinary launches (and for any kernel launched without
+ *    the programmatic-serialization attribute) stream order is unchanged; a
+ *    caller's own kernel launched WITH that attribute right after this call
+ *    may start early and must execute griddepcontrol.wait /
+ *    cudaGridDependencySynchronize() before reading this call's outputs.
+ *    Environment PDA_PDL=0 disables PDL.
  *  - Host-side argument errors are returned synchronously before any launch;
  *    launch failures map to PDA_ERR_CUDA.  No C++ exception crosses the ABI.
  *  - Device-resident values (block ids, lengths) are not validated: a block
@@ -255,9 +262,18 @@ pda_status paged_decode_attention_timeline(const void* q, const void* k_cache, c
  *   head_offset    first global q head of this rank's shard (its Hq heads land
  *                  at [head_offset, head_offset + Hq) of every buffer)
  * Other arguments as paged_decode_attention; split-K kernel only.  Completion
- * is ordered on `stream`; before any rank reads its buffer the group must pass
- * a cross-device barrier after every rank's call (e.g. the symmetric-memory
- * barrier), which is the caller's responsibility. */
+ * is ordered on `stream`.  Two cross-rank hazards are the caller's to order:
+ *   read-after-write  before any rank reads its buffer, the group must pass a
+ *                     cross-device barrier after every rank's call (e.g. the
+ *                     symmetric-memory barrier);
+ *   write-after-read  a rank's call writes into its PEERS' buffers, so no rank
+ *                     may start the call that overwrites a buffer while a peer
+ *                     still reads that buffer's previous contents.  Either
+ *                     alternate two buffer sets between consecutive steps (step
+ *                     k writes set k % 2; the barrier ending step k+1 then
+ *                     orders every peer's reads of step k before anyone's step
+ *                     k+2 writes -- what TPDecodeAttention does), or pass a
+ *                     second barrier before the call. */
 pda_status paged_decode_attention_gather(const void* q, const void* k_cache, const void* v_cache,
                                          const int32_t* block_tables, const int32_t* context_lens,
                                          float scale, void* const* out_peers, int32_t n_peers,

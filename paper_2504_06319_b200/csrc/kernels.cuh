@@ -151,7 +151,6 @@ struct CombineParams {
 cudaError_t launch_splitk(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, bool trace,
                           dim3 grid, cudaStream_t stream, bool kv8 = false, bool self_issue = false);
-size_t splitk_smem_bytes(int head_dim, int n_tiles, int stages, bool kv8 = false);
 // per-MODE instantiation sets (decode_splitk_m{0,1,2}.cu): plain, debug trace, cluster-launched
 #define PDA_SPLITK_MODE_DECL(M)                                                                          \
     cudaError_t launch_splitk_m##M(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p, \

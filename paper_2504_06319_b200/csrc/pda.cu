@@ -94,8 +94,14 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
     return o->issue_mode != 1;
 }
 
-// Resident split-K CTAs per SM (matches splitk_min_blocks in splitk_impl.cuh):
-// 3, except the two-tile producer-warp kernels (2).
+// Resident split-K CTAs per SM that the planner assumes when it chooses the
+// split: 3 (the default-depth rings), 2 for the two-tile producer-warp kernels.
+// The split is chosen BEFORE the ring depth, so the two instantiations built
+// for 4 CTAs/SM (16-bit 4-stage, e4m3 12-stage; splitk_min_blocks in
+// splitk_impl.cuh) are planned as 3/SM too: a grid of 445-592 units counts as
+// multi-wave (combine kernel, not a cluster merge) although it would fit one
+// wave at 4/SM.  The split sizes and thresholds below were measured with this
+// convention.
 int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
     return (n_tiles > 1 && s->kv_dtype != PDA_E4M3 && !self_issue(s, o)) ? 2 : 3;
 }

@@ -50,6 +50,11 @@ class TPDecodeAttention:
     (all_gather_into_tensor, default), or, with fused_gather=True, inside the
     kernel's own stores into every rank's symmetric-memory output buffer
     followed by one symmetric-memory barrier.
+
+    The returned [B, N, Hq/N, D] view aliases an internal buffer: with the NCCL
+    gather it is valid until the next call, with the fused gather (two
+    alternating buffers) until the call after next; reads must be enqueued on
+    the calling stream (or finished) before then.
     """
 
     def __init__(self, k_cache, v_cache, num_seqs, num_q_heads_local, max_blocks, dtype, group=None,
@@ -77,12 +82,19 @@ class TPDecodeAttention:
                                             **{k: v for k, v in opts.items() if k in _lib.OPTION_KEYS})
         self.hq_local = num_q_heads_local
         if self.fused:
+            # Two symmetric output buffers, alternated step by step: this rank's
+            # kernel stores into its PEERS' buffers, so reusing one buffer would
+            # let a fast rank's step k+1 overwrite step k's output while a slower
+            # peer still reads it (write-after-read).  With step k in set k % 2,
+            # the barrier that ends step k+1 orders every rank's stream-ordered
+            # reads of step k before any rank's step k+2 stores (include/pda.h).
             import torch.distributed._symmetric_memory as symm_mem
             hq = num_q_heads_local * self.world
-            self.out_full = symm_mem.empty((num_seqs, hq, D), dtype=dtype, device=dev)
             grp = group if group is not None else dist.group.WORLD
-            self.symm = symm_mem.rendezvous(self.out_full, grp)
-            self.peer_ptrs = list(self.symm.buffer_ptrs)
+            self.out_full = [symm_mem.empty((num_seqs, hq, D), dtype=dtype, device=dev) for _ in range(2)]
+            self.symm = [symm_mem.rendezvous(buf, grp) for buf in self.out_full]
+            self.peer_ptrs = [list(h.buffer_ptrs) for h in self.symm]
+            self.step_index = 0
 
     def launches_per_step(self) -> int:
         # split-K launches its combine kernel when sequences are split and the
@@ -91,11 +103,14 @@ class TPDecodeAttention:
 
     def __call__(self, q_local, block_tables, context_lens, scale):
         if self.fused:
+            k = self.step_index & 1
+            self.step_index += 1
             _lib.paged_decode_attention_gather(q_local, self.k, self.v, block_tables, context_lens, scale,
-                                               self.peer_ptrs, self.rank * self.hq_local,
+                                               self.peer_ptrs[k], self.rank * self.hq_local,
                                                self.hq_local * self.world, workspace=self.ws, **self.opts)
-            self.symm.barrier(channel=0)  # every rank's stores have landed everywhere
-            return self.out_full.view(self.out_full.shape[0], 1, *self.out_full.shape[1:])
+            self.symm[k].barrier(channel=0)  # every rank's stores have landed everywhere
+            out = self.out_full[k]
+            return out.view(out.shape[0], 1, *out.shape[1:])
         self.prepared(q_local, self.k, self.v, block_tables, context_lens, scale, out=self.out_local)
         if self.world == 1:
             return self.out_local.unsqueeze(1)

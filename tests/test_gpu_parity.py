@@ -322,75 +322,10 @@ def test_nan_poison_never_leaks(pda):
         assert torch.isfinite(gpu(pda, dev, **kw)).all()
 
 
-@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
-def test_full_size_sampled_stream(pda, oracle_mod, cfg):
-    B = cfg.num_seqs
-    sampled_check(pda, oracle_mod, cfg, [0, B // 3, B - 1], kernel="stream")
-    sampled_check(pda, oracle_mod, cfg, [1, B // 2, B - 2], kernel="splitk")
-
-
 def test_rejects_cpu_tensors(pda):
     inp = synth.make_inputs(synth.C1_TINY, seed=0)
     with pytest.raises(ValueError):
         gpu(pda, inp)
-
-
-# ---- full BASELINE sizes, in bench.py's launch configuration, sampled rows ----
-
-def sampled_check(pda, oracle_mod, cfg, seqs, **kw):
-    inp = synth.make_inputs(cfg, seed=0, device="cuda")
-    out = gpu(pda, inp, **kw)
-    torch.cuda.synchronize()
-    sub = synth.sample_rows(inp, seqs)
-    ref = oracle_out(oracle_mod, sub)
-    got = out[list(seqs)]
-    assert max_err(got, ref) <= TOL
-    assert torch.isfinite(out).all()
-    del inp, out
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
-def test_full_size_sampled(pda, oracle_mod, cfg):
-    B = cfg.num_seqs
-    sampled_check(pda, oracle_mod, cfg, [0, B // 2, B - 1])
-    sampled_check(pda, oracle_mod, cfg, [1, B - 2], prefetch="off")
-
-
-@pytest.mark.parametrize("batch,ctx", [(64, 512), (128, 512), (64, 1024)])
-def test_sweep_cell_four_ctas_per_sm_sampled(pda, oracle_mod, batch, ctx):
-    """Sweep cells where the planner picks 4-stage rings at 4 CTAs/SM (DESIGN 6)."""
-    cfg = synth.sweep_cell(batch, ctx, seed=batch + ctx)
-    s = pda.make_shape(torch.empty((batch, 32, 128), dtype=torch.bfloat16, device="meta"),
-                       torch.empty((cfg.num_blocks, 8, 16, 128), dtype=torch.bfloat16, device="meta"),
-                       torch.empty((batch, cfg.max_blocks_per_seq), dtype=torch.int32, device="meta"))
-    assert pda.plan(s, pda.make_options())["smem_stages"] == 4
-    sampled_check(pda, oracle_mod, cfg, [0, batch // 2, batch - 1])
-
-
-@pytest.mark.parametrize("batch,ctx", [(64, 4096), (4, 4096)])
-def test_kv8_sweep_cell_twelve_stages_sampled(pda, oracle_mod, batch, ctx):
-    """e4m3 steps <= 1 GiB run 12 single-block stages at 4 CTAs/SM (DESIGN 6)."""
-    cfg = synth.sweep_cell(batch, ctx, seed=batch + ctx)
-    inp = kv8(synth.make_inputs(cfg, seed=0, device="cuda"))
-    out = gpu_kv8(pda, inp)
-    torch.cuda.synchronize()
-    seqs = [0, batch // 2, batch - 1]
-    sub = synth.sample_rows(inp, seqs)
-    sub.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
-    assert max_err(out[seqs], oracle_kv8(oracle_mod, sub)) <= TOL
-    assert torch.isfinite(out).all()
-
-
-def test_full_size_c5_tp8_shard(pda, oracle_mod):
-    """Llama-3-70B shape, one TP=8 rank's shard (1 KV head, 8 q heads)."""
-    cfg = synth.C5_LLAMA3_70B.with_heads(8, 1, name="c5_tp8_rank")
-    sampled_check(pda, oracle_mod, cfg, [0, 128, 255])
-
-
-def test_sweep_cell_ragged(pda, oracle_mod):
-    cfg = synth.sweep_cell(16, 8192, seed=3)
-    sampled_check(pda, oracle_mod, cfg, list(range(0, 16, 5)))
 
 
 # ---- FP8 (e4m3) KV cache (SURVEY 8f NEXT f3) ---------------------------------
@@ -465,25 +400,16 @@ def test_kv8_trace_matches_oracle_plan(pda, oracle_mod):
         assert np.array_equal(tr.cpu().numpy().reshape(ref.shape), ref)
 
 
-@pytest.mark.parametrize("cfg", [synth.C2_LLAMA2_7B, synth.C3_LLAMA3_8B], ids=lambda c: c.name)
-def test_kv8_full_size_sampled(pda, oracle_mod, cfg):
-    inp = kv8(synth.make_inputs(cfg, seed=0, device="cuda"))
-    out = gpu_kv8(pda, inp)
-    torch.cuda.synchronize()
-    B = cfg.num_seqs
-    sub = synth.sample_rows(inp, [0, B // 2, B - 1])
-    sub.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
-    assert max_err(out[[0, B // 2, B - 1]], oracle_kv8(oracle_mod, sub)) <= TOL
-    assert torch.isfinite(out).all()
-
-
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kernel", ["splitk", "balanced"])
-def test_tp_shards_bitwise_equal_unsharded(pda, world, kernel):
+def test_tp_shards_match_unsharded(pda, oracle_mod, world, kernel):
     """KV-head tensor parallelism: each rank's shard, computed by the
-    CUDA kernel on its own heads, concatenated in rank order, equals the
-    unsharded step bit for bit (partition size pinned so the split-K plans
-    match; the balanced kernel's partition depends on the grid -> same num_sms)."""
+    CUDA kernel on its own heads and concatenated in rank order, matches the
+    unsharded oracle (<= 2e-3); for split-K it also equals the unsharded step
+    bit for bit (partition size pinned so the plans match).  The balanced
+    kernel cuts its block ranges by the step's total work, which changes with
+    the head count, so its shards agree with the unsharded step only to
+    rounding -- both are checked against the oracle instead."""
     cfg = synth.Config("tp", 3, 16, 4, 128, (300, 77, 1024), "bf16", poison_blocks=2)
     inp = synth.make_inputs(cfg, seed=31)
     dev = to_dev(inp)
@@ -494,10 +420,10 @@ def test_tp_shards_bitwise_equal_unsharded(pda, world, kernel):
         sh = to_dev(synth.shard_kv_heads(inp, r, world))
         parts.append(gpu(pda, sh, **kw))
     got = torch.cat(parts, dim=1)
+    ref = oracle_out(oracle_mod, inp)
+    assert max_err(got, ref) <= TOL and max_err(full, ref) <= TOL
     if kernel == "splitk":
         assert torch.equal(got, full)
-    else:  # balanced: ranges differ with the head count, results agree to rounding
-        assert (got.float() - full.float()).abs().max().item() <= 2e-3
 
 
 # ---- multi-token (speculative) decode ---------------------
@@ -556,30 +482,54 @@ def test_multi_token_prefetch_bitwise_invisible(pda):
 
 # ---- fused TP output all-gather ----------------------------
 
-@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=32), dict(q_len=2)],
-                         ids=["direct", "combine", "multi_token"])
-def test_fused_gather_writes_every_peer_slice(pda, kw):
-    """The kernel's stores land this rank's heads in every destination buffer at
-    its head offset (three local buffers stand in for three ranks' peer-mapped
-    buffers) and touch nothing else; values equal the plain call bitwise."""
+@pytest.mark.parametrize("kw", [dict(), dict(partition_tokens=32), dict(partition_tokens=64, merge="cluster"),
+                                dict(q_len=2)],
+                         ids=["direct", "combine", "cluster", "multi_token"])
+def test_fused_gather_tp_world_vs_oracle(pda, oracle_mod, kw):
+    """Fused output all-gather (NEXT f2) for a simulated TP world of 3 ranks on
+    one GPU: three local buffers stand in for the ranks' peer-mapped output
+    buffers.  Rank r runs its KV-head shard and its kernel stores
+    its heads into every buffer at head offset r * Hq/N.  After rank 0 only its
+    slice is written (nothing else touched); after all three, every buffer
+    holds the whole step and matches the unsharded fp64 oracle on every row
+    (<= 2e-3), and each slice equals that rank's plain call bit for bit."""
+    kw = dict(kw)
     q_len = kw.pop("q_len", 1)
-    cfg = synth.Config("fg", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
+    world, hq, hkv = 3, 24, 6
+    cfg = synth.Config("fg", 3, hq, hkv, 128, (300, 17, 64), "bf16", poison_blocks=2)
     inp = synth.make_inputs(cfg, seed=9)
     if q_len > 1:
         inp = synth.with_query_tokens(inp, q_len)
-    dev = to_dev(inp)
-    ref = gpu(pda, dev, **kw)
-    world, rank = 3, 1
-    shape = (3, q_len, 8 * world, 128) if q_len > 1 else (3, 8 * world, 128)
+        q4 = inp["q"]
+        ref = oracle_mod.paged_attention_mq(q4, inp["k_cache"], inp["v_cache"], inp["block_tables"],
+                                            inp["context_lens"], inp["scale"], cfg.dtype)
+    else:
+        ref = oracle_out(oracle_mod, inp)
+    shape = tuple(inp["q"].shape)
     peers = [torch.full(shape, 7.0, dtype=torch.bfloat16, device="cuda") for _ in range(world)]
-    pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
-                                      dev["context_lens"], dev["scale"], peers, rank * 8, 8 * world, **kw)
-    torch.cuda.synchronize()
+    hl = hq // world
+    for r in range(world):
+        sh = synth.shard_kv_heads(inp, r, world) if q_len == 1 else _shard_mq(inp, r, world)
+        dev = to_dev(sh)
+        plain = gpu(pda, dev, **kw)
+        pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                          dev["context_lens"], dev["scale"], peers, r * hl, hq, **kw)
+        torch.cuda.synchronize()
+        for pb in peers:
+            assert torch.equal(pb[..., r * hl:(r + 1) * hl, :], plain)
+            if r == 0:
+                assert (pb[..., hl:, :] == 7.0).all()
     for pb in peers:
-        mine = pb[..., 8:16, :]
-        assert torch.equal(mine, ref)
-        others = torch.cat([pb[..., :8, :], pb[..., 16:, :]], dim=-2)
-        assert (others == 7.0).all()
+        assert max_err(pb, ref) <= TOL
+
+
+def _shard_mq(inp, rank, world):
+    """shard_kv_heads for a multi-token q [B, q_len, Hq, D] (heads on dim 2)."""
+    flat = dict(inp, q=inp["q"][:, 0])
+    sh = synth.shard_kv_heads(flat, rank, world)
+    qh = inp["q"].shape[2] // world
+    sh["q"] = inp["q"][:, :, rank * qh:(rank + 1) * qh].contiguous()
+    return sh
 
 
 def test_fused_gather_rejects_bad_offsets(pda):
@@ -699,25 +649,6 @@ def test_fused_append_e4m3(pda, oracle_mod, kw):
     assert max_err(out, ref) <= TOL
 
 
-def test_fused_append_full_size_c2_sampled(pda, oracle_mod):
-    """BASELINE C2 at full size in the bench launch configuration: the written
-    slots match the oracle append (all B x Hkv rows), outputs on sampled rows."""
-    cfg = synth.C2_LLAMA2_7B
-    inp = synth.make_inputs(cfg, seed=16, device="cuda")
-    kn, vn = synth.new_kv_rows(inp, 1, seed=7)
-    out = gpu(pda, inp, k_new=kn, v_new=vn)
-    torch.cuda.synchronize()
-    bt, L = inp["block_tables"].long(), inp["context_lens"].long()
-    t = L - 1
-    phys = bt[torch.arange(cfg.num_seqs, device="cuda"), t // 16]
-    assert torch.equal(inp["k_cache"][phys, :, t % 16], kn[:, 0])
-    assert torch.equal(inp["v_cache"][phys, :, t % 16], vn[:, 0])
-    seqs = [0, 31, 63]
-    sub = synth.sample_rows(inp, seqs)
-    ref = oracle_out(oracle_mod, sub)
-    assert max_err(out[seqs], ref) <= TOL
-
-
 # ---- debug validation of device-resident tables / lengths ------------------------
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
@@ -738,42 +669,6 @@ def test_validate_inputs_matches_oracle(pda, oracle_mod, seed):
     assert got == want
     good = synth.make_inputs(SHAPES[1], seed=1, device="cuda")
     assert pda.validate_inputs(good["block_tables"], good["context_lens"], good["k_cache"].shape[0]) == (0, 0, 0)
-
-
-# ---- maximum sizes ----------------------------------------------------------------
-
-def test_full_size_c5_unsharded(pda, oracle_mod):
-    """Llama-3-70B shape on one GPU (TP=1): 17 GB of KV, 64 q / 8 kv heads."""
-    cfg = synth.C5_LLAMA3_70B
-    sampled_check(pda, oracle_mod, cfg, [0, 255])
-
-
-@pytest.mark.parametrize("kernel", ["splitk", "balanced"])
-def test_max_context_single_sequence(pda, oracle_mod, kernel):
-    """One sequence of 256k tokens (16384 blocks), g = 8: the longest split."""
-    cfg = synth.Config("ctx256k", 1, 8, 1, 128, (262144 - 5,), "bf16", poison_blocks=3)
-    inp = synth.make_inputs(cfg, seed=2, device="cuda")
-    out = gpu(pda, inp, kernel=kernel)
-    torch.cuda.synchronize()
-    rows = [0, 5]
-    ref = oracle_mod.paged_attention(inp["q"].cpu(), inp["k_cache"].cpu(), inp["v_cache"].cpu(),
-                                     inp["block_tables"].cpu(), inp["context_lens"].cpu(), inp["scale"], "bf16",
-                                     rows=rows)
-    g = out.double().cpu().numpy().reshape(-1, 128)
-    assert np.abs(g[rows] - ref.reshape(-1, 128)[rows]).max() <= TOL
-
-
-def test_large_batch_short_contexts(pda, oracle_mod):
-    """8192 sequences (grid z) of 1-64 tokens, MHA D=64."""
-    rng = np.random.default_rng(5)
-    lens = tuple(int(x) for x in rng.integers(0, 65, size=8192))
-    cfg = synth.Config("b8192", 8192, 4, 4, 64, lens, "fp16", poison_blocks=16)
-    inp = synth.make_inputs(cfg, seed=3, device="cuda")
-    out = gpu(pda, inp)
-    torch.cuda.synchronize()
-    seqs = [0, 1, 4095, 8191] + [int(i) for i in np.flatnonzero(np.array(lens) == 0)[:2]]
-    sub = synth.sample_rows(inp, seqs)
-    assert max_err(out[seqs], oracle_out(oracle_mod, sub)) <= TOL
 
 
 # ---- S8 merge inside a thread-block cluster (DSMEM) vs the combine kernel ---------
@@ -821,22 +716,13 @@ def test_cluster_merge_multi_token_kv8_gather_trace(pda, oracle_mod):
     torch.cuda.synchronize()
     for pb in peers:
         assert torch.equal(pb[:, 8:], ref) and (pb[:, :8] == 7.0).all()
+        assert max_err(pb[:, 8:], oracle_out(oracle_mod, synth.make_inputs(cfg, seed=26))) <= TOL
     # the kernel's own bookkeeping is unchanged by the merge mode
     inp = synth.make_inputs(SHAPES[2], seed=27)
     dv = to_dev(inp)
     _, tr_a, _ = gpu(pda, dv, partition_tokens=128, trace=True)
     _, tr_b, _ = gpu(pda, dv, partition_tokens=128, merge="combine", trace=True)
     assert torch.equal(tr_a, tr_b)
-
-
-def test_cluster_merge_full_size_c3(pda, oracle_mod):
-    """BASELINE C3 (P_max 2, the bench partitioning): clusters of 2 == combine, bitwise."""
-    inp = synth.make_inputs(synth.C3_LLAMA3_8B, seed=28, device="cuda")
-    a = gpu(pda, inp, merge="cluster")
-    b = gpu(pda, inp, merge="combine")
-    assert torch.equal(a, b)
-    seqs = [0, 127]
-    assert max_err(a[seqs], oracle_out(oracle_mod, synth.sample_rows(inp, seqs))) <= TOL
 
 
 def test_prepared_decode_matches_wrapper(pda):
