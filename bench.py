@@ -172,6 +172,27 @@ def algorithmic_bytes(cfg, out_elem=2):
     return cfg.kv_bytes() + cfg.other_bytes(out_elem)
 
 
+def spread(xs):
+    """median, p10, p90 (nearest-rank on the sorted sample) and n of a list of times."""
+    xs = sorted(xs)
+    n = len(xs)
+
+    def q(f):
+        return xs[min(n - 1, max(0, int(round(f * (n - 1)))))]
+    return {"median": statistics.median(xs), "p10": q(0.10), "p90": q(0.90), "n": n}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ CPU oracle legs
 def oracle_sample(cfg, seconds: float, seed: int = 0):
     """Time the fp64 oracle (as it stands) on whole sequences of the workload
@@ -229,7 +250,8 @@ def run_reference(args, rank, world):
         "data": "synthetic",
         "config": {"workload": cfg.name, "sample": "one sequence per step (all heads)"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "oracle",
-                         "sample": f"one sequence of {cfg.name} per step, {args.steps} steps"},
+                         "sample": f"one sequence of {cfg.name} per step, {args.steps} steps",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -334,7 +356,11 @@ def main():
     # steps: flush it between timed steps (outside the timed spans)
     flush_buf = L2Flush(torch) if local_cfg.kv_bytes() < 4 * L2_BYTES else None
 
-    def time_steps(fn, steps, warmup, join=None):
+    step_spread = {}
+
+    def time_steps(fn, steps, warmup, join=None, key=None):
+        """Mean device ms per step over `steps` timed steps (max over ranks); with
+        `key`, the per-step spread (median / p10 / p90, us) is kept in step_spread."""
         for _ in range(warmup):
             fn(q, bt, lens, scale)
         if join:
@@ -355,22 +381,28 @@ def main():
                 spans.append((e0, e1))
             torch.cuda.synchronize()
             barrier()
-            ms = sum(a.elapsed_time(b) for a, b in spans) / steps
+            per = [a.elapsed_time(b) for a, b in spans]
+            ms = sum(per) / steps
         else:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(steps):
+            # back-to-back steps, an event between consecutive steps: the K
+            # intervals are the per-step times, their sum the span of the K steps
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+            ev[0].record(stream)
+            for i in range(steps):
                 fn(q, bt, lens, scale)
-            if join:
-                join(stream)  # multi-stream steps: the timer's stream waits for all of them
-            e1.record(stream)
+                if join:
+                    join(stream)  # multi-stream steps: the timer's stream waits for all of them
+                ev[i + 1].record(stream)
             torch.cuda.synchronize()
             barrier()
-            ms = e0.elapsed_time(e1) / steps
+            per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+            ms = ev[0].elapsed_time(ev[-1]) / steps
         if world > 1:
             t = torch.tensor([ms], device="cpu" if share else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
+        if key is not None:
+            step_spread[key] = {k: (v * 1e3 if k != "n" else v) for k, v in spread(per).items()}
         return ms
 
     total_bytes = algorithmic_bytes(cfg)  # whole job (all ranks' shards)
@@ -378,7 +410,7 @@ def main():
     peak, peak_src = load_peaks()
 
     with ClockSampler(dev_index) as clk:
-        ms = time_steps(step_main, args.steps, args.warmup)
+        ms = time_steps(step_main, args.steps, args.warmup, key="step")
         extras = {}
         if step_nccl is not None:  # the NCCL-gather step, for comparison with the fused one
             extras["tp_nccl_gather_us_per_step"] = time_steps(step_nccl, args.steps, 2) * 1e3
@@ -396,7 +428,7 @@ def main():
             for k, fn in arms.items():  # warm each arm
                 fn(q, bt, lens, scale)
             torch.cuda.synchronize()
-            n_rep = max(10, args.steps // 4)
+            n_rep = max(50, args.steps)
             for _ in range(n_rep):
                 for k, fn in arms.items():
                     if flush_buf is not None:
@@ -407,7 +439,11 @@ def main():
                     e1.record(stream)
                     per[k].append((e0, e1))
             torch.cuda.synchronize()
-            med = {k: statistics.median(a.elapsed_time(b) for a, b in v) * 1e3 for k, v in per.items()}
+            us = {k: [a.elapsed_time(b) * 1e3 for a, b in v] for k, v in per.items()}
+            med = {k: statistics.median(v) for k, v in us.items()}
+
+            def ratio(off, on):  # paired per round (the arms of one round ran back to back)
+                return spread([a / b for a, b in zip(us[off], us[on])])
             extras = {
                 "prefetch_on_us": med["on"],
                 "prefetch_off_us": med["off"],
@@ -421,7 +457,11 @@ def main():
                     "prefetch_speedup": med["paper_off"] / med["paper_on"],
                     "desc": "paper structure: grid [Hq,B], 4 warps, warp-per-block LDG, Alg. 1 bulk d=4",
                 },
-                "arms_timing": f"{n_rep} interleaved steps per arm, per-step CUDA events, median",
+                "arms_us": {k: spread(v) for k, v in us.items()},
+                "speedup_spread": {"line_d4": ratio("off", "on"), "bulk_d4": ratio("off", "bulk"),
+                                   "paper_bulk_d4": ratio("paper_off", "paper_on")},
+                "arms_timing": f"{n_rep} interleaved rounds (A B C D E, A B C D E, ...), per-step CUDA events; "
+                               f"medians, p10/p90; speedups = off/on paired per round",
             }
             # FP8 (e4m3) KV-cache variant of the same step
             if cfg.head_dim == 128:
@@ -480,19 +520,24 @@ def main():
                 "desc": "step = append the new token's K/V into its paged slot + attention; fused: the split-K "
                         "CTA owning the slot writes it before its TMA loads (one launch fewer)"}
             del kn, vn
-            # in-run read roofline (read-only stream over a 4 GiB buffer)
+            # in-run read roofline (read-only streams over a 4 GiB buffer): LDG.128 and
+            # two bulk-copy (TMA engine) variants, the best of them is the ceiling
             buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
             sink = torch.zeros(4, dtype=torch.int32, device="cuda")
-            for _ in range(2):
-                pda.read_roofline(buf, sink)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(5):
-                pda.read_roofline(buf, sink)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            extras["read_roofline_gbs"] = buf.numel() * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            probe = {}
+            for mode in ("ldg", "bulk16k", "bulk_ring"):
+                for _ in range(2):
+                    pda.read_roofline(buf, sink, mode=mode)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(5):
+                    pda.read_roofline(buf, sink, mode=mode)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                probe[mode] = buf.numel() * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            extras["read_roofline_probes_gbs"] = probe
+            extras["read_roofline_gbs"] = max(probe.values())
             del buf
             # Eq. 1-2 and the L2 residency bound re-derived for this device (DESIGN 7.5)
             l2 = getattr(torch.cuda.get_device_properties(dev_index), "L2_cache_size", L2_BYTES)
@@ -513,8 +558,28 @@ def main():
     def attn_only(q_, bt_, lens_, scale_):
         pda.paged_decode_attention(q_, inp["k_cache"], inp["v_cache"], bt_, lens_, scale_,
                                    out=step_main.out_local, workspace=step_main.ws, **opt_kw)
-    attn_ms = time_steps(attn_only, args.steps, 2)
+    attn_ms = time_steps(attn_only, args.steps, 2, key="attention")
     achieved = local_bytes / (attn_ms * 1e-3) / 1e9
+
+    # the same attention call captured in a CUDA graph (a serving loop replays the
+    # decode step this way; it removes the Python + C-ABI host cost per launch,
+    # which dominates steps of a few tens of microseconds)
+    graph = None
+    if not args.no_extras:
+        gr = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            attn_only(q, bt, lens, scale)
+        stream.wait_stream(side)
+        with torch.cuda.graph(gr):
+            attn_only(q, bt, lens, scale)
+        graph_ms = time_steps(lambda *_: gr.replay(), args.steps, 2, key="graph")
+        graph = {"us_per_step": graph_ms * 1e3, "eager_us_per_step": attn_ms * 1e3,
+                 "gbs": local_bytes / (graph_ms * 1e-3) / 1e9, "spread_us": step_spread["graph"],
+                 "desc": "attention call (this rank) captured once in a CUDA graph and replayed; eager = the "
+                         "same call launched from Python through the C ABI"}
+        del gr
 
     # end to end through the public C-ABI host entry (pinned host q/bt/lens in, out back)
     e2e = None
@@ -557,7 +622,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_extras:
         gbs, desc, threads, _ = oracle_sample(cfg, 10.0)  # ~10 s of CPU work (bounded sample)
-        cpu = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc}
+        cpu = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": desc,
+               "cpu_model": cpu_model()}
 
     value = total_bytes / (ms * 1e-3) / 1e9
     pl = step_main.plan
@@ -608,6 +674,9 @@ def main():
             "frac_of_read_probe": (achieved / extras["read_roofline_gbs"]) if "read_roofline_gbs" in extras
             else None,
         },
+        "step_us_spread": step_spread.get("step"),
+        "attention_us_spread": step_spread.get("attention"),
+        "cuda_graph": graph,
         "gpu_launches": args.steps * step_main.launches_per_step(),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

@@ -358,8 +358,19 @@ pda_status pda_decode_step_host_async(const void* q_host, const int32_t* block_t
 
 /* Measurement helper (not part of the method): stream-read `bytes` of device
  * memory at `buf` with 16-byte loads on a grid of num_sms * 4 CTAs, writing a
- * checksum word to `sink` (device, 16 B).  Gives the in-run read roofline. */
+ * checksum word to `sink` (device, 16 B).  Gives the in-run read roofline.
+ * Same as pda_read_roofline_mode(buf, bytes, sink, 0, stream). */
 pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream);
+
+/* The read roofline probe with a choice of load path:
+ *   mode 0  16-byte LDG (as pda_read_roofline);
+ *   mode 1  1-D bulk copies (TMA engine) of 16 KiB chunks into a 12-stage
+ *           shared-memory ring, one CTA per SM;
+ *   mode 2  bulk copies shaped like the decode kernel's ring: 8 KiB chunks,
+ *           8 stages, 3 CTAs per SM.
+ * Bulk modes read floor(bytes / chunk) whole chunks.  `buf` and `sink` must
+ * be 16-B aligned (PDA_ERR_ALIGN); mode outside 0..2: PDA_ERR_SHAPE. */
+pda_status pda_read_roofline_mode(const void* buf, size_t bytes, void* sink, int32_t mode, void* stream);
 
 /* Human-readable name of a status code (static string). */
 const char* pda_status_string(pda_status status);

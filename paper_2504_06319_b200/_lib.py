@@ -103,6 +103,8 @@ def lib():
             L.pda_decode_step_host_async.restype = i32
             L.pda_read_roofline.argtypes = [p, sz, p, p]
             L.pda_read_roofline.restype = i32
+            L.pda_read_roofline_mode.argtypes = [p, sz, p, i32, p]
+            L.pda_read_roofline_mode.restype = i32
             L.pda_status_string.argtypes = [i32]
             L.pda_status_string.restype = ctypes.c_char_p
             L.pda_abi_version.restype = ctypes.c_int32
@@ -523,9 +525,13 @@ class HostDecodeStep:
             caller.wait_stream(s)
 
 
-def read_roofline(buf, sink, stream=None):
-    """Launch the read-only streaming probe over `buf` (CUDA tensor)."""
+READ_PROBE_MODES = {"ldg": 0, "bulk16k": 1, "bulk_ring": 2}
+
+
+def read_roofline(buf, sink, stream=None, mode="ldg"):
+    """Launch the read-only streaming probe over `buf` (CUDA tensor); mode: ldg |
+    bulk16k | bulk_ring (include/pda.h pda_read_roofline_mode)."""
     _require_cuda(buf, sink)
-    st = lib().pda_read_roofline(buf.data_ptr(), buf.numel() * buf.element_size(), sink.data_ptr(),
-                                 _stream_handle(stream))
-    _check(st, "pda_read_roofline")
+    st = lib().pda_read_roofline_mode(buf.data_ptr(), buf.numel() * buf.element_size(), sink.data_ptr(),
+                                      READ_PROBE_MODES[mode], _stream_handle(stream))
+    _check(st, "pda_read_roofline_mode")

@@ -189,7 +189,7 @@ cudaError_t launch_kv_append(const AppendParams& a, const int32_t* bt, const int
 cudaError_t launch_validate(const int32_t* bt, const int32_t* lens, int B, int max_blocks,
                             int64_t num_blocks, long long* counts, cudaStream_t stream);
 
-cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms,
+cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms, int mode,
                                  cudaStream_t stream);
 
 }  // namespace pda

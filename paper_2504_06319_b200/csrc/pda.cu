@@ -735,18 +735,23 @@ pda_status pda_decode_step_host_async(const void* q_host, const int32_t* block_t
     return PDA_OK;
 }
 
-pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream) {
+pda_status pda_read_roofline_mode(const void* buf, size_t bytes, void* sink, int32_t mode, void* stream) {
     if (!buf || !sink) return PDA_ERR_NULL;
     if (!aligned16(buf) || !aligned16(sink)) return PDA_ERR_ALIGN;
+    if (mode < 0 || mode > 2) return PDA_ERR_SHAPE;
     pda_status st = use_device_of(buf);
     if (st != PDA_OK) return st;
     int dev = 0, sms = kDefaultSms;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return pda::launch_read_roofline(buf, bytes, sink, sms, static_cast<cudaStream_t>(stream)) ==
+    return pda::launch_read_roofline(buf, bytes, sink, sms, mode, static_cast<cudaStream_t>(stream)) ==
                    cudaSuccess
                ? PDA_OK
                : PDA_ERR_CUDA;
+}
+
+pda_status pda_read_roofline(const void* buf, size_t bytes, void* sink, void* stream) {
+    return pda_read_roofline_mode(buf, bytes, sink, 0, stream);
 }
 
 const char* pda_status_string(pda_status status) {
@@ -762,6 +767,6 @@ const char* pda_status_string(pda_status status) {
     return "PDA_ERR_UNKNOWN";
 }
 
-int32_t pda_abi_version(void) { return 13; }
+int32_t pda_abi_version(void) { return 14; }
 
 }  // extern "C"

@@ -1,6 +1,16 @@
-// roofline.cu -- measurement helper (not part of the method): a read-only
-// stream over a large device buffer with 16-byte non-allocating loads, used
-// by bench.py as the in-run read roofline next to the decode kernel.
+// roofline.cu -- measurement helpers (not part of the method): read-only
+// streams over a large device buffer, used by bench.py as the in-run read
+// roofline next to the decode kernel (LDG.128 and bulk-copy
+// variants).
+//   mode 0  16-byte non-allocating loads (LDG.E.128.CONSTANT), 148 x 4 CTAs x
+//           512 threads, 8 loads in flight per thread;
+//   mode 1  1-D bulk copies (UBLKCP, the TMA engine) of 16 KiB chunks into a
+//           12-stage shared-memory ring per CTA, one CTA per SM (192 KiB in
+//           flight per SM);
+//   mode 2  the decode kernel's own ring shape: 8 KiB chunks (one K + V slab
+//           pair at D = 128), 8 stages, 3 CTAs per SM.
+// The bulk variants move data the way splitk_kernel does (TMA into shared
+// memory, mbarrier completion), so they bound what that kernel can read.
 #include "kernels.cuh"
 #include "ptx.cuh"
 
@@ -28,13 +38,71 @@ __global__ void __launch_bounds__(512) read_roofline_kernel(const uint4* __restr
     if (x == 0x9e3779b9u) sink[0] = x;  // keeps the loads alive; practically never taken
 }
 
+// One warp per CTA: lane 0 keeps S bulk copies of CHUNK bytes in flight; the
+// warp reads one word per lane of every landed chunk (so the data is consumed)
+// and refills the stage.  CTA c streams chunks c, c + G, c + 2G, ...
+template <int CHUNK, int S>
+__global__ void __launch_bounds__(32) read_roofline_bulk_kernel(const uint8_t* __restrict__ buf, size_t n_chunks,
+                                                                uint32_t* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* ring = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+    __shared__ uint64_t bar[S];
+    const int lane = threadIdx.x;
+    const size_t G = gridDim.x;
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            const size_t c = blockIdx.x + s * G;
+            if (c >= n_chunks) break;
+            mbar_arrive_expect_tx(&bar[s], CHUNK);
+            bulk_load_1d(ring + s * CHUNK, buf + c * CHUNK, CHUNK, &bar[s]);
+        }
+    }
+    uint32_t x = 0;
+    for (size_t k = 0;; ++k) {
+        const size_t c = blockIdx.x + k * G;
+        if (c >= n_chunks) break;
+        const int s = (int)(k % S);
+        mbar_wait(&bar[s], (uint32_t)((k / S) & 1));
+        x ^= reinterpret_cast<const uint32_t*>(ring + s * CHUNK)[lane * (CHUNK / 128)];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        const size_t nxt = c + S * G;
+        if (lane == 0 && nxt < n_chunks) {
+            mbar_arrive_expect_tx(&bar[s], CHUNK);
+            bulk_load_1d(ring + s * CHUNK, buf + nxt * CHUNK, CHUNK, &bar[s]);
+        }
+    }
+    if (x == 0x9e3779b9u) sink[0] = x;
+}
+
+template <int CHUNK, int S>
+cudaError_t launch_bulk(const void* buf, size_t bytes, void* sink, int ctas, cudaStream_t stream) {
+    auto kern = read_roofline_bulk_kernel<CHUNK, S>;
+    constexpr size_t smem = (size_t)CHUNK * S + 128;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<ctas, 32, smem, stream>>>(static_cast<const uint8_t*>(buf), bytes / CHUNK, static_cast<uint32_t*>(sink));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms,
+cudaError_t launch_read_roofline(const void* buf, size_t bytes, void* sink, int num_sms, int mode,
                                  cudaStream_t stream) {
-    read_roofline_kernel<<<num_sms * 4, 512, 0, stream>>>(static_cast<const uint4*>(buf), bytes / 16,
-                                                          static_cast<uint32_t*>(sink));
-    return cudaGetLastError();
+    switch (mode) {
+        case 0:
+            read_roofline_kernel<<<num_sms * 4, 512, 0, stream>>>(static_cast<const uint4*>(buf), bytes / 16,
+                                                                  static_cast<uint32_t*>(sink));
+            return cudaGetLastError();
+        case 1: return launch_bulk<16384, 12>(buf, bytes, sink, num_sms, stream);
+        case 2: return launch_bulk<8192, 8>(buf, bytes, sink, num_sms * 3, stream);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace pda

@@ -230,7 +230,7 @@ def test_e4m3_cache_needs_splitk():
 def test_status_strings():
     for code in range(7):
         assert pda.status_string(code).startswith("PDA_")
-    assert pda.lib().pda_abi_version() == 13
+    assert pda.lib().pda_abi_version() == 14
 
 
 def test_product_never_imports_oracle():
