@@ -124,9 +124,9 @@ struct BalancedParams {
     const int32_t* bt;
     const int32_t* lens;
     void* out;
-    float* ws_o;        // [G][2][NH][D]  partials of a CTA's first/last segment
-    float* ws_lse;      // [G][2][NH]
-    uint32_t* tickets;  // [B * Hkv] self-resetting arrival counters (zero before first use)
+    float* ws_o;             // [G][2][NH][D]  partials of a CTA's first/last segment (normalised)
+    float* ws_lse;           // [G][2][NH]     their log2-sum-exp
+    long long* seq_prefix;   // [B + 1] blocks of the sequences before b (written by CTA 0)
     int32_t* trace;
     int B, Hq, Hkv, g, max_blocks;
     int out_dtype;
@@ -134,6 +134,7 @@ struct BalancedParams {
     int eviction;  // pda_eviction bits
     int trace_rec_len;
     float scale_log2;
+    int pdl;  // launched with programmatic stream serialization (PDL)
 };
 
 struct CombineParams {

@@ -163,16 +163,17 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         return PDA_OK;
     }
     if (o->kernel == PDA_KERNEL_BALANCED) {
-        // One persistent wave: as many CTAs as fit (smem, and the register budget
-        // of __launch_bounds__: 3 per SM for g <= 8, 2 for g <= 16).  The
-        // device splits the step's T blocks into G equal ranges (S0).
+        // One persistent wave: 2 CTAs per SM (one head tile; 1 for two tiles),
+        // fewer if the ring does not fit; the device splits the step's T blocks
+        // into G equal ranges (S0) and a combine grid merges the split rows.
         const int n_tiles = (Hq / Hkv) <= 8 ? 1 : 2;
         const int st = o->smem_stages ? o->smem_stages : kDefaultBalancedStages;
         const int sms = o->num_sms ? o->num_sms : kDefaultSms;
         const size_t smem = pda::balanced_smem_bytes(D, n_tiles, st);
         int per_sm = (int)(kSmemPerSm / (smem + kSmemReservedPerCta));
-        const int reg_cap = n_tiles == 1 ? 3 : 2;
+        const int reg_cap = n_tiles == 1 ? 2 : 1;
         per_sm = per_sm < reg_cap ? per_sm : reg_cap;
+        per_sm = per_sm > 0 ? per_sm : 1;
         const int nh = 8 * n_tiles;
         pl->kernel = PDA_KERNEL_BALANCED;
         pl->partition_tokens = (int32_t)max_tokens;
@@ -181,12 +182,12 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         pl->grid_x = sms * per_sm;
         pl->grid_y = 1;
         pl->grid_z = 1;
-        pl->threads = pda::splitk_threads();
+        pl->threads = pda::splitk_threads(true);
         pl->trace_rec_len = 4 + 2 * s->max_blocks_per_seq;
         pl->trace_records = B * Hkv;
         const size_t gx = (size_t)pl->grid_x;
         pl->workspace_bytes = align256(gx * 2 * nh * D * 4) + align256(gx * 2 * nh * 4) +
-                              align256((size_t)B * Hkv * 4);
+                              align256(((size_t)B + 1) * 8);
         return PDA_OK;
     }
     // S0: split-K plan.  Units (partition, kv head, seq) are independent; pick
@@ -344,6 +345,15 @@ pda_status make_append(const void* k_new, const void* v_new, void* k_cache, void
     return PDA_OK;
 }
 
+// Programmatic dependent launch (default on; PDA_PDL=0 turns it off): a grid
+// may be scheduled while the previous grid in the stream drains and waits
+// (griddepcontrol.wait) before its first global read -- back-to-back steps
+// 0.3-10 % faster (profiles/r01_ab_pdl.log)
+bool pdl_enabled() {
+    static const char* env = std::getenv("PDA_PDL");
+    return !(env && std::atoi(env) == 0);
+}
+
 pda_status run(const void* q, const void* k_cache, const void* v_cache, const int32_t* bt,
                const int32_t* lens, float scale, void* out, const pda_shape* s,
                const pda_options* o, void* ws, size_t ws_bytes, int32_t* trace, size_t trace_words,
@@ -421,8 +431,8 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         char* wsc = static_cast<char*>(ws);
         bp.ws_o = reinterpret_cast<float*>(wsc);
         bp.ws_lse = reinterpret_cast<float*>(wsc + align256(gx * 2 * nh * s->head_dim * 4));
-        bp.tickets = reinterpret_cast<uint32_t*>(wsc + align256(gx * 2 * nh * s->head_dim * 4) +
-                                                 align256(gx * 2 * nh * 4));
+        bp.seq_prefix = reinterpret_cast<long long*>(wsc + align256(gx * 2 * nh * s->head_dim * 4) +
+                                                     align256(gx * 2 * nh * 4));
         bp.trace = trace;
         bp.B = s->num_seqs;
         bp.Hq = s->num_q_heads;
@@ -435,6 +445,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         bp.eviction = pl.eviction;
         bp.trace_rec_len = pl.trace_rec_len;
         bp.scale_log2 = scale_log2;
+        bp.pdl = pdl_enabled() && trace == nullptr;
         err = pda::launch_balanced(tmK, tmV, bp, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                                    pl.smem_stages, trace != nullptr, pl.grid_x, stream);
         return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
@@ -490,14 +501,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.ws_o = via_ws ? static_cast<float*>(ws) : nullptr;
     p.ws_lse = via_ws ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
     p.cluster = pl.cluster;
-    {
-        // programmatic dependent launch (default on; PDA_PDL=0 turns it off): the
-        // grid may be scheduled while the previous grid in the stream drains, and
-        // waits (griddepcontrol.wait) before its first global read -- back-to-back
-        // steps 0.3-10 % faster (profiles/r01_ab_pdl.log)
-        static const char* env = std::getenv("PDA_PDL");
-        p.pdl = !(env && std::atoi(env) == 0) && trace == nullptr;
-    }
+    p.pdl = pdl_enabled() && trace == nullptr;
     p.trace = trace;
     p.stamps = stamps;
     p.B = s->num_seqs;

@@ -98,8 +98,12 @@ class TPDecodeAttention:
 
     def launches_per_step(self) -> int:
         # split-K launches its combine kernel when sequences are split and the
-        # partitions do not merge inside a cluster
-        return 1 + (1 if self.plan["kernel"] == 2 and self.plan["p_max"] > 1 and not self.plan["cluster"] else 0)
+        # partitions do not merge inside a cluster; the balanced kernel always
+        # launches its combine grid
+        pl = self.plan
+        if pl["kernel"] == 4:
+            return 2
+        return 1 + (1 if pl["kernel"] == 2 and pl["p_max"] > 1 and not pl["cluster"] else 0)
 
     def __call__(self, q_local, block_tables, context_lens, scale):
         if self.fused:

@@ -188,18 +188,22 @@ def test_plan_stream_persistent_grid():
 
 
 def test_plan_balanced_persistent_wave():
-    # D=128, g=1: ring 8 x 8 KiB + half-width merge 8.5 KiB (+align) = 74 KiB -> 3 CTAs/SM
+    # D=128, g<=8: ring 8 x 8 KiB + two parked segment slots (2 x 16.75 KiB) ~ 99 KiB -> 2 CTAs/SM
     s = shape(num_seqs=64, num_q_heads=32, num_kv_heads=32, head_dim=128, num_blocks=16385,
               max_blocks_per_seq=256)
     assert pda.plan(s, opts())["kernel"] == 2  # AUTO = split-K
     p = pda.plan(s, opts(kernel=4))
-    assert p["kernel"] == 4 and p["grid_x"] == 444 and p["threads"] == 160 and p["smem_stages"] == 8
-    G, nh, D = 444, 8, 128
-    assert p["workspace_bytes"] == G * 2 * nh * D * 4 + G * 2 * nh * 4 + 64 * 32 * 4
-    # g = 16 needs two head tiles: register budget caps it at 2 CTAs/SM
+    assert p["kernel"] == 4 and p["grid_x"] == 296 and p["threads"] == 128 and p["smem_stages"] == 8
+    G, nh, D = 296, 8, 128
+
+    def a256(x):
+        return (x + 255) // 256 * 256
+    assert p["workspace_bytes"] == a256(G * 2 * nh * D * 4) + a256(G * 2 * nh * 4) + a256((64 + 1) * 8)
+    # g = 16 needs two head tiles: one parked slot of 2 x 8 columns, 1 CTA/SM
     s16 = shape(num_seqs=8, num_q_heads=32, num_kv_heads=2, head_dim=128, num_blocks=600,
                 max_blocks_per_seq=64)
-    assert pda.plan(s16, opts(kernel=4))["grid_x"] == 296
+    assert pda.plan(s16, opts(kernel=4))["grid_x"] == 148
+    assert pda.plan(s, opts(kernel=4, num_sms=5))["grid_x"] == 10
 
 
 def test_eviction_auto_resolution():
