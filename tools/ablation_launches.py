@@ -28,10 +28,25 @@ VARIANTS = [
 ]
 
 
+# the batch x context grid (BASELINE configs[3]): paper and
+# split-K kernels, prefetch off / on, at the library's default ring and eviction
+GRID_VARIANTS = [
+    dict(kernel="paper", prefetch="off"),
+    dict(kernel="paper", prefetch="bulk", prefetch_distance=4),
+    dict(kernel="paper", prefetch="bulk", prefetch_distance=4, eviction="prefetch_last"),
+    dict(kernel="paper", prefetch="line", prefetch_distance=4),
+    dict(kernel="splitk", prefetch="off"),
+    dict(kernel="splitk", prefetch="line", prefetch_distance=4),
+    dict(kernel="splitk", prefetch="bulk", prefetch_distance=4),
+]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--grid", action="store_true", help="the C4 grid variant list (GRID_VARIANTS)")
     a = ap.parse_args()
+    variants = GRID_VARIANTS if a.grid else VARIANTS
     import torch
 
     import paper_2504_06319_b200 as pda
@@ -40,10 +55,10 @@ def main():
     from bench import workload_config
     cfg = workload_config(a.config)
     inp = synth.make_inputs(cfg, seed=5, device="cuda")
-    inp8 = synth.quantize_kv_e4m3(inp)
+    inp8 = synth.quantize_kv_e4m3(inp) if any(v.get("kv") == "e4m3" for v in variants) else None
     ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
     order = []
-    for v in VARIANTS:
+    for v in variants:
         kw = {k: x for k, x in v.items() if k != "kv"}
         src = inp
         if v.get("kv") == "e4m3":

@@ -29,7 +29,7 @@ ROWS = [
 def label(v):
     s = v["kernel"]
     if v["kernel"] == "splitk":
-        s += f" S{v['smem_stages']}"
+        s += f" S{v['smem_stages']}" if v.get("smem_stages") else " default ring"
         if v.get("issue_mode"):
             s += f" {v['issue_mode']}"
         if v.get("kv"):
@@ -37,6 +37,8 @@ def label(v):
     s += " " + v["prefetch"]
     if v["prefetch"] != "off":
         s += f" d{v['prefetch_distance']}"
+    if v.get("eviction"):
+        s += f" {v['eviction']}"
     return s
 
 
@@ -50,7 +52,7 @@ def load(path):
     out = []
     for (kid, m), v in zip(kern.items(), order):
         if v["rep"] == 1:
-            out.append((label(v), m))
+            out.append((label(v), m, v))
     return out
 
 
@@ -68,10 +70,46 @@ def fmt(m, key, scale):
     return f"{x:.2f}"
 
 
+def summary(paths):
+    """One row per cell: duration, L2 read hit rate and long-scoreboard share
+    of CPI with prefetch off / on, and the speedup, for every variant."""
+    hdr = None
+    for path in paths:
+        cfg = os.path.basename(path)[len("ablation_"):-4]
+        full = load(path)
+        base = {}
+        for c, m, v in full:
+            if v["prefetch"] == "off":
+                base[(v["kernel"], v.get("issue_mode"), v.get("kv"))] = m
+        if hdr is None:
+            hdr = [c for c, _, v in full if v["prefetch"] != "off"]
+            print("| cell | " + " | ".join(f"{c}: speedup / L2 hit off->on / LS share off->on" for c in hdr) + " |")
+            print("|---|" + "---|" * len(hdr))
+        cells = []
+        for c, m, v in full:
+            if v["prefetch"] == "off":
+                continue
+            m0 = base[(v["kernel"], v.get("issue_mode"), v.get("kv"))]
+            d0 = float(m0["gpu__time_duration.sum"][0])
+            d1 = float(m["gpu__time_duration.sum"][0])
+            h0 = float(m0["lts__t_sector_op_read_hit_rate.pct"][0])
+            h1 = float(m["lts__t_sector_op_read_hit_rate.pct"][0])
+
+            def ls(x):
+                return 100 * float(x["smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"][0]) / \
+                    float(x["smsp__average_warp_latency_per_inst_issued.ratio"][0])
+            cells.append(f"{d0 / d1:.3f}x / {h0:.0f}->{h1:.0f}% / {ls(m0):.0f}->{ls(m):.0f}%")
+        print(f"| {cfg} | " + " | ".join(cells) + " |")
+
+
 def main():
+    if sys.argv[1] == "--summary":
+        summary(sys.argv[2:])
+        return
     for path in sys.argv[1:]:
         cfg = os.path.basename(path)[len("ablation_"):-4]
-        cols = load(path)
+        full = load(path)
+        cols = [(c, m) for c, m, _ in full]
         print(f"### {cfg}\n")
         print("| metric | " + " | ".join(c for c, _ in cols) + " |")
         print("|---|" + "---|" * len(cols))
@@ -90,10 +128,9 @@ def main():
         d0 = [float(m["gpu__time_duration.sum"][0]) for _, m in cols]
         base = {}
         sp = []
-        for (c, m), d in zip(cols, d0):
-            fam = c.rsplit(" ", 2)[0] if (" bulk" in c or " line" in c) else c.rsplit(" ", 1)[0]
-            fam = fam.replace(" S16", "").replace(" S8", "")
-            if c.endswith(" off"):
+        for (c, m, v), d in zip(full, d0):
+            fam = (v["kernel"], v.get("issue_mode"), v.get("kv"))  # same kernel, any ring depth
+            if v["prefetch"] == "off":
                 base[fam] = d
             sp.append(f"{base.get(fam, d) / d:.3f}x")
         print("| Speedup vs same kernel, prefetch off | " + " | ".join(sp) + " |\n")
