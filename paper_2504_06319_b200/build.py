@@ -45,7 +45,11 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out_dir: str | None = None) -> str:
+    """Compile and link; `defines` (-DNAME=V) and `out_dir` (objects + libpda.so
+    elsewhere) exist for A/B builds of compile-time variants only."""
+    BUILD = os.path.join(out_dir, "_build") if out_dir else globals()["BUILD"]
+    LIB = os.path.join(out_dir, "libpda.so") if out_dir else globals()["LIB"]
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "pda.h")]
     jobs = []
@@ -59,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(job):
         path, obj = job
-        cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-c", path, "-o", obj]
+        cmd = [nvcc()] + ARCH + NVCC_FLAGS + list(defines) + ["-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {path}:\n{r.stderr}")
@@ -85,5 +89,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--define", action="append", default=[], help="-DNAME=V for an A/B variant build")
+    ap.add_argument("--out", default=None, help="output directory of an A/B variant build")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, defines=[f"-D{d}" for d in a.define], out_dir=a.out))

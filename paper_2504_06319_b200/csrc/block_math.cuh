@@ -48,6 +48,18 @@ __device__ __forceinline__ void store_out_peers(const OutPeers& o, size_t row, i
 template <int kSlab, int kChunks, int kBoxCols>
 __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                                int row, uint64_t* bar, int eviction, uint64_t pol_first) {
+    if constexpr (kChunks > 1 && kTma3d) {
+        // one 3-D box per slab: (64 columns, 16 rows, kChunks column chunks)
+        // lands as [chunk][row][128 B], the same bytes as kChunks 2-D boxes
+        if (eviction & 1) {
+            tma_load_3d_hint(dst, tmK, 0, row, 0, bar, pol_first);
+            tma_load_3d_hint(dst + kSlab, tmV, 0, row, 0, bar, pol_first);
+        } else {
+            tma_load_3d(dst, tmK, 0, row, 0, bar);
+            tma_load_3d(dst + kSlab, tmV, 0, row, 0, bar);
+        }
+        return;
+    }
 #pragma unroll
     for (int ch = 0; ch < kChunks; ++ch) {
         if (eviction & 1) {
@@ -143,13 +155,14 @@ struct BlockMath {
     }
 
     // Columns = (query token i, head h) pairs, c = i * g + h, c < q_len * g.
-    __device__ __forceinline__ void set_q_tokens(int q_len, int g, int lane) {
+    // col0: first column of this warp's tiles (8 with the tile-split kernel's second tile)
+    __device__ __forceinline__ void set_q_tokens(int q_len, int g, int lane, int col0 = 0) {
         qm1 = q_len - 1;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int col = nt * 8 + 2 * (lane & 3) + c;
+                const int col = col0 + nt * 8 + 2 * (lane & 3) + c;
                 qoff[nt][c] = col < q_len * g ? q_len - 1 - col / g : 0;
             }
     }
@@ -157,11 +170,11 @@ struct BlockMath {
     // q rows of the columns (token i, head h) of kv head kvh of sequence b
     // (q [B, q_len, Hq, D]); padded columns are zero.
     __device__ __forceinline__ void load_q_tokens(const uint16_t* q, int b, int kvh, int Hq, int q_len, int g,
-                                                  int lane) {
+                                                  int lane, int col0 = 0) {
         const int dq = 2 * (lane & 3);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const int col = nt * 8 + (lane >> 2);
+            const int col = col0 + nt * 8 + (lane >> 2);
             const bool ok = col < q_len * g;
             const size_t row = ((size_t)b * q_len + (ok ? col / g : 0)) * Hq + kvh * g + (ok ? col % g : 0);
             const uint32_t* qrow = reinterpret_cast<const uint32_t*>(q + row * D);
@@ -374,11 +387,11 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
     // Q B fragments: qf[2j + half][nt] = Q[col][32j + 16 half + 4(lane%4) + {0,1 | 2,3}],
     // columns = (query token i, head h), c = i * g + h
     __device__ __forceinline__ void load_q_tokens(const uint16_t* q, int b, int kvh, int Hq, int q_len, int g,
-                                                  int lane) {
+                                                  int lane, int col0 = 0) {
         const int t = lane & 3;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const int col = nt * 8 + (lane >> 2);
+            const int col = col0 + nt * 8 + (lane >> 2);
             const bool ok = col < q_len * g;
             const size_t row = ((size_t)b * q_len + (ok ? col / g : 0)) * Hq + kvh * g + (ok ? col % g : 0);
             const uint16_t* qrow = q + row * D;

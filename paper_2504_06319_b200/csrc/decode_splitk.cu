@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
 }  // namespace
 
 
-int splitk_threads(bool self_issue) {
+int splitk_threads(bool self_issue, bool tile_split) {
+    if (tile_split) return splitk_block_threads<true, true>();
     return self_issue ? splitk_block_threads<true>() : splitk_block_threads<false>();
 }
 

@@ -26,6 +26,12 @@ inline cudaError_t ensure_smem_limit(Kern kern, size_t smem, std::atomic<uint64_
 
 constexpr int kBlockSize = 16;     // tokens per KV block
 constexpr int kConsumerWarps = 4;  // split-K kernel consumer warps
+#ifndef PDA_TMA3D
+#define PDA_TMA3D 1
+#endif
+// 16-bit D = 128 slabs (two 128-byte column chunks) load as ONE 3-D TMA box
+// per slab (K and V: 2 UTMALDG per block instead of 4); 0 = two 2-D boxes
+constexpr bool kTma3d = PDA_TMA3D != 0;
 constexpr int kPaperWarps = 4;     // paper kernel: 128 threads = 4 warps (Table 2)
 
 enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };
@@ -79,6 +85,7 @@ struct SplitKParams {
     int cluster;       // > 1: launched as clusters of P_max CTAs (one per partition of a
                        // (seq, kv head) row) that merge their partials through DSMEM
     int pdl;           // launched with programmatic stream serialization (PDL)
+    int tile_split;    // two head tiles on 8 consumer warps, one tile each (16-bit, self-issue)
 };
 
 struct PaperParams {
@@ -161,7 +168,7 @@ PDA_SPLITK_MODE_DECL(0)
 PDA_SPLITK_MODE_DECL(1)
 PDA_SPLITK_MODE_DECL(2)
 #undef PDA_SPLITK_MODE_DECL
-int splitk_threads(bool self_issue = false);
+int splitk_threads(bool self_issue = false, bool tile_split = false);
 
 cudaError_t launch_stream(const CUtensorMap& tmK, const CUtensorMap& tmV, const StreamParams& p,
                           bool bf16, int head_dim, int n_tiles, int stages, int warps, bool trace,

@@ -14,6 +14,8 @@ namespace {
 
 constexpr int kDefaultStages = 8;
 constexpr int kDefaultStagesKV8 = 16;
+constexpr bool kDefaultTileSplit = true;   // tile-split kernel for two-head-tile 16-bit steps
+constexpr int kDefaultTileSplitStages = 12; // 3 stages per warp pair, 2 CTAs/SM: 192 KiB in flight per SM
 constexpr int kDefaultStreamStages = 6;
 constexpr int kDefaultStreamWarps = 2;
 constexpr int kDefaultBalancedStages = 8;
@@ -102,7 +104,18 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 // multi-wave (combine kernel, not a cluster merge) although it would fit one
 // wave at 4/SM.  The split sizes and thresholds below were measured with this
 // convention.
+// Two-head-tile 16-bit steps (g = 16, or q_len * g > 8) run the tile-split
+// kernel: 8 consumer warps, one head tile each, 2 CTAs/SM (splitk_impl.cuh TS).
+// PDA_TILE_SPLIT=0 / 1 overrides the default (A/B measurements only).
+bool tile_split(const pda_shape* s, const pda_options* o) {
+    if (s->kv_dtype == PDA_E4M3 || !self_issue(s, o)) return false;
+    if (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) <= 8) return false;
+    static const char* env = std::getenv("PDA_TILE_SPLIT");
+    return env ? std::atoi(env) != 0 : kDefaultTileSplit;
+}
+
 int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
+    if (tile_split(s, o)) return 2;
     return (n_tiles > 1 && s->kv_dtype != PDA_E4M3 && !self_issue(s, o)) ? 2 : 3;
 }
 
@@ -196,7 +209,9 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     const int n_tiles = q_tokens(s) * (Hq / Hkv) <= 8 ? 1 : 2;
     // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
     int stages = o->smem_stages ? o->smem_stages
-                                : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
+                                : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8
+                                   : tile_split(s, o)     ? kDefaultTileSplitStages
+                                                          : kDefaultStages);
     if (o->smem_stages == 0 && s->kv_dtype == PDA_E4M3 && n_tiles == 1 &&
         2.0 * B * (double)max_tokens * Hkv * D <= 1073741824.0) {
         // e4m3 steps up to 1 GiB of KV: 12 stages consumed one block at a time
@@ -261,7 +276,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->grid_x = (int32_t)p_max;
     pl->grid_y = Hkv;
     pl->grid_z = B;
-    pl->threads = pda::splitk_threads(self_issue(s, o));
+    pl->threads = pda::splitk_threads(self_issue(s, o), tile_split(s, o));
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
     // S8: merge partitions inside a thread-block cluster (DSMEM) when they fit
@@ -301,6 +316,17 @@ bool encode_cache_map(CUtensorMap* m, const void* base, const pda_shape* s) {
     auto enc = get_encode();
     if (!enc) return false;
     const bool kv8 = s->kv_dtype == PDA_E4M3;
+    if (pda::kTma3d && !kv8 && s->head_dim == 128) {
+        // 3-D view (col within a 64-column chunk, row, chunk): one box of
+        // 64 x 16 x 2 is a whole slab, written as [chunk][row][128 B]
+        const cuuint64_t dims[3] = {64, (cuuint64_t)s->num_blocks * s->num_kv_heads * s->block_size, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)s->head_dim * 2, 128};
+        const cuuint32_t box[3] = {64u, (cuuint32_t)s->block_size, 2u};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     const cuuint64_t dims[2] = {(cuuint64_t)s->head_dim,
                                 (cuuint64_t)s->num_blocks * s->num_kv_heads * s->block_size};
     const cuuint64_t strides[1] = {(cuuint64_t)s->head_dim * (kv8 ? 1 : 2)};
@@ -520,6 +546,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.scale_log2 = (float)((double)scale * k_scale * 1.4426950408889634);
     p.out_scale = kv8 && o->v_scale > 0.f ? o->v_scale : 1.f;
     if (app) p.app = *app;  // fused into the split-K kernel (else p.app.k_new == nullptr)
+    p.tile_split = tile_split(s, o) && !app;  // the fused append keeps the two-tile kernel
     const int n_tiles = p.q_len * p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,

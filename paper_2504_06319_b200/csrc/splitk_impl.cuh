@@ -58,8 +58,12 @@ struct MathFor<BF16, D, NT, true> {
 // Self-issue mode (always for e4m3 caches): no producer warp -- each consumer
 // warp refills the ring stages it owns (4 issuers instead of 1; the 2 KiB e4m3
 // slabs need twice the issue rate of the 16-bit path).
-template <bool SELF>
-constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) * 32; }
+// Tile split (TS, two head tiles, 16-bit): 8 consumer warps, warp w computes
+// head tile w / 4 of the blocks j = w (mod 4); the two warps of a block share
+// its ring stage and the second to finish it refills it.  Half the math per
+// warp and twice the warps of the two-tile kernel, at 2 CTAs/SM.
+template <bool SELF, bool TS = false>
+constexpr int splitk_block_threads() { return TS ? 2 * kConsumerWarps * 32 : (kConsumerWarps + (SELF ? 0 : 1)) * 32; }
 
 // MODE: 0 = plain, 1 = debug trace (+ runtime cluster support), 2 = launched
 // as clusters (merge over DSMEM).  The plain instantiation carries no cluster
@@ -73,20 +77,24 @@ constexpr int splitk_block_threads() { return (kConsumerWarps + (SELF ? 0 : 1)) 
 // (it would spill at 3).
 // The producer-warp form (160 threads) keeps 2 CTAs/SM for two tiles (it
 // would spill at 3).
-template <bool KV8, int STAGES, int NT, bool SELF>
+template <bool KV8, int STAGES, int NT, bool SELF, bool TS = false>
 constexpr int splitk_min_blocks() {
-    return KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 3)
-               : (NT == 1 ? (STAGES == 4 && SELF ? 4 : 3) : (SELF ? 3 : 2));
+    return TS ? 2
+              : KV8 ? (NT == 1 ? (STAGES == 12 ? 4 : 3) : 3)
+                    : (NT == 1 ? (STAGES == 4 && SELF ? 4 : 3) : (SELF ? 3 : 2));
 }
 
-template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF>
-__global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_blocks<KV8, STAGES, NT, SELF>())
+template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF, bool TS = false>
+__global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_blocks<KV8, STAGES, NT, SELF, TS>())
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
+    static_assert(!TS || (SELF && !KV8 && NT == 2), "tile split: two 16-bit head tiles, self-issue");
     constexpr bool TRACE = MODE == 1;
     const bool clustered = MODE != 0 && p.cluster > 1;
     using G = Geometry<D, KV8>;
-    using BM = typename MathFor<BF16, D, NT, KV8>::type;
+    constexpr int NTW = TS ? 1 : NT;                       // head tiles per warp
+    constexpr int NW = TS ? 2 * kConsumerWarps : kConsumerWarps;  // consumer warps
+    using BM = typename MathFor<BF16, D, NTW, KV8>::type;
     constexpr int NH = 8 * NT;  // padded heads per CTA
     constexpr int MT = D / 16;  // m-tiles of O^T
 
@@ -108,8 +116,10 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
     float* cl_lse = cl_o + NH * D;                                   // [NH]
 
     const int part = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
-    const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // TS: warp = block slot (mod 4), tile = head tile; else tile 0
+    const int warp = TS ? (threadIdx.x >> 5) & (kConsumerWarps - 1) : threadIdx.x >> 5;
+    const int tile = TS ? threadIdx.x >> 7 : 0;
     const int g = p.g;
 
     // PDL: everything this grid reads may come from the previous grid in the
@@ -147,12 +157,12 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
     // same arithmetic, in the same partition order, as combine_kernel.
     auto cluster_merge = [&]() {
         cluster_sync_all();  // every partition's (o, lse) is in its shared memory
-        if (threadIdx.x < kConsumerWarps * 32) {
+        if (threadIdx.x < NW * 32) {
             const int E = p.q_len * g * D;
             const int per = (E + p.cluster - 1) / p.cluster;
             const int e1 = (part + 1) * per < E ? (part + 1) * per : E;
             const uint32_t o_base = smem_u32(cl_o), l_base = smem_u32(cl_lse);
-            for (int idx = part * per + threadIdx.x; idx < e1; idx += kConsumerWarps * 32) {
+            for (int idx = part * per + threadIdx.x; idx < e1; idx += NW * 32) {
                 const int h = idx / D, dd = idx % D;
                 float M = -INFINITY;
                 for (int q = 0; q < n_parts; ++q) M = fmaxf(M, ld_cluster_f32(cluster_map(l_base + h * 4, q)));
@@ -222,10 +232,15 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
     const int jn0 = t_new0 < e_tok ? t_new0 / kBlockSize - sb : n;
     const int jn1 = t_new0 < e_tok ? (e_tok - 1) / kBlockSize - sb : n - 1;
 
+    // TS: the empty-barrier words are per-stage consumer counters instead
+    int* done_cnt = reinterpret_cast<int*>(empty);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);    // producer's arrive.expect_tx (+ TMA bytes)
-            mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
+            mbar_init(&full[s], 1);  // producer's arrive.expect_tx (+ TMA bytes)
+            if constexpr (TS)
+                done_cnt[s] = 0;
+            else
+                mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
         }
         fence_barrier_init();
         if constexpr (TRACE && SELF) {
@@ -297,8 +312,8 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
 
     // ============================== consumer warps ==============================
     BM bm;
-    bm.set_q_tokens(p.q_len, g, lane);
-    bm.load_q_tokens(p.q, b, kvh, p.Hq, p.q_len, g, lane);
+    bm.set_q_tokens(p.q_len, g, lane, 8 * tile);
+    bm.load_q_tokens(p.q, b, kvh, p.Hq, p.q_len, g, lane, 8 * tile);
     bm.reset();
     if constexpr (SELF) {
         // A warp takes blocks in groups of PAIR (e4m3: pairs 2w, 2w+1 mod 8 with
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
                 ++npf;
             }
         };
-        for (int pos = PAIR * warp; pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
+        for (int pos = PAIR * warp; tile == 0 && pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
             if (pos >= jn0 && pos <= jn1) write_new(pos);
             issue(pos);
             if (PAIR == 2 && pos + 1 < n) {
@@ -362,7 +377,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
         // new-token blocks past the prologue: written now (overlapping the
         // prologue loads), ahead of their refill issue by this same warp
         for (int j = jn0 > STAGES ? jn0 : STAGES; j <= jn1; ++j)
-            if ((j / PAIR) % kConsumerWarps == warp) write_new(j);
+            if ((j / PAIR) % kConsumerWarps == warp && !TS) write_new(j);  // (TS: no fused append)
         int mine = 0;
         for (int j = PAIR * warp; j < n; j += PAIR * kConsumerWarps) {
             const bool two = PAIR == 2 && j + 1 < n;
@@ -391,13 +406,28 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
                 else
                     bm.template block<false>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
             }
-            mine += two ? 2 : 1;
+            if (tile == 0) mine += two ? 2 : 1;
             // our ldmatrix reads of the stages are complete (their registers fed the
             // MMAs above); order them before the async-proxy refills
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (j + STAGES < n) issue(j + STAGES);
-            if (two && j + 1 + STAGES < n) issue(j + 1 + STAGES);
+            if constexpr (TS) {
+                // the second of the stage's two warps to finish refills it (the
+                // count per stage alternates odd / even round by round)
+                if (j + STAGES < n) {
+                    __threadfence_block();
+                    int old = 0;
+                    if (lane == 0) old = atomicAdd(done_cnt + st0, 1);
+                    old = __shfl_sync(kFull, old, 0);
+                    if (old & 1) {
+                        __threadfence_block();
+                        issue(j + STAGES);
+                    }
+                }
+            } else {
+                if (j + STAGES < n) issue(j + STAGES);
+                if (two && j + 1 + STAGES < n) issue(j + 1 + STAGES);
+            }
         }
         if constexpr (TRACE) {
             if (lane == 0) {
@@ -433,13 +463,13 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
     bm.reduce_l();
     const int r0 = lane >> 2;
     const int t0 = 2 * (lane & 3);
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring reads done
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // ring reads done
     if (lane < 4) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int h = nt * 8 + 2 * lane + c;
+                const int h = (tile + nt) * 8 + 2 * lane + c;
                 merge_m[warp * NH + h] = bm.m_run[nt][c];
                 merge_l[warp * NH + h] = bm.l_run[nt][c];
             }
@@ -447,17 +477,17 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF>(), splitk_min_block
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const int dd = BM::dcol(i, lane, r);
-                const int h = nt * 8 + t0 + (r & 1);
+                const int h = (tile + nt) * 8 + t0 + (r & 1);
                 merge_acc[(warp * NH + h) * (D + 4) + dd] = bm.acc[i][nt][r];
             }
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 
     const bool direct = n_parts == 1;
-    for (int idx = threadIdx.x; idx < p.q_len * g * D; idx += kConsumerWarps * 32) {
+    for (int idx = threadIdx.x; idx < p.q_len * g * D; idx += NW * 32) {
         const int h = idx / D, dd = idx % D;  // h: column = (query token, head)
         float M = -INFINITY;
 #pragma unroll
@@ -496,10 +526,10 @@ constexpr size_t smem_bytes_for() {
     return 1024 /* alignment slack */ + big + 2 * STAGES * 8 + 2 * kConsumerWarps * 8 * NT * 4;
 }
 
-template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8 = false, bool SELF = KV8>
+template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8 = false, bool SELF = KV8, bool TS = false>
 cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                        dim3 grid, cudaStream_t stream) {
-    auto kern = splitk_kernel<BF16, D, NT, STAGES, MODE, KV8, SELF>;
+    auto kern = splitk_kernel<BF16, D, NT, STAGES, MODE, KV8, SELF, TS>;
     constexpr size_t smem = smem_bytes_for<D, NT, STAGES, KV8>();
     static std::atomic<uint64_t> smem_set{0};
     if (cudaError_t e = ensure_smem_limit(kern, smem, smem_set); e != cudaSuccess) return e;
@@ -510,7 +540,7 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
     if (p.cluster > 1 || p.pdl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
-        cfg.blockDim = dim3(splitk_block_threads<SELF>(), 1, 1);
+        cfg.blockDim = dim3(splitk_block_threads<SELF, TS>(), 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = stream;
         cudaLaunchAttribute attr[2];
@@ -532,13 +562,22 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
         cfg.numAttrs = na;
         return cudaLaunchKernelEx(&cfg, kern, tmK, tmV, p);
     }
-    kern<<<grid, splitk_block_threads<SELF>(), smem, stream>>>(tmK, tmV, p);
+    kern<<<grid, splitk_block_threads<SELF, TS>(), smem, stream>>>(tmK, tmV, p);
     return cudaGetLastError();
 }
 
 template <bool BF16, int D, int NT, int MODE, bool SELF>
 cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                             int stages, dim3 grid, cudaStream_t s) {
+    if constexpr (NT == 2 && SELF) {
+        if (p.tile_split) {
+            switch (stages) {
+                case 8: return launch_one<BF16, D, 2, 8, MODE, false, true, true>(tmK, tmV, p, grid, s);
+                case 12: return launch_one<BF16, D, 2, 12, MODE, false, true, true>(tmK, tmV, p, grid, s);
+                default: return cudaErrorInvalidValue;
+            }
+        }
+    }
     switch (stages) {
         case 4: return launch_one<BF16, D, NT, 4, MODE, false, SELF>(tmK, tmV, p, grid, s);
         case 8: return launch_one<BF16, D, NT, 8, MODE, false, SELF>(tmK, tmV, p, grid, s);
