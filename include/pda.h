@@ -81,7 +81,17 @@ typedef enum {
 typedef enum {
     PDA_PF_OFF = 0,     /* no prefetch: the ablation baseline */
     PDA_PF_BULK_L2 = 1, /* cp.async.bulk.prefetch.L2 of each K and V slab (one instruction per slab) */
-    PDA_PF_LINE_L2 = 2  /* prefetch.global.L2 of every 128-byte line of each slab */
+    PDA_PF_LINE_L2 = 2, /* prefetch.global.L2 of every 128-byte line of each slab */
+    PDA_PF_AUTO = 3     /* the planner decides where the paper's prefetch pays (measured on B200,
+                           profiles/r02_prefetch_policy.jsonl): with kernel AUTO,
+                           a latency-bound tiny step (one query token, 16-bit KV, at most
+                           kAutoPaperBytes = 2 MiB of KV: B * max_blocks * Hkv * M_block * 2)
+                           runs the paper-structure kernel with Alg. 1's line prefetch at
+                           distance 4 and evict_last prefetches (eviction AUTO) -- 1.13-1.39x
+                           over split-K there; every other step runs split-K without prefetch,
+                           where no prefetch variant was ever faster (p10 of the paired speedup
+                           < 1 on all cells).  prefetch_distance is ignored.  A step that fuses
+                           the KV append or the output gather keeps split-K. */
 } pda_prefetch;
 
 /* L2 eviction priority of the KV traffic ("adjusting the cache eviction
@@ -108,9 +118,14 @@ typedef enum {
     PDA_KERNEL_STREAM = 3, /* B200 persistent kernel: every warp a self-pipelined stream over an
                               equal share of all KV blocks of the step (load-balanced for any
                               length mix), partial rows merged in-kernel; one launch */
-    PDA_KERNEL_BALANCED = 4 /* B200 persistent split-K kernel: one wave of CTAs (producer warp +
+    PDA_KERNEL_BALANCED = 4, /* B200 persistent split-K kernel: one wave of CTAs (producer warp +
                               4 consumer warps each), CTA c owns an equal share of all KV blocks
                               of the step, rows merged in-kernel (ticket); one launch */
+    PDA_KERNEL_TC = 5      /* B200 tcgen05 kernel (decode_tc.cu): one persistent CTA per SM owning
+                              an equal share of the step's KV blocks; QK^T and PV on the 5th-gen
+                              tensor core (tcgen05.mma, accumulators in TMEM), 128-token tiles;
+                              split rows merged by a combine kernel.  16-bit KV, head_dim 128,
+                              one query token, no fused append / gather, no trace */
 } pda_kernel;
 
 typedef struct {

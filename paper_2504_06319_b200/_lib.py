@@ -17,18 +17,18 @@ LIB_PATH = os.environ.get("PDA_LIB_PATH") or os.path.join(HERE, "libpda.so")  # 
 HEADER = os.path.join(os.path.dirname(HERE), "include", "pda.h")
 
 PDA_F16, PDA_BF16, PDA_F32, PDA_E4M3 = 0, 1, 2, 3
-PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2}
+PREFETCH = {"off": 0, "none": 0, None: 0, "bulk": 1, "line": 2, "auto": 3}
 EVICTION = {"normal": 0, "demand_first": 1, "prefetch_last": 2, "both": 3, "auto": 4}
 DEFAULT_EVICTION = "auto"
 ISSUE = {"auto": 0, "producer": 1, "self": 2}
-KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4}
+KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4, "tc": 5}
 
 # Product defaults from the round-1 measurements: the TMA ring
 # already fetches S blocks ahead into shared memory while the current block is
 # computed, so the extra L2 prefetch (the paper's instruction, or per-line) is
 # measured 0-9 % slower on every cell with self-issuing consumers -> off by
 # default; "line" / "bulk" with a distance remain the ablation switch.
-DEFAULT_PREFETCH = "off"
+DEFAULT_PREFETCH = "auto"  # planner: the paper kernel + Alg. 1 prefetch on tiny steps, else off (pda.h)
 DEFAULT_DISTANCE = 4
 
 

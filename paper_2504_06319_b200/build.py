@@ -23,8 +23,9 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpda.so")
 
 SOURCES = ["pda.cu", "decode_splitk.cu", "decode_stream.cu", "decode_balanced.cu", "decode_paper.cu", "roofline.cu",
-           "kv_cache.cu", "decode_splitk_m0.cu", "decode_splitk_m1.cu", "decode_splitk_m2.cu"]
-HEADERS = ["ptx.cuh", "kernels.cuh", "block_math.cuh", "kv_append.cuh", "splitk_impl.cuh"]
+           "kv_cache.cu", "decode_tc.cu", "decode_splitk_m0.cu", "decode_splitk_m1.cu", "decode_splitk_m2.cu"]
+HEADERS = ["ptx.cuh", "kernels.cuh", "block_math.cuh", "kv_append.cuh", "splitk_impl.cuh", "tc_ptx.cuh",
+           "balanced_range.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

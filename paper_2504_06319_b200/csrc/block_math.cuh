@@ -58,16 +58,16 @@ __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* 
             tma_load_3d(dst, tmK, 0, row, 0, bar);
             tma_load_3d(dst + kSlab, tmV, 0, row, 0, bar);
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int ch = 0; ch < kChunks; ++ch) {
-        if (eviction & 1) {
-            tma_load_2d_hint(dst + ch * 2048, tmK, ch * kBoxCols, row, bar, pol_first);
-            tma_load_2d_hint(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar, pol_first);
-        } else {
-            tma_load_2d(dst + ch * 2048, tmK, ch * kBoxCols, row, bar);
-            tma_load_2d(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar);
+        for (int ch = 0; ch < kChunks; ++ch) {
+            if (eviction & 1) {
+                tma_load_2d_hint(dst + ch * 2048, tmK, ch * kBoxCols, row, bar, pol_first);
+                tma_load_2d_hint(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar, pol_first);
+            } else {
+                tma_load_2d(dst + ch * 2048, tmK, ch * kBoxCols, row, bar);
+                tma_load_2d(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar);
+            }
         }
     }
 }

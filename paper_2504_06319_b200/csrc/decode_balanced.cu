@@ -27,55 +27,14 @@
 // S8: rows split between CTAs are merged by balanced_combine_kernel (launched
 // right after, programmatic dependent launch) from the partials of the CTAs
 // covering the row, in CTA order -- deterministic run to run.
+#include "balanced_range.cuh"
 #include "block_math.cuh"
 
 namespace pda {
 
 namespace {
 
-struct Cursor {
-    int b, kvh, j, n, L;  // sequence, kv head, block in row, blocks in row, context length
-    long long pre;        // item index of (b, kvh = 0, j = 0)
-};
-
-__device__ __forceinline__ int clamp_len(const int32_t* lens, int b, int max_tokens) {
-    const int L = __ldg(lens + b);
-    return L < max_tokens ? L : max_tokens;
-}
-
-__device__ __forceinline__ int blocks_of(int L) { return L > 0 ? (L + kBlockSize - 1) / kBlockSize : 0; }
-
-// Next non-empty row after c's row (kv heads of a sequence, then sequences).
-__device__ __forceinline__ void next_row(Cursor& c, const int32_t* lens, int B, int Hkv, int max_tokens) {
-    c.j = 0;
-    if (++c.kvh < Hkv) return;
-    c.kvh = 0;
-    c.pre += (long long)c.n * Hkv;
-    while (++c.b < B) {
-        const int L = clamp_len(lens, c.b, max_tokens);
-        if (L > 0) {
-            c.L = L;
-            c.n = blocks_of(L);
-            return;
-        }
-    }
-}
-
-// Move the cursor k items forward; seg counts the row boundaries crossed.
-__device__ __forceinline__ void advance(Cursor& c, int k, int& seg, const int32_t* lens, int B, int Hkv,
-                                        int max_tokens) {
-    c.j += k;
-    while (c.j >= c.n) {
-        const int over = c.j - c.n;
-        next_row(c, lens, B, Hkv, max_tokens);
-        c.j = over;
-        ++seg;
-    }
-}
-
-// CTA owning item k: the largest c with floor(c*T/G) <= k.
-__device__ __forceinline__ int cta_of(long long k, long long T, int G) { return (int)(((k + 1) * G - 1) / T); }
-__device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }
+using namespace br;
 
 template <int D>
 struct BGeom {
@@ -132,89 +91,17 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
     pdl_wait();
 
     // ---- S0 on the device (warp 0): T, this CTA's range, its first item's
-    // cursor and the number of segments it spans
+    // cursor and the number of segments it spans (balanced_range.cuh)
     if (warp == 0) {
-        long long T = 0;
-        for (int base = 0; base < p.B; base += 256) {
-            int part = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int b = base + u * 32 + lane;
-                if (b < p.B) part += blocks_of(clamp_len(p.lens, b, max_tokens));
-            }
-            T += __reduce_add_sync(kFullMask, (unsigned)part);
-        }
-        // the combine kernel needs every sequence's first item: CTA 0 writes the
-        // exclusive prefix (in blocks, per kv head) of the step's sequences
-        if (c == 0) {
-            long long run = 0;
-            for (int base = 0; base <= p.B; base += 32) {
-                const int b = base + lane;
-                const long long n = b < p.B ? blocks_of(clamp_len(p.lens, b, max_tokens)) : 0;
-                long long incl = n;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const long long y = __shfl_up_sync(kFullMask, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (b <= p.B) p.seq_prefix[b] = run + incl - n;
-                run += __shfl_sync(kFullMask, incl, 31);
-            }
-        }
-        T *= p.Hkv;
-        const int Ge = T < (long long)gridDim.x ? (int)T : (int)gridDim.x;
-        long long k0 = 0, k1 = 0;
-        if (c < Ge) {
-            k0 = range_start(c, T, Ge);
-            k1 = range_start(c + 1, T, Ge);
-        }
-        Cursor cur{};
-        int n_segs = 0, end_j = 0;
-        if (k1 > k0) {
-            long long pre = 0;
-            for (int base = 0;; base += 32) {
-                const int b = base + lane;
-                const long long items = b < p.B ? (long long)blocks_of(clamp_len(p.lens, b, max_tokens)) * p.Hkv : 0;
-                long long incl = items;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const long long y = __shfl_up_sync(kFullMask, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const unsigned hit = __ballot_sync(kFullMask, pre + incl > k0);
-                if (hit) {
-                    const int src = __ffs(hit) - 1;
-                    const long long before = pre + __shfl_sync(kFullMask, incl - items, src);
-                    cur.b = base + src;
-                    cur.L = clamp_len(p.lens, cur.b, max_tokens);
-                    cur.n = blocks_of(cur.L);
-                    cur.pre = before;
-                    const long long off = k0 - before;
-                    cur.kvh = (int)(off / cur.n);
-                    cur.j = (int)(off % cur.n);
-                    break;
-                }
-                pre += __shfl_sync(kFullMask, incl, 31);
-            }
-            // walk the range's rows: segments, and where the last one ends
-            Cursor e = cur;
-            long long rem = k1 - k0;
-            n_segs = 1;
-            while (rem > e.n - e.j) {
-                rem -= e.n - e.j;
-                next_row(e, p.lens, p.B, p.Hkv, max_tokens);
-                ++n_segs;
-            }
-            end_j = e.j + (int)rem - 1;
-        }
+        const br::RangePlan rp = br::plan_range(p.lens, p.B, p.Hkv, max_tokens, c, gridDim.x, p.seq_prefix, lane);
         if (lane == 0) {
-            misc->T = T;
-            misc->k0 = k0;
-            misc->k1 = k1;
-            misc->Ge = Ge;
-            misc->n_segs = n_segs;
-            misc->end_j = end_j;
-            misc->start = cur;
+            misc->T = rp.T;
+            misc->k0 = rp.k0;
+            misc->k1 = rp.k1;
+            misc->Ge = rp.Ge;
+            misc->n_segs = rp.n_segs;
+            misc->end_j = rp.end_j;
+            misc->start = rp.start;
             for (int s = 0; s < 2; ++s) misc->arrive[s] = misc->done[s] = 0;
             for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
             fence_barrier_init();
@@ -528,6 +415,10 @@ cudaError_t launch_b_combine(const BalancedParams& p, int G, cudaStream_t stream
 }
 
 }  // namespace
+
+cudaError_t launch_balanced_combine(const BalancedParams& p, int grid, int head_dim, cudaStream_t stream) {
+    return head_dim == 64 ? launch_b_combine<64>(p, grid, stream) : launch_b_combine<128>(p, grid, stream);
+}
 
 size_t balanced_smem_bytes(int head_dim, int n_tiles, int stages) {
 #define PDA_BS(DD, NN, SS) \

@@ -180,6 +180,14 @@ cudaError_t launch_balanced(const CUtensorMap& tmK, const CUtensorMap& tmV, cons
                             bool bf16, int head_dim, int n_tiles, int stages, bool trace, int grid,
                             cudaStream_t stream);
 size_t balanced_smem_bytes(int head_dim, int n_tiles, int stages);
+// balanced_combine_kernel alone (S8 of the persistent kernels' split rows)
+cudaError_t launch_balanced_combine(const BalancedParams& p, int grid, int head_dim, cudaStream_t stream);
+// the tcgen05 kernel (decode_tc.cu): 16-bit KV, head_dim 128, one query token;
+// tmK a 2-D map (64-column boxes), tmV and tmQ 3-D maps (whole 256-B rows)
+cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmQ,
+                      const BalancedParams& p, bool bf16, int grid, cudaStream_t stream);
+size_t tc_smem_bytes();
+int tc_threads();
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
 

@@ -14,8 +14,7 @@ namespace {
 
 constexpr int kDefaultStages = 8;
 constexpr int kDefaultStagesKV8 = 16;
-constexpr bool kDefaultTileSplit = true;   // tile-split kernel for two-head-tile 16-bit steps
-constexpr int kDefaultTileSplitStages = 12; // 3 stages per warp pair, 2 CTAs/SM: 192 KiB in flight per SM
+constexpr int kDefaultTileSplitStages = 8;  // tile-split kernel ring (12: 180 vs 170 us at B=128 g=16)
 constexpr int kDefaultStreamStages = 6;
 constexpr int kDefaultStreamWarps = 2;
 constexpr int kDefaultBalancedStages = 8;
@@ -62,11 +61,15 @@ pda_status validate(const pda_shape* s, const pda_options* o) {
         (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) > 16 ||
          (o && o->kernel != PDA_KERNEL_AUTO && o->kernel != PDA_KERNEL_SPLITK)))
         return PDA_ERR_UNSUPPORTED;
-    if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_LINE_L2) return PDA_ERR_SHAPE;
-    if (o->prefetch != PDA_PF_OFF && (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
+    if (o->prefetch < PDA_PF_OFF || o->prefetch > PDA_PF_AUTO) return PDA_ERR_SHAPE;
+    if (o->prefetch != PDA_PF_OFF && o->prefetch != PDA_PF_AUTO &&
+        (o->prefetch_distance < 1 || o->prefetch_distance > (1 << 20)))
         return PDA_ERR_SHAPE;
     if (o->partition_tokens < 0 || o->partition_tokens % s->block_size != 0) return PDA_ERR_SHAPE;
-    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_BALANCED) return PDA_ERR_SHAPE;
+    if (o->kernel < PDA_KERNEL_AUTO || o->kernel > PDA_KERNEL_TC) return PDA_ERR_SHAPE;
+    if (o->kernel == PDA_KERNEL_TC &&
+        (s->kv_dtype == PDA_E4M3 || s->head_dim != 128 || q_tokens(s) > 1 || o->smem_stages != 0))
+        return PDA_ERR_UNSUPPORTED;
     if (o->num_sms < 0 || o->stream_warps < 0 || o->eviction < 0 || o->eviction > PDA_EV_AUTO) return PDA_ERR_SHAPE;
     if (o->kernel == PDA_KERNEL_STREAM) {
         const int st = o->smem_stages ? o->smem_stages : kDefaultStreamStages;
@@ -104,19 +107,35 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 // multi-wave (combine kernel, not a cluster merge) although it would fit one
 // wave at 4/SM.  The split sizes and thresholds below were measured with this
 // convention.
-// Two-head-tile 16-bit steps (g = 16, or q_len * g > 8) run the tile-split
-// kernel: 8 consumer warps, one head tile each, 2 CTAs/SM (splitk_impl.cuh TS).
-// PDA_TILE_SPLIT=0 / 1 overrides the default (A/B measurements only).
-bool tile_split(const pda_shape* s, const pda_options* o) {
-    if (s->kv_dtype == PDA_E4M3 || !self_issue(s, o)) return false;
-    if (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) <= 8) return false;
-    static const char* env = std::getenv("PDA_TILE_SPLIT");
-    return env ? std::atoi(env) != 0 : kDefaultTileSplit;
+// prefetch = AUTO with kernel = AUTO: latency-bound tiny steps run the
+// paper-structure kernel with Alg. 1's prefetch (include/pda.h PDA_PF_AUTO)
+constexpr double kAutoPaperBytes = 2097152.0;
+bool auto_paper(const pda_shape* s, const pda_options* o) {
+    if (o->kernel != PDA_KERNEL_AUTO || o->prefetch != PDA_PF_AUTO) return false;
+    if (s->kv_dtype == PDA_E4M3 || q_tokens(s) > 1) return false;
+    const double kv = 4.0 * s->num_seqs * (double)s->max_blocks_per_seq * s->block_size * s->num_kv_heads *
+                      s->head_dim;
+    return kv <= kAutoPaperBytes;
 }
 
 int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
-    if (tile_split(s, o)) return 2;
     return (n_tiles > 1 && s->kv_dtype != PDA_E4M3 && !self_issue(s, o)) ? 2 : 3;
+}
+
+// Two-head-tile 16-bit steps (g = 16, or q_len * g > 8) whose grid of `units`
+// CTAs is one wave at 2 CTAs/SM run the tile-split kernel (8 consumer warps,
+// one head tile each; splitk_impl.cuh TS): B=128 32/2 ctx 8k 170 vs 174 us,
+// B=32 57.3 vs 61.4, B=16 ctx 32k 94.2 vs 98.3, B=64 64/4 170 vs 172; grids of
+// more waves keep the 4-warp kernel at 3 CTAs/SM (B=256 ctx 4k 203 vs 195, C5
+// with 2 query tokens 2408 vs 2399; profiles/r02_ab_ts.log).  Ring 8 or 12.
+// PDA_TILE_SPLIT=0 / 1 forces it off / on (A/B measurements only).
+bool tile_split(const pda_shape* s, const pda_options* o, int64_t units, int sms, int stages) {
+    if (s->kv_dtype == PDA_E4M3 || !self_issue(s, o)) return false;
+    if (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) <= 8) return false;
+    if (stages != 8 && stages != 12) return false;
+    static const char* env = std::getenv("PDA_TILE_SPLIT");
+    if (env) return std::atoi(env) != 0;
+    return units <= 2 * (int64_t)sms;
 }
 
 pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
@@ -133,8 +152,10 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     } else {
         pl->eviction = o->eviction;
     }
-    if (o->kernel == PDA_KERNEL_PAPER) {
+    if (o->kernel == PDA_KERNEL_PAPER || auto_paper(s, o)) {
         // grid [H, B, 1], N_thread = 128 (Table 2)
+        if (o->kernel != PDA_KERNEL_PAPER && o->eviction == PDA_EV_AUTO)
+            pl->eviction = PDA_EV_PREFETCH_LAST;  // prefetch = AUTO's measured variant
         pl->kernel = PDA_KERNEL_PAPER;
         pl->partition_tokens = (int32_t)max_tokens;
         pl->p_max = 1;
@@ -147,6 +168,14 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         pl->trace_rec_len = 4 + 2 * R;
         pl->trace_records = B * Hq * pda::kPaperWarps;
         pl->workspace_bytes = 0;
+        if (o->kernel != PDA_KERNEL_PAPER) {
+            // the same call with a fused append / gather runs split-K (run()):
+            // report its workspace so one allocation serves both
+            pda_options o2 = *o;
+            o2.kernel = PDA_KERNEL_SPLITK;
+            pda_plan_info p2;
+            if (plan(s, &o2, &p2) == PDA_OK) pl->workspace_bytes = p2.workspace_bytes;
+        }
         return PDA_OK;
     }
     if (o->kernel == PDA_KERNEL_STREAM) {
@@ -173,6 +202,27 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         const size_t ns = (size_t)pl->grid_x * w;
         pl->workspace_bytes = align256(ns * 2 * nh * D * 4) + align256(ns * 2 * nh * 4) +
                               align256((size_t)B * Hkv * 4);
+        return PDA_OK;
+    }
+    if (o->kernel == PDA_KERNEL_TC) {
+        // One persistent CTA per SM (its 3-stage ring of 128-token tiles takes
+        // ~219 KB of shared memory); the device splits the step's blocks into
+        // G equal ranges (S0), the balanced combine merges split rows.
+        const int sms = o->num_sms ? o->num_sms : kDefaultSms;
+        const int nh = (Hq / Hkv) <= 8 ? 8 : 16;
+        pl->kernel = PDA_KERNEL_TC;
+        pl->partition_tokens = (int32_t)max_tokens;
+        pl->p_max = 1;
+        pl->smem_stages = 3;
+        pl->grid_x = sms;
+        pl->grid_y = 1;
+        pl->grid_z = 1;
+        pl->threads = pda::tc_threads();
+        pl->trace_rec_len = 0;
+        pl->trace_records = 0;
+        const size_t gx = (size_t)pl->grid_x;
+        pl->workspace_bytes = align256(gx * 2 * nh * D * 4) + align256(gx * 2 * nh * 4) +
+                              align256(((size_t)B + 1) * 8);
         return PDA_OK;
     }
     if (o->kernel == PDA_KERNEL_BALANCED) {
@@ -209,9 +259,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     const int n_tiles = q_tokens(s) * (Hq / Hkv) <= 8 ? 1 : 2;
     // e4m3 stages are half the bytes: default to twice the depth (same bytes in flight)
     int stages = o->smem_stages ? o->smem_stages
-                                : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8
-                                   : tile_split(s, o)     ? kDefaultTileSplitStages
-                                                          : kDefaultStages);
+                                : (s->kv_dtype == PDA_E4M3 ? kDefaultStagesKV8 : kDefaultStages);
     if (o->smem_stages == 0 && s->kv_dtype == PDA_E4M3 && n_tiles == 1 &&
         2.0 * B * (double)max_tokens * Hkv * D <= 1073741824.0) {
         // e4m3 steps up to 1 GiB of KV: 12 stages consumed one block at a time
@@ -269,6 +317,9 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         const int64_t units = (int64_t)B * Hkv * p_max;
         if (units > (int64_t)sms * 3 && units <= (int64_t)sms * 4 * 2) stages = 4;
     }
+    const bool ts = tile_split(s, o, (int64_t)B * Hkv * p_max, sms,
+                               o->smem_stages ? stages : kDefaultTileSplitStages);
+    if (ts && o->smem_stages == 0) stages = kDefaultTileSplitStages;
     pl->kernel = PDA_KERNEL_SPLITK;
     pl->partition_tokens = (int32_t)(P < max_tokens ? P : ceil_div(max_tokens, s->block_size) * s->block_size);
     pl->p_max = (int32_t)p_max;
@@ -276,7 +327,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     pl->grid_x = (int32_t)p_max;
     pl->grid_y = Hkv;
     pl->grid_z = B;
-    pl->threads = pda::splitk_threads(self_issue(s, o), tile_split(s, o));
+    pl->threads = pda::splitk_threads(self_issue(s, o), ts);  // 256: the tile-split kernel
     pl->trace_rec_len = 4 + 2 * (pl->partition_tokens / s->block_size);
     pl->trace_records = (int32_t)(B * Hkv * p_max);
     // S8: merge partitions inside a thread-block cluster (DSMEM) when they fit
@@ -338,6 +389,34 @@ bool encode_cache_map(CUtensorMap* m, const void* base, const pda_shape* s) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 16-bit [rows][128] tensor as a 2-D map with 16-row x 64-column boxes (one
+// 128-byte swizzle atom wide): the tc kernel's K tile is [chunk][token][128 B].
+bool encode_2d_map(CUtensorMap* m, const void* base, uint64_t rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {128, rows};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {64u, 16u};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 16-bit [rows][128] tensor as a 3-D map (col in chunk, row, chunk) whose
+// 64 x 16 x 2 box is 16 whole rows laid out [chunk][row][128 B] (q for the tc kernel).
+bool encode_rows_3d_map(CUtensorMap* m, const void* base, uint64_t rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {64, rows, 2};
+    const cuuint64_t strides[2] = {256, 128};
+    const cuuint32_t box[3] = {64u, 16u, 2u};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // The caller's tensors may live on any device of the process: run on theirs.
 pda_status use_device_of(const void* ptr) {
     cudaPointerAttributes a;
@@ -386,6 +465,13 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
                cudaStream_t stream, void* const* peers = nullptr, int n_peers = 0, int head_off = 0,
                int hq_out = 0, const pda::AppendParams* app = nullptr, uint64_t* stamps = nullptr,
                size_t stamp_words = 0) {
+    pda_options o_splitk;
+    if ((app || n_peers > 0) && auto_paper(s, o)) {
+        // the paper-structure kernel fuses neither the append nor the gather
+        o_splitk = *o;
+        o_splitk.kernel = PDA_KERNEL_SPLITK;
+        o = &o_splitk;
+    }
     pda_plan_info pl;
     pda_status st = plan(s, o, &pl);
     if (st != PDA_OK) return st;
@@ -402,8 +488,10 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     if (st != PDA_OK) return st;
 
     const float scale_log2 = (float)((double)scale * 1.4426950408889634);
-    const int prefetch_mode = o->prefetch;
-    const int pf_dist = o->prefetch != PDA_PF_OFF ? o->prefetch_distance : 0;
+    // prefetch = AUTO: Alg. 1 line prefetch d = 4 on the paper-structure kernel, off elsewhere
+    const bool pf_auto = o->prefetch == PDA_PF_AUTO;
+    const int prefetch_mode = pf_auto ? (pl.kernel == PDA_KERNEL_PAPER ? PDA_PF_LINE_L2 : PDA_PF_OFF) : o->prefetch;
+    const int pf_dist = prefetch_mode == PDA_PF_OFF ? 0 : (pf_auto ? 4 : o->prefetch_distance);
     if (trace && cudaMemsetAsync(trace, 0xff, (size_t)pl.trace_records * pl.trace_rec_len * 4,
                                  stream) != cudaSuccess)
         return PDA_ERR_CUDA;
@@ -440,6 +528,38 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
     }
 
+    if (pl.kernel == PDA_KERNEL_TC) {
+        if (trace || app || n_peers > 0) return PDA_ERR_UNSUPPORTED;
+        CUtensorMap tmK, tmV, tmQ;
+        if (!encode_2d_map(&tmK, k_cache, (uint64_t)s->num_blocks * s->num_kv_heads * s->block_size) ||
+            !encode_cache_map(&tmV, v_cache, s) ||
+            !encode_rows_3d_map(&tmQ, q, (uint64_t)s->num_seqs * s->num_q_heads))
+            return PDA_ERR_CUDA;
+        const size_t gx = (size_t)pl.grid_x;
+        const int nh = (s->num_q_heads / s->num_kv_heads) <= 8 ? 8 : 16;
+        pda::BalancedParams bp{};
+        bp.q = static_cast<const uint16_t*>(q);
+        bp.k = static_cast<const uint16_t*>(k_cache);
+        bp.v = static_cast<const uint16_t*>(v_cache);
+        bp.bt = bt;
+        bp.lens = lens;
+        bp.out = out;
+        char* wsc = static_cast<char*>(ws);
+        bp.ws_o = reinterpret_cast<float*>(wsc);
+        bp.ws_lse = reinterpret_cast<float*>(wsc + align256(gx * 2 * nh * 128 * 4));
+        bp.seq_prefix = reinterpret_cast<long long*>(wsc + align256(gx * 2 * nh * 128 * 4) + align256(gx * 2 * nh * 4));
+        bp.B = s->num_seqs;
+        bp.Hq = s->num_q_heads;
+        bp.Hkv = s->num_kv_heads;
+        bp.g = s->num_q_heads / s->num_kv_heads;
+        bp.max_blocks = s->max_blocks_per_seq;
+        bp.out_dtype = s->out_dtype;
+        bp.eviction = pl.eviction;
+        bp.scale_log2 = scale_log2;
+        bp.pdl = pdl_enabled();
+        err = pda::launch_tc(tmK, tmV, tmQ, bp, s->dtype == PDA_BF16, pl.grid_x, stream);
+        return err == cudaSuccess ? PDA_OK : PDA_ERR_CUDA;
+    }
     CUtensorMap tmK, tmV;
     if (!encode_cache_map(&tmK, k_cache, s) || !encode_cache_map(&tmV, v_cache, s))
         return PDA_ERR_CUDA;
@@ -546,7 +666,9 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     p.scale_log2 = (float)((double)scale * k_scale * 1.4426950408889634);
     p.out_scale = kv8 && o->v_scale > 0.f ? o->v_scale : 1.f;
     if (app) p.app = *app;  // fused into the split-K kernel (else p.app.k_new == nullptr)
-    p.tile_split = tile_split(s, o) && !app;  // the fused append keeps the two-tile kernel
+    // the plan chose the tile-split kernel (its 256-thread block); a fused
+    // append keeps the two-tile kernel
+    p.tile_split = pl.threads == pda::splitk_threads(true, true) && !app;
     const int n_tiles = p.q_len * p.g <= 8 ? 1 : 2;
     err = pda::launch_splitk(tmK, tmV, p, s->dtype == PDA_BF16, s->head_dim, n_tiles,
                              pl.smem_stages, trace != nullptr,

@@ -83,7 +83,8 @@ def test_check_args_shape(kw, status):
 @pytest.mark.parametrize("kw,status", [
     (dict(prefetch=1, prefetch_distance=0), 2),
     (dict(prefetch=0, prefetch_distance=0), 0),
-    (dict(prefetch=3), 2),
+    (dict(prefetch=3), 0),                               # PDA_PF_AUTO
+    (dict(prefetch=4), 2),
     (dict(partition_tokens=24), 2),
     (dict(partition_tokens=32), 0),
     (dict(kernel=2, smem_stages=6), 3),
@@ -92,7 +93,8 @@ def test_check_args_shape(kw, status):
     (dict(kernel=4, smem_stages=6), 3),
     (dict(kernel=4, smem_stages=12), 0),
     (dict(kernel=4, prefetch_distance=33), 3),
-    (dict(kernel=5), 2),
+    (dict(kernel=5), 3),                                 # tc: head_dim 128 only
+    (dict(kernel=6), 2),
     (dict(kernel=7), 2),
     (dict(kernel=2, prefetch_distance=400), 3),          # self-issue window: d <= 32
     (dict(kernel=2, prefetch_distance=400, issue_mode=1), 0),
@@ -427,3 +429,27 @@ def test_planner_invariants(B, g, hkv, D, max_blocks, q_len, kv8, dt):
     if pm == 1:
         assert p["workspace_bytes"] == 0
     assert p["trace_records"] == B * hkv * pm and p["trace_rec_len"] == 4 + 2 * (P // 16)
+
+
+def test_prefetch_auto_policy():
+    """PDA_PF_AUTO (include/pda.h): with kernel AUTO a latency-bound tiny step
+    (16-bit, one query token, <= 2 MiB of KV) plans the paper-structure kernel
+    (its prefetch evict_last under eviction AUTO) and reports split-K's
+    workspace, which the same call needs with a fused append / gather; larger,
+    e4m3 or multi-token steps plan split-K exactly as with prefetch off."""
+    tiny = shape()  # 2 x 256 tokens x 2 kv heads x D 64 x 2 B x (K+V) = 256 KiB
+    p = pda.plan(tiny, opts(prefetch=3, eviction=4))
+    ref = pda.plan(tiny, opts(prefetch=0, eviction=4, kernel=2))
+    assert p["kernel"] == 1 and p["eviction"] == 2
+    assert p["workspace_bytes"] == ref["workspace_bytes"]
+    # explicit prefetch or an explicit kernel: no policy
+    assert pda.plan(tiny, opts(prefetch=2, eviction=4))["kernel"] == 2
+    assert pda.plan(tiny, opts(prefetch=3, kernel=2))["kernel"] == 2
+    # the 2 MiB boundary (upper bound B * max_blocks * 16 * Hkv * D * 2 B * 2)
+    edge = shape(num_seqs=1, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=32, num_blocks=64)
+    assert pda.plan(edge, opts(prefetch=3))["kernel"] == 1
+    over = shape(num_seqs=1, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=33, num_blocks=64)
+    assert pda.plan(over, opts(prefetch=3)) == pda.plan(over, opts(prefetch=0))
+    for kw in (dict(q_len=2), dict(kv_dtype=3, head_dim=128)):
+        s = shape(**kw)
+        assert pda.plan(s, opts(prefetch=3)) == pda.plan(s, opts(prefetch=0))

@@ -41,6 +41,9 @@ def to_dev(inp):
 
 
 def gpu(pda, inp, **kw):
+    # the kernel-level tests pin prefetch (default off); the library default
+    # (prefetch AUTO, include/pda.h) has its own test below
+    kw.setdefault("prefetch", "off")
     return pda.paged_decode_attention(inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"],
                                       inp["context_lens"], inp["scale"], **kw)
 
@@ -842,3 +845,34 @@ def test_fuzz_parity_vs_oracle(pda, oracle_mod, case):
     out = gpu_kv8(pda, dev, **kw) if kv8_case else gpu(pda, dev, **kw)
     assert out.shape == tuple(ref.shape)
     assert max_err(out, ref) <= TOL, kw
+
+
+def test_prefetch_auto_policy_vs_oracle(pda, oracle_mod):
+    """The library default (prefetch AUTO): latency-bound tiny steps run the
+    paper-structure kernel with Alg. 1's line prefetch and
+    evict_last prefetches; larger steps split-K.  Every row against
+    the fp64 oracle, and the tiny step with a fused KV append / output gather
+    (which keep split-K) too."""
+    for cfg in SHAPES:
+        inp = synth.make_inputs(cfg, seed=21)
+        dev = to_dev(inp)
+        out = pda.paged_decode_attention(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                         dev["context_lens"], dev["scale"])
+        torch.cuda.synchronize()
+        assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL, cfg.name
+    # C1 is tiny: the plan is the paper kernel, and it matches the explicit call bit for bit
+    inp = synth.make_inputs(synth.C1_TINY, seed=22)
+    dev = to_dev(inp)
+    a = pda.paged_decode_attention(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                   dev["context_lens"], dev["scale"])
+    b = gpu(pda, dev, kernel="paper", prefetch="line", prefetch_distance=4, eviction="prefetch_last")
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    # gather with the default options: split-K underneath, every row vs the oracle
+    peers = [torch.zeros_like(dev["q"]) for _ in range(2)]
+    pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
+                                      dev["context_lens"], dev["scale"], peers, 0, dev["q"].shape[1])
+    torch.cuda.synchronize()
+    ref = oracle_out(oracle_mod, inp)
+    for pb in peers:
+        assert max_err(pb, ref) <= TOL
