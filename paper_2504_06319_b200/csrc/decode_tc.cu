@@ -40,17 +40,36 @@ namespace {
 
 using namespace br;
 
-constexpr int kTcBlocks = 8;                    // 16-token blocks per tile
-constexpr int kTcTile = kTcBlocks * kBlockSize;  // 128 tokens = UMMA M of QK^T
-constexpr int kTcStages = 3;
+#ifndef PDA_TC_M
+#define PDA_TC_M 128  // tokens per tile = UMMA M of QK^T (64 or 128)
+#endif
+constexpr int kTcTile = PDA_TC_M;                 // tokens per tile = UMMA M of QK^T
+constexpr int kTcBlocks = kTcTile / kBlockSize;  // 16-token blocks per tile
+#ifndef PDA_TC_STAGES
+#define PDA_TC_STAGES (PDA_TC_M == 64 ? 6 : 3)
+#endif
+#ifndef PDA_TC_HINT
+#define PDA_TC_HINT 1
+#endif
+#ifndef PDA_TC_K4D
+#define PDA_TC_K4D 1  // K block = one 4-D box [half][chunk][8 rows][128 B] (else two 2-D boxes)
+#endif
+#ifndef PDA_TC_PAR
+#define PDA_TC_PAR 1  // lane b of the producer warp issues block b's loads (else lane 0 all)
+#endif
+constexpr int kTcStages = PDA_TC_STAGES;
 constexpr int kTcNQ = 16;  // q rows per tile (the GQA group, padded; UMMA N of QK^T)
 constexpr int kTcSoftWarps = 4;
 constexpr int kTcThreads = (kTcSoftWarps + 2) * 32;
-constexpr int kTcKBytes = 2 * kTcTile * 128;       // [chunk][128 tokens][128 B]
-constexpr int kTcVBytes = kTcBlocks * 4096;        // 8 slabs [chunk][16 tokens][128 B]
+// K tile: K4D [block][8-row half][chunk][8 rows][128 B] (8-row groups of a
+// chunk 2048 B apart), else [chunk][tile tokens][128 B] (groups 1024 B apart)
+constexpr int kTcKBytes = 2 * kTcTile * 128;
+constexpr int kTcKChunk = PDA_TC_K4D ? 1024 : kTcTile * 128;  // chunk 1 offset
+constexpr int kTcKSbo = PDA_TC_K4D ? 2048 : 1024;
+constexpr int kTcVBytes = kTcBlocks * 4096;        // one slab [chunk][16 tokens][128 B] per block
 constexpr int kTcQBytes = 2 * kTcNQ * 128;         // [chunk][16 rows][128 B]
 constexpr int kTcStageBytes = kTcKBytes + kTcVBytes + kTcQBytes;
-constexpr int kTcPBytes = kTcTile * 32 * 2;        // P: 128 tokens x (16 hi + 16 lo) columns
+constexpr int kTcPBytes = kTcTile * 32 * 2;        // one P buffer: tile tokens x (16 hi + 16 lo) columns
 constexpr int kTcPSbo = (kTcTile / 8) * 128;       // P core-matrix stride between 8-column groups
 constexpr uint32_t kTcTmemCols = 128;              // S0 [0,16) S1 [16,32) O0 [32,64) O1 [64,96)
 constexpr float kTcRescaleLog2 = 8.f;              // raise m only past m + 8 (p <= 256)
@@ -61,7 +80,7 @@ struct TcTileInfo {
 
 struct TcShared {
     uint64_t full[kTcStages], empty[kTcStages];
-    uint64_t s_full[2], s_free[2], p_full, p_free, o_full[2], o_free[2];
+    uint64_t s_full[2], s_free[2], p_full[2], p_free[2], o_full[2], o_free[2];
     TcTileInfo info[kTcStages];
     uint32_t tmem;
     int n_tiles;
@@ -73,7 +92,7 @@ struct TcShared {
     float lsum[kTcSoftWarps][kTcNQ];
 };
 
-constexpr size_t kTcSmemBytes = 1024 + kTcStages * kTcStageBytes + kTcPBytes + sizeof(TcShared) + 64;
+constexpr size_t kTcSmemBytes = 1024 + kTcStages * kTcStageBytes + 2 * kTcPBytes + sizeof(TcShared) + 64;
 
 // float -> uint key whose unsigned order is the float order (for redux.max)
 __device__ __forceinline__ uint32_t fkey(float x) {
@@ -99,7 +118,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* stages = smem;
     uint8_t* pbuf = smem + kTcStages * kTcStageBytes;
-    TcShared* sh = reinterpret_cast<TcShared*>(pbuf + kTcPBytes);
+    TcShared* sh = reinterpret_cast<TcShared*>(pbuf + 2 * kTcPBytes);  // P double-buffered by tile parity
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int max_tokens = p.max_blocks * kBlockSize;
@@ -138,9 +157,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_init(&sh->s_free[s], kTcSoftWarps);
                 mbar_init(&sh->o_full[s], 1);
                 mbar_init(&sh->o_free[s], kTcSoftWarps);
+                mbar_init(&sh->p_full[s], kTcSoftWarps);
+                mbar_init(&sh->p_free[s], 1);
             }
-            mbar_init(&sh->p_full, kTcSoftWarps);
-            mbar_init(&sh->p_free, 1);
             fence_barrier_init();
         }
     }
@@ -196,13 +215,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     mbar_arrive_expect_tx(&sh->full[st], kTcQBytes + nblk * 8192);
                     tma_load_3d(sb + kTcKBytes + kTcVBytes, &tmQ, 0, cur.b * p.Hq + cur.kvh * g, 0, &sh->full[st]);
                 }
-                for (int blk = 0; blk < nblk; ++blk) {
-                    const int phys = __shfl_sync(kAllLanes, w0, j - wbase + blk);
-                    if (lane == 0) {
-                        const int row = (phys * p.Hkv + cur.kvh) * kBlockSize;
-                        tma_load_2d_hint(sb + blk * 2048, &tmK, 0, row, &sh->full[st], pol_first);
-                        tma_load_2d_hint(sb + kTcTile * 128 + blk * 2048, &tmK, 64, row, &sh->full[st], pol_first);
-                        tma_load_3d_hint(sb + kTcKBytes + blk * 4096, &tmV, 0, row, 0, &sh->full[st], pol_first);
+                __syncwarp();  // lane 0's expect_tx precedes every lane's copies
+                auto issue_block = [&](int blk, int phys) {
+                    const int row = (phys * p.Hkv + cur.kvh) * kBlockSize;
+                    uint64_t* bar = &sh->full[st];
+                    if (PDA_TC_K4D) {
+                        if (PDA_TC_HINT)
+                            tma_load_4d_hint(sb + blk * 4096, &tmK, 0, 0, 0, row >> 3, bar, pol_first);
+                        else
+                            tma_load_4d(sb + blk * 4096, &tmK, 0, 0, 0, row >> 3, bar);
+                    } else if (PDA_TC_HINT) {
+                        tma_load_2d_hint(sb + blk * 2048, &tmK, 0, row, bar, pol_first);
+                        tma_load_2d_hint(sb + kTcTile * 128 + blk * 2048, &tmK, 64, row, bar, pol_first);
+                    } else {
+                        tma_load_2d(sb + blk * 2048, &tmK, 0, row, bar);
+                        tma_load_2d(sb + kTcTile * 128 + blk * 2048, &tmK, 64, row, bar);
+                    }
+                    if (PDA_TC_HINT)
+                        tma_load_3d_hint(sb + kTcKBytes + blk * 4096, &tmV, 0, row, 0, bar, pol_first);
+                    else
+                        tma_load_3d(sb + kTcKBytes + blk * 4096, &tmV, 0, row, 0, bar);
+                };
+                if (PDA_TC_PAR) {
+                    const int phys = __shfl_sync(kAllLanes, w0, (j - wbase + lane) & 31);
+                    if (lane < nblk) issue_block(lane, phys);
+                } else {
+                    for (int blk = 0; blk < nblk; ++blk) {
+                        const int phys = __shfl_sync(kAllLanes, w0, j - wbase + blk);
+                        if (lane == 0) issue_block(blk, phys);
                     }
                 }
             }
@@ -217,7 +257,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             auto pv = [&](int j) {
                 const int st = j % kTcStages;
                 const TcTileInfo in = sh->info[st];
-                mbar_wait(&sh->p_full, j & 1);
+                mbar_wait(&sh->p_full[j & 1], (j >> 1) & 1);
                 tc::fence_after();
                 const int seg = in.flags >> 4, ob = seg & 1;
                 const bool first = in.flags & 1;
@@ -228,10 +268,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t vb = smem_u32(stages + st * kTcStageBytes + kTcKBytes);
                 for (int blk = 0; blk < in.nblk; ++blk) {
                     const uint64_t a = tc::smem_desc(vb + blk * 4096, 2048, 1024, tc::kLayoutSw128);
-                    const uint64_t bd = tc::smem_desc(pb + blk * 256, 128, kTcPSbo, tc::kLayoutInterleave);
+                    const uint64_t bd = tc::smem_desc(pb + (j & 1) * kTcPBytes + blk * 256, 128, kTcPSbo,
+                                                      tc::kLayoutInterleave);
                     tc::mma_f16_ss(tm + 32 + 32 * ob, a, bd, idp, !(first && blk == 0));
                 }
-                tc::commit(&sh->p_free);
+                tc::commit(&sh->p_free[j & 1]);
                 tc::commit(&sh->empty[st]);
                 if (in.flags & 2) tc::commit(&sh->o_full[ob]);
             };
@@ -244,7 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t qb = kb + kTcKBytes + kTcVBytes;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t a = tc::smem_desc(kb + (kk >> 2) * (kTcTile * 128) + (kk & 3) * 32, 16, 1024,
+                    const uint64_t a = tc::smem_desc(kb + (kk >> 2) * kTcKChunk + (kk & 3) * 32, 16, kTcKSbo,
                                                      tc::kLayoutSw128);
                     const uint64_t bd = tc::smem_desc(qb + (kk >> 2) * (kTcNQ * 128) + (kk & 3) * 32, 16, 1024,
                                                       tc::kLayoutSw128);
@@ -258,7 +299,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         __syncwarp();
     } else {
         // ===================== softmax + epilogue (thread = token / d row) =====================
-        const int t = threadIdx.x;                      // token of the tile; d row of O^T
+        // the S^T row (token) of this thread: M = 128 -> TMEM lane = row; M = 64 ->
+        // rows 16w..16w+15 in lanes 0-15 of warp w's quarter (lanes 16-31 unused)
+        const bool mine = kTcTile == 128 || lane < 16;
+        const int t = kTcTile == 128 ? threadIdx.x : warp * 16 + (lane & 15);  // token of the tile
+        const int t_d = threadIdx.x;                                          // d row of O^T
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
         float m_ref[kTcNQ], l[kTcNQ];
         const float scale_log2 = p.scale_log2;
@@ -282,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     l[cc] = 0.f;
                 }
             }
-            const bool valid = t < in.nblk * kBlockSize && in.j0 * kBlockSize + t < in.L;
+            const bool valid = mine && t < in.nblk * kBlockSize && in.j0 * kBlockSize + t < in.L;
             float s[kTcNQ];
             bool need = false;
 #pragma unroll
@@ -320,10 +365,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 rescale_o &= !first;
             }
-            // PV of the previous tile is complete: O^T and P may be touched
-            if (i >= 1) mbar_wait(&sh->p_free, (i - 1) & 1);
+            // P buffer i & 1 is free once PV(i - 2) completed; rescaling O^T
+            // needs every PV issued so far complete (PV(i - 1) too)
+            if (i >= 2) mbar_wait(&sh->p_free[i & 1], ((i >> 1) - 1) & 1);
             const int ob = (in.flags >> 4) & 1;
             if (rescale_o) {
+                mbar_wait(&sh->p_free[(i - 1) & 1], ((i - 1) >> 1) & 1);
                 tc::fence_after();
 #pragma unroll
                 for (int h = 0; h < NP / 16; ++h) {
@@ -351,14 +398,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     lo[cc / 2] = pack2<true>(p0 - hf.x, p1 - hf.y);
                 }
             }
-            uint8_t* prow = pbuf + (t & 7) * 16 + (t >> 3) * 128;
-            *reinterpret_cast<uint4*>(prow) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(prow + kTcPSbo) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-            if constexpr (BF16) {
-                *reinterpret_cast<uint4*>(prow + 2 * kTcPSbo) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                *reinterpret_cast<uint4*>(prow + 3 * kTcPSbo) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+            uint8_t* prow = pbuf + (i & 1) * kTcPBytes + (t & 7) * 16 + (t >> 3) * 128;
+            if (mine) {
+                *reinterpret_cast<uint4*>(prow) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(prow + kTcPSbo) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+                if constexpr (BF16) {
+                    *reinterpret_cast<uint4*>(prow + 2 * kTcPSbo) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4*>(prow + 3 * kTcPSbo) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+                }
             }
-            if (!valid && t < in.nblk * kBlockSize) {
+            if (mine && !valid && t < in.nblk * kBlockSize) {
                 // a loaded token past the context end: zero its V row (0 * NaN would poison PV)
                 uint8_t* vrow = stages + st * kTcStageBytes + kTcKBytes + (t >> 4) * 4096 + (t & 15) * 128;
 #pragma unroll
@@ -370,7 +419,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::fence_async_smem();
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sh->p_full);
+            if (lane == 0) mbar_arrive(&sh->p_full[i & 1]);
 
             if (in.flags & 2) {
                 // ---- S7: the segment's output (whole row) or partial (split row)
@@ -401,7 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) mbar_arrive(&sh->o_free[ob]);
                 const int kind = (in.flags >> 2) & 3;
                 const int NH = g <= 8 ? 8 : 16;
-                const int d = t;
+                const int d = t_d;
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
                     if (cc >= g) break;
@@ -448,6 +497,7 @@ cudaError_t launch_tc_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
 }  // namespace
 
 size_t tc_smem_bytes() { return kTcSmemBytes; }
+bool tc_k4d() { return PDA_TC_K4D != 0; }
 int tc_threads() { return kTcThreads; }
 
 cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmQ,

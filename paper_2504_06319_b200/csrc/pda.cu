@@ -403,6 +403,22 @@ bool encode_2d_map(CUtensorMap* m, const void* base, uint64_t rows) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 16-bit [rows][128] tensor as a 4-D map (col in chunk, row in an 8-row half,
+// chunk, half) whose 64 x 8 x 2 x 2 box is one 16-row block laid out
+// [half][chunk][8 rows][128 B]: the tc kernel's K tile (8-row groups of a
+// chunk 2048 B apart, one box per block).
+bool encode_k4d_map(CUtensorMap* m, const void* base, uint64_t rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[4] = {64, 8, 2, rows / 8};
+    const cuuint64_t strides[3] = {256, 128, 2048};
+    const cuuint32_t box[4] = {64u, 8u, 2u, 2u};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 16-bit [rows][128] tensor as a 3-D map (col in chunk, row, chunk) whose
 // 64 x 16 x 2 box is 16 whole rows laid out [chunk][row][128 B] (q for the tc kernel).
 bool encode_rows_3d_map(CUtensorMap* m, const void* base, uint64_t rows) {
@@ -531,7 +547,8 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
     if (pl.kernel == PDA_KERNEL_TC) {
         if (trace || app || n_peers > 0) return PDA_ERR_UNSUPPORTED;
         CUtensorMap tmK, tmV, tmQ;
-        if (!encode_2d_map(&tmK, k_cache, (uint64_t)s->num_blocks * s->num_kv_heads * s->block_size) ||
+        const uint64_t krows = (uint64_t)s->num_blocks * s->num_kv_heads * s->block_size;
+        if (!(pda::tc_k4d() ? encode_k4d_map(&tmK, k_cache, krows) : encode_2d_map(&tmK, k_cache, krows)) ||
             !encode_cache_map(&tmV, v_cache, s) ||
             !encode_rows_3d_map(&tmQ, q, (uint64_t)s->num_seqs * s->num_q_heads))
             return PDA_ERR_CUDA;
