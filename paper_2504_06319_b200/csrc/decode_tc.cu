@@ -40,56 +40,54 @@ namespace {
 
 using namespace br;
 
-#ifndef PDA_TC_M
-#define PDA_TC_M 128  // tokens per tile = UMMA M of QK^T (64 or 128)
-#endif
-constexpr int kTcTile = PDA_TC_M;                 // tokens per tile = UMMA M of QK^T
+constexpr int kTcTile = 128;                      // tokens per tile = UMMA M of QK^T (thread = token)
 constexpr int kTcBlocks = kTcTile / kBlockSize;  // 16-token blocks per tile
 #ifndef PDA_TC_STAGES
-#define PDA_TC_STAGES (PDA_TC_M == 64 ? 6 : 3)
-#endif
-#ifndef PDA_TC_HINT
-#define PDA_TC_HINT 1
-#endif
-#ifndef PDA_TC_K4D
-#define PDA_TC_K4D 1  // K block = one 4-D box [half][chunk][8 rows][128 B] (else two 2-D boxes)
-#endif
-#ifndef PDA_TC_PAR
-#define PDA_TC_PAR 1  // lane b of the producer warp issues block b's loads (else lane 0 all)
+#define PDA_TC_STAGES 3  // 68 KiB stages: the ring takes 204 KiB of shared memory
 #endif
 constexpr int kTcStages = PDA_TC_STAGES;
 constexpr int kTcNQ = 16;  // q rows per tile (the GQA group, padded; UMMA N of QK^T)
-constexpr int kTcSoftWarps = 4;
+constexpr int kTcGroupWarps = 4;                       // softmax warps per group (one per TMEM lane quarter)
+constexpr int kTcSoftWarps = 2 * kTcGroupWarps;        // two groups, alternating tiles
+constexpr int kTcProducerWarp = kTcSoftWarps, kTcMmaWarp = kTcSoftWarps + 1;
 constexpr int kTcThreads = (kTcSoftWarps + 2) * 32;
-// K tile: K4D [block][8-row half][chunk][8 rows][128 B] (8-row groups of a
-// chunk 2048 B apart), else [chunk][tile tokens][128 B] (groups 1024 B apart)
+// K tile [block][8-row half][chunk][8 rows][128 B]: the 8-row groups of a
+// chunk lie 2048 B apart (one 4-D TMA box per block, encode_k4d_map)
 constexpr int kTcKBytes = 2 * kTcTile * 128;
-constexpr int kTcKChunk = PDA_TC_K4D ? 1024 : kTcTile * 128;  // chunk 1 offset
-constexpr int kTcKSbo = PDA_TC_K4D ? 2048 : 1024;
 constexpr int kTcVBytes = kTcBlocks * 4096;        // one slab [chunk][16 tokens][128 B] per block
 constexpr int kTcQBytes = 2 * kTcNQ * 128;         // [chunk][16 rows][128 B]
 constexpr int kTcStageBytes = kTcKBytes + kTcVBytes + kTcQBytes;
 constexpr int kTcPBytes = kTcTile * 32 * 2;        // one P buffer: tile tokens x (16 hi + 16 lo) columns
 constexpr int kTcPSbo = (kTcTile / 8) * 128;       // P core-matrix stride between 8-column groups
-constexpr uint32_t kTcTmemCols = 128;              // S0 [0,16) S1 [16,32) O0 [32,64) O1 [64,96)
+// TMEM: S of group 0 / 1 at columns [0,16) / [16,32); O^T of (group, segment parity) 32 columns each
+constexpr uint32_t kTcTmemCols = 256;
+__device__ __forceinline__ uint32_t tc_ocol(int gr, int ob) { return 32 + 64 * gr + 32 * ob; }
 constexpr float kTcRescaleLog2 = 8.f;              // raise m only past m + 8 (p <= 256)
 
+// tile flags (per group: a segment's tiles alternate between the two softmax groups)
+constexpr int kFirstG = 1, kLastG = 2, kFinal = 4, kBoth = 8;  // kind << 4, segment parity << 6
+
 struct TcTileInfo {
-    int b, kvh, j0, nblk, L, flags;  // flags: 1 first tile of its segment, 2 last, kind << 2, seg << 4
+    int b, kvh, j0, nblk, L, flags;
+    int ouse[2];  // how many earlier segments of this parity used O[group][parity] (barrier phases)
+    int suse;     // earlier handoffs through st_ready[non-final group][parity]
 };
 
 struct TcShared {
     uint64_t full[kTcStages], empty[kTcStages];
-    uint64_t s_full[2], s_free[2], p_full[2], p_free[2], o_full[2], o_free[2];
+    uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
+    uint64_t o_full[2][2], o_free[2][2], st_ready[2][2];
     TcTileInfo info[kTcStages];
     uint32_t tmem;
     int n_tiles;
-    long long k0, k1;
     int n_segs, end_j;
     Cursor start;
-    int vote[2][kTcSoftWarps];
-    float tmax[2][kTcSoftWarps][kTcNQ];
-    float lsum[kTcSoftWarps][kTcNQ];
+    int vote[2][2][kTcGroupWarps];
+    float tmax[2][2][kTcGroupWarps][kTcNQ];
+    float lsum[2][kTcGroupWarps][kTcNQ];
+    // a group's (m, l) handed to the merging group, [group][parity][handoff parity]: the
+    // writer may run one handoff ahead of the merger's read
+    float st_m[2][2][2][kTcNQ], st_l[2][2][2][kTcNQ];
 };
 
 constexpr size_t kTcSmemBytes = 1024 + kTcStages * kTcStageBytes + 2 * kTcPBytes + sizeof(TcShared) + 64;
@@ -118,7 +116,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* stages = smem;
     uint8_t* pbuf = smem + kTcStages * kTcStageBytes;
-    TcShared* sh = reinterpret_cast<TcShared*>(pbuf + 2 * kTcPBytes);  // P double-buffered by tile parity
+    TcShared* sh = reinterpret_cast<TcShared*>(pbuf + 2 * kTcPBytes);  // P: one buffer per softmax group
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int max_tokens = p.max_blocks * kBlockSize;
@@ -143,8 +141,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         if (lane == 0) {
             sh->n_tiles = n_tiles;
-            sh->k0 = rp.k0;
-            sh->k1 = rp.k1;
             sh->n_segs = rp.n_segs;
             sh->end_j = rp.end_j;
             sh->start = rp.start;
@@ -154,16 +150,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&sh->s_full[s], 1);
-                mbar_init(&sh->s_free[s], kTcSoftWarps);
-                mbar_init(&sh->o_full[s], 1);
-                mbar_init(&sh->o_free[s], kTcSoftWarps);
-                mbar_init(&sh->p_full[s], kTcSoftWarps);
+                mbar_init(&sh->s_free[s], kTcGroupWarps);
+                mbar_init(&sh->p_full[s], kTcGroupWarps);
                 mbar_init(&sh->p_free[s], 1);
+                for (int ob = 0; ob < 2; ++ob) {
+                    mbar_init(&sh->o_full[s][ob], 1);
+                    mbar_init(&sh->o_free[s][ob], kTcGroupWarps);
+                    mbar_init(&sh->st_ready[s][ob], 1);
+                }
             }
             fence_barrier_init();
         }
     }
-    if (warp == kTcSoftWarps + 1) tc::alloc<kTcTmemCols>(&sh->tmem);
+    if (warp == kTcMmaWarp) tc::alloc<kTcTmemCols>(&sh->tmem);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -177,7 +176,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int i = threadIdx.x; i < p.Hq * 128; i += kTcSoftWarps * 32)
                     store_out(p.out, (size_t)b * p.Hq * 128 + i, 0.f, p.out_dtype);
 
-    if (warp == kTcSoftWarps) {
+    if (warp == kTcProducerWarp) {
         // ============================ TMA producer ============================
         if (lane == 0) {
             prefetch_tmap(&tmK);
@@ -190,10 +189,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const bool starts_row = cur.j == 0;
         int tile = 0;
         int wrow = -1, wbase = 0, w0 = 0;  // 32 block ids [wbase, wbase + 32) of row wrow
+        int ouse[2][2] = {{0, 0}, {0, 0}}, suse[2][2] = {{0, 0}, {0, 0}};  // barrier use counts
         for (int seg = 0; tile < n_tiles; ++seg) {
             const int jend = seg == n_segs - 1 ? end_j : cur.n - 1;
             const int kind = tc_kind(seg, n_segs, end_j, cur.n, starts_row);
             const int32_t* btrow = p.bt + (size_t)cur.b * p.max_blocks;
+            const int t0 = tile, nt = (jend - cur.j + kTcBlocks) / kTcBlocks;  // this segment's tiles
+            const int ob = seg & 1;
+            const int merger = (t0 + nt - 1) & 1;  // the group of the final tile merges both groups
+            // use indices of this segment's O buffers / state handoff (see TcTileInfo)
+            const int u0 = ouse[0][ob], u1 = ouse[1][ob], us = suse[merger ^ 1][ob];
+            for (int gg = 0; gg < 2; ++gg)
+                if (nt >= 2 || (t0 & 1) == gg) ++ouse[gg][ob];
+            if (nt >= 2) ++suse[merger ^ 1][ob];
             for (int j = cur.j; j <= jend; j += kTcBlocks, ++tile) {
                 const int nblk = jend - j + 1 < kTcBlocks ? jend - j + 1 : kTcBlocks;
                 if (cur.b != wrow || j < wbase || j + nblk > wbase + 32) {  // refill the id window
@@ -211,115 +219,109 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     in.j0 = j;
                     in.nblk = nblk;
                     in.L = cur.L;
-                    in.flags = (j == cur.j ? 1 : 0) | (j + kTcBlocks > jend ? 2 : 0) | (kind << 2) | (seg << 4);
+                    const int k = tile - t0;
+                    in.flags = (k < 2 ? kFirstG : 0) | (k >= nt - 2 ? kLastG : 0) | (k == nt - 1 ? kFinal : 0) |
+                               (nt >= 2 ? kBoth : 0) | (kind << 4) | (ob << 6);
+                    in.ouse[0] = u0;
+                    in.ouse[1] = u1;
+                    in.suse = us;
                     mbar_arrive_expect_tx(&sh->full[st], kTcQBytes + nblk * 8192);
                     tma_load_3d(sb + kTcKBytes + kTcVBytes, &tmQ, 0, cur.b * p.Hq + cur.kvh * g, 0, &sh->full[st]);
                 }
                 __syncwarp();  // lane 0's expect_tx precedes every lane's copies
-                auto issue_block = [&](int blk, int phys) {
+                // lane b issues block b: K as one 4-D box, V as one 3-D box
+                const int phys = __shfl_sync(kAllLanes, w0, (j - wbase + lane) & 31);
+                if (lane < nblk) {
                     const int row = (phys * p.Hkv + cur.kvh) * kBlockSize;
-                    uint64_t* bar = &sh->full[st];
-                    if (PDA_TC_K4D) {
-                        if (PDA_TC_HINT)
-                            tma_load_4d_hint(sb + blk * 4096, &tmK, 0, 0, 0, row >> 3, bar, pol_first);
-                        else
-                            tma_load_4d(sb + blk * 4096, &tmK, 0, 0, 0, row >> 3, bar);
-                    } else if (PDA_TC_HINT) {
-                        tma_load_2d_hint(sb + blk * 2048, &tmK, 0, row, bar, pol_first);
-                        tma_load_2d_hint(sb + kTcTile * 128 + blk * 2048, &tmK, 64, row, bar, pol_first);
-                    } else {
-                        tma_load_2d(sb + blk * 2048, &tmK, 0, row, bar);
-                        tma_load_2d(sb + kTcTile * 128 + blk * 2048, &tmK, 64, row, bar);
-                    }
-                    if (PDA_TC_HINT)
-                        tma_load_3d_hint(sb + kTcKBytes + blk * 4096, &tmV, 0, row, 0, bar, pol_first);
-                    else
-                        tma_load_3d(sb + kTcKBytes + blk * 4096, &tmV, 0, row, 0, bar);
-                };
-                if (PDA_TC_PAR) {
-                    const int phys = __shfl_sync(kAllLanes, w0, (j - wbase + lane) & 31);
-                    if (lane < nblk) issue_block(lane, phys);
-                } else {
-                    for (int blk = 0; blk < nblk; ++blk) {
-                        const int phys = __shfl_sync(kAllLanes, w0, j - wbase + blk);
-                        if (lane == 0) issue_block(blk, phys);
-                    }
+                    tma_load_4d_hint(sb + lane * 4096, &tmK, 0, 0, 0, row >> 3, &sh->full[st], pol_first);
+                    tma_load_3d_hint(sb + kTcKBytes + lane * 4096, &tmV, 0, row, 0, &sh->full[st], pol_first);
                 }
             }
             if (tile < n_tiles) next_row(cur, p.lens, p.B, p.Hkv, max_tokens);
         }
-    } else if (warp == kTcSoftWarps + 1) {
+    } else if (warp == kTcMmaWarp) {
         // ============================ MMA issuer ============================
         if (lane == 0) {
             const uint32_t idq = tc::idesc_f16(BF16, kTcTile, kTcNQ, false, false);
             const uint32_t idp = tc::idesc_f16(BF16, 128, NP, true, true);
             const uint32_t pb = smem_u32(pbuf);
             auto pv = [&](int j) {
-                const int st = j % kTcStages;
+                const int st = j % kTcStages, gj = j & 1;
                 const TcTileInfo in = sh->info[st];
-                mbar_wait(&sh->p_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&sh->p_full[gj], (j >> 1) & 1);
                 tc::fence_after();
-                const int seg = in.flags >> 4, ob = seg & 1;
-                const bool first = in.flags & 1;
-                if (first && seg >= 2) {
-                    mbar_wait(&sh->o_free[ob], ((seg >> 1) - 1) & 1);
+                const int ob = (in.flags >> 6) & 1;
+                const bool first = in.flags & kFirstG;
+                const int use = gj ? in.ouse[1] : in.ouse[0];
+                if (first && use >= 1) {  // O[gj][ob] read out by the previous segment's merge
+                    mbar_wait(&sh->o_free[gj][ob], (use - 1) & 1);
                     tc::fence_after();
                 }
                 const uint32_t vb = smem_u32(stages + st * kTcStageBytes + kTcKBytes);
                 for (int blk = 0; blk < in.nblk; ++blk) {
                     const uint64_t a = tc::smem_desc(vb + blk * 4096, 2048, 1024, tc::kLayoutSw128);
-                    const uint64_t bd = tc::smem_desc(pb + (j & 1) * kTcPBytes + blk * 256, 128, kTcPSbo,
+                    const uint64_t bd = tc::smem_desc(pb + gj * kTcPBytes + blk * 256, 128, kTcPSbo,
                                                       tc::kLayoutInterleave);
-                    tc::mma_f16_ss(tm + 32 + 32 * ob, a, bd, idp, !(first && blk == 0));
+                    tc::mma_f16_ss(tm + tc_ocol(gj, ob), a, bd, idp, !(first && blk == 0));
                 }
-                tc::commit(&sh->p_free[j & 1]);
+                tc::commit(&sh->p_free[gj]);
                 tc::commit(&sh->empty[st]);
-                if (in.flags & 2) tc::commit(&sh->o_full[ob]);
+                if (in.flags & kLastG) tc::commit(&sh->o_full[gj][ob]);
             };
-            for (int i = 0; i < n_tiles; ++i) {
-                const int st = i % kTcStages, sb = i & 1;
-                mbar_wait(&sh->full[st], (i / kTcStages) & 1);
-                if (i >= 2) mbar_wait(&sh->s_free[sb], ((i >> 1) - 1) & 1);
-                tc::fence_after();
-                const uint32_t kb = smem_u32(stages + st * kTcStageBytes);
-                const uint32_t qb = kb + kTcKBytes + kTcVBytes;
+            // event loop: QK^T of tile i as soon as its data and its group's S
+            // buffer are there (up to 2 tiles ahead of PV), PV of tile j as soon
+            // as its group's P is written -- the two softmax groups never wait
+            // for each other through this thread's program order
+            int i = 0, j = 0;
+            while (j < n_tiles) {
+                if (i < n_tiles && i < j + 2) {
+                    const int st = i % kTcStages, sb = i & 1;
+                    if (mbar_test(&sh->full[st], (i / kTcStages) & 1) &&
+                        (i < 2 || mbar_test(&sh->s_free[sb], ((i >> 1) - 1) & 1))) {
+                        tc::fence_after();
+                        const uint32_t kb = smem_u32(stages + st * kTcStageBytes);
+                        const uint32_t qb = kb + kTcKBytes + kTcVBytes;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t a = tc::smem_desc(kb + (kk >> 2) * kTcKChunk + (kk & 3) * 32, 16, kTcKSbo,
-                                                     tc::kLayoutSw128);
-                    const uint64_t bd = tc::smem_desc(qb + (kk >> 2) * (kTcNQ * 128) + (kk & 3) * 32, 16, 1024,
-                                                      tc::kLayoutSw128);
-                    tc::mma_f16_ss(tm + 16 * sb, a, bd, idq, kk > 0);
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t a =
+                                tc::smem_desc(kb + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 2048, tc::kLayoutSw128);
+                            const uint64_t bd = tc::smem_desc(qb + (kk >> 2) * (kTcNQ * 128) + (kk & 3) * 32, 16,
+                                                              1024, tc::kLayoutSw128);
+                            tc::mma_f16_ss(tm + 16 * sb, a, bd, idq, kk > 0);
+                        }
+                        tc::commit(&sh->s_full[sb]);
+                        ++i;
+                        continue;
+                    }
                 }
-                tc::commit(&sh->s_full[sb]);
-                if (i >= 1) pv(i - 1);
+                if (j < i && mbar_test(&sh->p_full[j & 1], (j >> 1) & 1)) {
+                    pv(j);
+                    ++j;
+                }
             }
-            if (n_tiles > 0) pv(n_tiles - 1);
         }
         __syncwarp();
     } else {
-        // ===================== softmax + epilogue (thread = token / d row) =====================
-        // the S^T row (token) of this thread: M = 128 -> TMEM lane = row; M = 64 ->
-        // rows 16w..16w+15 in lanes 0-15 of warp w's quarter (lanes 16-31 unused)
-        const bool mine = kTcTile == 128 || lane < 16;
-        const int t = kTcTile == 128 ? threadIdx.x : warp * 16 + (lane & 15);  // token of the tile
-        const int t_d = threadIdx.x;                                          // d row of O^T
-        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        // ========= softmax + epilogue: group gr (warps 4gr..4gr+3) owns tiles i with i % 2 == gr =========
+        const int gr = warp / kTcGroupWarps, gw = warp % kTcGroupWarps;  // gw = the warp's TMEM lane quarter
+        const int t = gw * 32 + lane;  // token of the tile = S^T row; d row of O^T
+        const uint32_t lane_base = (uint32_t)(gw * 32) << 16;
+        const int bar_id = 1 + gr;
         float m_ref[kTcNQ], l[kTcNQ];
         const float scale_log2 = p.scale_log2;
-        for (int i = 0; i < n_tiles; ++i) {
-            const int st = i % kTcStages, sb = i & 1;
+        for (int i = gr; i < n_tiles; i += 2) {
+            const int st = i % kTcStages, it = i >> 1;
             mbar_wait(&sh->full[st], (i / kTcStages) & 1);  // acquire the producer's tile info
             const TcTileInfo in = sh->info[st];
-            mbar_wait(&sh->s_full[sb], (i >> 1) & 1);
+            mbar_wait(&sh->s_full[gr], it & 1);
             tc::fence_after();
             uint32_t r[16];
-            tc::ld_32x32b_x16(tm + lane_base + 16 * sb, r);
+            tc::ld_32x32b_x16(tm + lane_base + 16 * gr, r);
             tc::wait_ld();
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sh->s_free[sb]);
-            const bool first = in.flags & 1;
+            if (lane == 0) mbar_arrive(&sh->s_free[gr]);
+            const bool first = in.flags & kFirstG;
             if (first) {
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     l[cc] = 0.f;
                 }
             }
-            const bool valid = mine && t < in.nblk * kBlockSize && in.j0 * kBlockSize + t < in.L;
+            const bool valid = t < in.nblk * kBlockSize && in.j0 * kBlockSize + t < in.L;
             float s[kTcNQ];
             bool need = false;
 #pragma unroll
@@ -336,13 +338,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 s[cc] = valid ? __uint_as_float(r[cc]) * scale_log2 : -INFINITY;
                 need |= s[cc] > m_ref[cc] + kTcRescaleLog2;
             }
-            // every softmax warp must agree on m: one vote per tile
+            // every warp of the group must agree on m: one vote per tile
             const bool wneed = __any_sync(kAllLanes, need);
-            if (lane == 0) sh->vote[i & 1][warp] = wneed;
-            asm volatile("bar.sync 1, %0;" ::"n"(kTcSoftWarps * 32) : "memory");
+            if (lane == 0) sh->vote[gr][it & 1][gw] = wneed;
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kTcGroupWarps * 32) : "memory");
             bool any = false;
 #pragma unroll
-            for (int w = 0; w < kTcSoftWarps; ++w) any |= sh->vote[i & 1][w] != 0;
+            for (int w = 0; w < kTcGroupWarps; ++w) any |= sh->vote[gr][it & 1][w] != 0;
             bool rescale_o = false;
             float alpha[kTcNQ];
             if (any) {
@@ -350,14 +352,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
                     const uint32_t k = __reduce_max_sync(kAllLanes, fkey(s[cc]));
-                    if (lane == cc) sh->tmax[i & 1][warp][cc] = fkey_inv(k);
+                    if (lane == cc) sh->tmax[gr][it & 1][gw][cc] = fkey_inv(k);
                 }
-                asm volatile("bar.sync 1, %0;" ::"n"(kTcSoftWarps * 32) : "memory");
+                asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kTcGroupWarps * 32) : "memory");
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
                     float mx = m_ref[cc];
 #pragma unroll
-                    for (int w = 0; w < kTcSoftWarps; ++w) mx = fmaxf(mx, sh->tmax[i & 1][w][cc]);
+                    for (int w = 0; w < kTcGroupWarps; ++w) mx = fmaxf(mx, sh->tmax[gr][it & 1][w][cc]);
                     alpha[cc] = m_ref[cc] == -INFINITY ? 0.f : ex2(m_ref[cc] - mx);
                     rescale_o |= alpha[cc] != 1.f;
                     l[cc] *= alpha[cc];
@@ -365,17 +367,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 rescale_o &= !first;
             }
-            // P buffer i & 1 is free once PV(i - 2) completed; rescaling O^T
-            // needs every PV issued so far complete (PV(i - 1) too)
-            if (i >= 2) mbar_wait(&sh->p_free[i & 1], ((i >> 1) - 1) & 1);
-            const int ob = (in.flags >> 4) & 1;
+            // the group's previous PV is complete: its P buffer and O^T may be touched
+            if (it >= 1) mbar_wait(&sh->p_free[gr], (it - 1) & 1);
+            const int ob = (in.flags >> 6) & 1;
             if (rescale_o) {
-                mbar_wait(&sh->p_free[(i - 1) & 1], ((i - 1) >> 1) & 1);
                 tc::fence_after();
 #pragma unroll
                 for (int h = 0; h < NP / 16; ++h) {
                     uint32_t o[16];
-                    const uint32_t oa = tm + lane_base + 32 + 32 * ob + 16 * h;
+                    const uint32_t oa = tm + lane_base + tc_ocol(gr, ob) + 16 * h;
                     tc::ld_32x32b_x16(oa, o);
                     tc::wait_ld();
 #pragma unroll
@@ -398,16 +398,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     lo[cc / 2] = pack2<true>(p0 - hf.x, p1 - hf.y);
                 }
             }
-            uint8_t* prow = pbuf + (i & 1) * kTcPBytes + (t & 7) * 16 + (t >> 3) * 128;
-            if (mine) {
-                *reinterpret_cast<uint4*>(prow) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<uint4*>(prow + kTcPSbo) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-                if constexpr (BF16) {
-                    *reinterpret_cast<uint4*>(prow + 2 * kTcPSbo) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                    *reinterpret_cast<uint4*>(prow + 3 * kTcPSbo) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-                }
+            uint8_t* prow = pbuf + gr * kTcPBytes + (t & 7) * 16 + (t >> 3) * 128;
+            *reinterpret_cast<uint4*>(prow) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(prow + kTcPSbo) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+            if constexpr (BF16) {
+                *reinterpret_cast<uint4*>(prow + 2 * kTcPSbo) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                *reinterpret_cast<uint4*>(prow + 3 * kTcPSbo) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
             }
-            if (mine && !valid && t < in.nblk * kBlockSize) {
+            if (!valid && t < in.nblk * kBlockSize) {
                 // a loaded token past the context end: zero its V row (0 * NaN would poison PV)
                 uint8_t* vrow = stages + st * kTcStageBytes + kTcKBytes + (t >> 4) * 4096 + (t & 15) * 128;
 #pragma unroll
@@ -419,50 +417,93 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::fence_async_smem();
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sh->p_full[i & 1]);
+            if (lane == 0) mbar_arrive(&sh->p_full[gr]);
 
-            if (in.flags & 2) {
-                // ---- S7: the segment's output (whole row) or partial (split row)
+            if (in.flags & kLastG) {
+                // ---- S7: this group's share of the segment: (m, l) per column
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
                     float v = l[cc];
 #pragma unroll
                     for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kAllLanes, v, o);
-                    if (lane == cc) sh->lsum[warp][cc] = v;
+                    if (lane == cc) sh->lsum[gr][gw][cc] = v;
                 }
-                asm volatile("bar.sync 1, %0;" ::"n"(kTcSoftWarps * 32) : "memory");
-                float Lsum[kTcNQ];
+                asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kTcGroupWarps * 32) : "memory");
+                float Ls[kTcNQ];
 #pragma unroll
                 for (int cc = 0; cc < kTcNQ; ++cc) {
-                    Lsum[cc] = 0.f;
+                    Ls[cc] = 0.f;
 #pragma unroll
-                    for (int w = 0; w < kTcSoftWarps; ++w) Lsum[cc] += sh->lsum[w][cc];
+                    for (int w = 0; w < kTcGroupWarps; ++w) Ls[cc] += sh->lsum[gr][w][cc];
                 }
-                const int seg = in.flags >> 4;
-                mbar_wait(&sh->o_full[ob], (seg >> 1) & 1);
-                tc::fence_after();
-                uint32_t oh[16], ol[16];
-                tc::ld_32x32b_x16(tm + lane_base + 32 + 32 * ob, oh);
-                if constexpr (BF16) tc::ld_32x32b_x16(tm + lane_base + 32 + 32 * ob + 16, ol);
-                tc::wait_ld();
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sh->o_free[ob]);
-                const int kind = (in.flags >> 2) & 3;
-                const int NH = g <= 8 ? 8 : 16;
-                const int d = t_d;
+                if (!(in.flags & kFinal)) {
+                    // hand the share to the other group, which merges at the segment's final tile
 #pragma unroll
-                for (int cc = 0; cc < kTcNQ; ++cc) {
-                    if (cc >= g) break;
-                    float o = __uint_as_float(oh[cc]);
-                    if constexpr (BF16) o += __uint_as_float(ol[cc]);
-                    o = o / Lsum[cc];
-                    if (kind == 0) {
-                        store_out(p.out, ((size_t)in.b * p.Hq + in.kvh * g + cc) * 128 + d, o, p.out_dtype);
-                    } else {
-                        const size_t ws = (size_t)c * 2 + (kind - 1);
-                        p.ws_o[(ws * NH + cc) * 128 + d] = o;
-                        if (d == 0) p.ws_lse[ws * NH + cc] = m_ref[cc] + __log2f(Lsum[cc]);
+                    for (int cc = 0; cc < kTcNQ; ++cc)
+                        if (t == cc) {  // (static register indices: no local-memory arrays)
+                            sh->st_m[gr][ob][in.suse & 1][cc] = m_ref[cc];
+                            sh->st_l[gr][ob][in.suse & 1][cc] = Ls[cc];
+                        }
+                    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kTcGroupWarps * 32) : "memory");
+                    if (t == 0) mbar_arrive(&sh->st_ready[gr][ob]);
+                } else {
+                    // ---- merge both groups' shares (the segment's output or partial)
+                    const int og = gr ^ 1;
+                    const bool both = in.flags & kBoth;
+                    const int use_own = gr ? in.ouse[1] : in.ouse[0], use_oth = gr ? in.ouse[0] : in.ouse[1];
+                    if (both) mbar_wait(&sh->st_ready[og][ob], in.suse & 1);
+                    mbar_wait(&sh->o_full[gr][ob], use_own & 1);
+                    if (both) mbar_wait(&sh->o_full[og][ob], use_oth & 1);
+                    tc::fence_after();
+                    // O^T row d of both groups (hi + lo terms summed as they are read)
+                    float oa[16], ox[16];
+                    {
+                        uint32_t h[16], lo_[16];
+                        tc::ld_32x32b_x16(tm + lane_base + tc_ocol(gr, ob), h);
+                        if constexpr (BF16) tc::ld_32x32b_x16(tm + lane_base + tc_ocol(gr, ob) + 16, lo_);
+                        tc::wait_ld();
+#pragma unroll
+                        for (int cc = 0; cc < 16; ++cc)
+                            oa[cc] = __uint_as_float(h[cc]) + (BF16 ? __uint_as_float(lo_[cc]) : 0.f);
+                        if (both) {
+                            tc::ld_32x32b_x16(tm + lane_base + tc_ocol(og, ob), h);
+                            if constexpr (BF16) tc::ld_32x32b_x16(tm + lane_base + tc_ocol(og, ob) + 16, lo_);
+                            tc::wait_ld();
+                        }
+#pragma unroll
+                        for (int cc = 0; cc < 16; ++cc)
+                            ox[cc] = both ? __uint_as_float(h[cc]) + (BF16 ? __uint_as_float(lo_[cc]) : 0.f) : 0.f;
+                    }
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&sh->o_free[gr][ob]);
+                        if (both) mbar_arrive(&sh->o_free[og][ob]);
+                    }
+                    const int kind = (in.flags >> 4) & 3;
+                    const int NH = g <= 8 ? 8 : 16;
+                    const int d = t;
+#pragma unroll
+                    for (int cc = 0; cc < kTcNQ; ++cc) {
+                        if (cc >= g) break;
+                        float M = m_ref[cc], den = Ls[cc], num = oa[cc];
+                        if (both) {
+                            const float mo = sh->st_m[og][ob][in.suse & 1][cc];
+                            const float lo2 = sh->st_l[og][ob][in.suse & 1][cc];
+                            const float Mn = fmaxf(M, mo);
+                            const float wa = ex2(M - Mn), wb = ex2(mo - Mn);
+                            num = num * wa + ox[cc] * wb;
+                            den = den * wa + lo2 * wb;
+                            M = Mn;
+                        }
+                        const float v = num / den;
+                        if (kind == 0) {
+                            store_out(p.out, ((size_t)in.b * p.Hq + in.kvh * g + cc) * 128 + d, v, p.out_dtype);
+                        } else {
+                            const size_t ws = (size_t)c * 2 + (kind - 1);
+                            p.ws_o[(ws * NH + cc) * 128 + d] = v;
+                            if (d == 0) p.ws_lse[ws * NH + cc] = M + __log2f(den);
+                        }
                     }
                 }
             }
@@ -472,7 +513,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     pdl_launch_dependents();
     tc::fence_before();
     __syncthreads();
-    if (warp == kTcSoftWarps + 1) tc::dealloc<kTcTmemCols>(tm);
+    if (warp == kTcMmaWarp) tc::dealloc<kTcTmemCols>(tm);
 }
 
 template <bool BF16>
@@ -497,7 +538,7 @@ cudaError_t launch_tc_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
 }  // namespace
 
 size_t tc_smem_bytes() { return kTcSmemBytes; }
-bool tc_k4d() { return PDA_TC_K4D != 0; }
+
 int tc_threads() { return kTcThreads; }
 
 cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmQ,

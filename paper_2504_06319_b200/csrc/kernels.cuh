@@ -187,7 +187,6 @@ cudaError_t launch_balanced_combine(const BalancedParams& p, int grid, int head_
 cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmQ,
                       const BalancedParams& p, bool bf16, int grid, cudaStream_t stream);
 size_t tc_smem_bytes();
-bool tc_k4d();  // the tc kernel loads K blocks with the 4-D map (encode_k4d_map)
 int tc_threads();
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);

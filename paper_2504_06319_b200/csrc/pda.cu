@@ -548,7 +548,7 @@ pda_status run(const void* q, const void* k_cache, const void* v_cache, const in
         if (trace || app || n_peers > 0) return PDA_ERR_UNSUPPORTED;
         CUtensorMap tmK, tmV, tmQ;
         const uint64_t krows = (uint64_t)s->num_blocks * s->num_kv_heads * s->block_size;
-        if (!(pda::tc_k4d() ? encode_k4d_map(&tmK, k_cache, krows) : encode_2d_map(&tmK, k_cache, krows)) ||
+        if (!encode_k4d_map(&tmK, k_cache, krows) ||
             !encode_cache_map(&tmV, v_cache, s) ||
             !encode_rows_3d_map(&tmQ, q, (uint64_t)s->num_seqs * s->num_q_heads))
             return PDA_ERR_CUDA;

@@ -100,15 +100,15 @@ FULL = {
     "c2": (synth.C2_LLAMA2_7B, [dict(), dict(prefetch="line", prefetch_distance=4),
                                 dict(prefetch="bulk", prefetch_distance=4),
                                 dict(kernel="paper", prefetch="bulk", prefetch_distance=4),
-                                dict(kernel="paper", prefetch="off"), dict(kernel="stream")]),
+                                dict(kernel="paper", prefetch="off"), dict(kernel="stream"), dict(kernel="tc")]),
     # C3: defaults (P_max 2 + combine), both merge forms, prefetch d 4, the persistent kernels
     "c3": (synth.C3_LLAMA3_8B, [dict(), dict(merge="cluster"), dict(prefetch="line", prefetch_distance=4),
                                 dict(prefetch="bulk", prefetch_distance=4), dict(kernel="balanced"),
-                                dict(kernel="stream")]),
-    "c5_tp1": (C5, [dict(), dict(prefetch="line", prefetch_distance=4)]),
+                                dict(kernel="stream"), dict(kernel="tc")]),
+    "c5_tp1": (C5, [dict(), dict(prefetch="line", prefetch_distance=4), dict(kernel="tc")]),
     "c5_tp2_rank": (C5.with_heads(32, 4, name="c5_tp2_rank"), [dict()]),
     "c5_tp4_rank": (C5.with_heads(16, 2, name="c5_tp4_rank"), [dict()]),
-    "c5_tp8_rank": (C5.with_heads(8, 1, name="c5_tp8_rank"), [dict(), dict(kernel="balanced")]),
+    "c5_tp8_rank": (C5.with_heads(8, 1, name="c5_tp8_rank"), [dict(), dict(kernel="balanced"), dict(kernel="tc")]),
 }
 
 

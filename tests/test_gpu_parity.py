@@ -876,3 +876,48 @@ def test_prefetch_auto_policy_vs_oracle(pda, oracle_mod):
     ref = oracle_out(oracle_mod, inp)
     for pb in peers:
         assert max_err(pb, ref) <= TOL
+
+
+TC_SHAPES = [c for c in SHAPES if c.head_dim == 128] + [
+    synth.Config("tc_long_gqa8", 2, 16, 2, 128, (4500, 129), "bf16", poison_blocks=2),
+    synth.Config("tc_ragged", 6, 8, 4, 128, (1, 0, 127, 128, 129, 2049), "fp16", poison_blocks=3),
+]
+
+
+@pytest.mark.parametrize("cfg", TC_SHAPES, ids=lambda c: c.name)
+@pytest.mark.parametrize("sms", [0, 7, 1])
+def test_tc_kernel_vs_oracle(pda, oracle_mod, cfg, sms):
+    """The tcgen05 kernel (kernel="tc", decode_tc.cu): every row vs the fp64
+    oracle, with the full grid and with 7 / 1 CTAs (ranges that split rows
+    many ways, or none), ragged and zero lengths, NaN-poisoned tails."""
+    inp = synth.make_inputs(cfg, seed=31)
+    dev = to_dev(inp)
+    out = gpu(pda, dev, kernel="tc", num_sms=sms)
+    torch.cuda.synchronize()
+    assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL
+
+
+def test_tc_kernel_rescale_paths(pda, oracle_mod):
+    """Scores that keep growing along the context (a ramp of +0.2 per token in
+    the log2 domain) make every tile raise the reference max by far more
+    than the 2^8 slack, so O^T and l are rescaled in TMEM on every tile; a
+    late needle does it once.  Both vs the fp64 oracle."""
+    for kind in ("ramp", "needle"):
+        cfg = synth.Config("tc_rescale", 2, 8, 1, 128, (1500, 700), "bf16")
+        inp = synth.make_inputs(cfg, seed=5)
+        q, k = inp["q"], inp["k_cache"]
+        q[:] = 0
+        q[..., 0] = 1.0
+        bt = inp["block_tables"]
+        for b, L in enumerate(cfg.context_lens):
+            for tok in range(L):
+                blk, row = bt[b, tok // 16], tok % 16
+                if kind == "ramp":
+                    val = tok * 0.2 / inp["scale"] / 1.4426950408889634
+                else:
+                    val = (60.0 if tok == L - 3 else 0.0) / inp["scale"] / 1.4426950408889634
+                k[blk, :, row, 0] = val
+        dev = to_dev(inp)
+        out = gpu(pda, dev, kernel="tc")
+        torch.cuda.synchronize()
+        assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL, kind
