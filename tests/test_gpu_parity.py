@@ -693,7 +693,8 @@ def test_cluster_merge_bitwise_equals_combine(pda, oracle_mod, cfg, kw):
     dev = to_dev(inp)
     kw = dict(kw)
     mode = kw.pop("merge", "auto")
-    info = pda.plan(pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"]), pda.make_options(merge=mode, **kw))
+    info = pda.plan(pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"]),
+                    pda.make_options(merge=mode, prefetch="off", **kw))
     assert info["cluster"] == info["p_max"] > 1
     a = gpu(pda, dev, merge=mode, **kw)
     b = gpu(pda, dev, merge="combine", **kw)
