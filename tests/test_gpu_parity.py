@@ -733,7 +733,7 @@ def test_prepared_decode_matches_wrapper(pda):
     for cfg, kw in ((SHAPES[2], dict(partition_tokens=64)), (SHAPES[0], dict(kernel="paper")),
                     (SHAPES[3], dict(kernel="balanced"))):
         dev = to_dev(synth.make_inputs(cfg, seed=29))
-        step = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], **kw)
+        step = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], prefetch="off", **kw)
         a = step(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"], dev["scale"])
         b = gpu(pda, dev, **kw)
         assert torch.equal(a, b)
@@ -745,7 +745,7 @@ def test_graphed_decode_replays_with_updated_inputs(pda, oracle_mod):
     cfg = synth.Config("graphed", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
     a_in, b_in = synth.make_inputs(cfg, seed=30), synth.make_inputs(cfg, seed=31)
     dev = to_dev(a_in)
-    prep = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], partition_tokens=64)
+    prep = pda.PreparedDecode(dev["q"], dev["k_cache"], dev["block_tables"], partition_tokens=64, prefetch="off")
     g = pda.GraphedDecode(prep, dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"], dev["context_lens"],
                           dev["scale"])
     out = g.replay().clone()
