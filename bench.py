@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attention us/step & achieved HBM GB/s (prefetch on/off); tokens/s at 1-8 GPU"
-KERNEL_NAMES = {1: "paper_kernel", 2: "splitk_kernel", 3: "stream_kernel", 4: "balanced_kernel"}
+KERNEL_NAMES = {1: "paper_kernel", 2: "splitk_kernel", 3: "stream_kernel", 4: "balanced_kernel", 5: "tc_kernel"}
 
 
 L2_BYTES = 126 * 1024 * 1024  # B200 L2
@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--distance", type=int, default=None)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--partition", type=int, default=0)
-    ap.add_argument("--kernel", default=None, help="auto|splitk|balanced|stream|paper")
+    ap.add_argument("--kernel", default=None, help="auto|splitk|balanced|stream|paper|tc")
     ap.add_argument("--no-extras", action="store_true", help="skip ablation arms / e2e / cpu baseline")
     ap.add_argument("--fused-gather", action="store_true",
                     help="TP output all-gather inside the kernel's stores (symmetric memory) instead of NCCL")
@@ -423,7 +423,13 @@ def main():
                 "off": make_step(**{**opt_kw, "prefetch": "off"}),
                 "paper_on": make_step(kernel="paper", prefetch="bulk", prefetch_distance=4),
                 "paper_off": make_step(kernel="paper", prefetch="off"),
+                # the paper kernel as prefetch AUTO runs it on tiny steps: line d4, evict_last
+                "paper_line_el": make_step(kernel="paper", prefetch="line", prefetch_distance=4,
+                                           eviction="prefetch_last"),
             }
+            tc_ok = cfg.head_dim == 128 and getattr(local_cfg, "kv_dtype", "") != "e4m3"
+            if tc_ok:  # the tcgen05 kernel (decode_tc.cu) on the same step
+                arms["tc"] = make_step(kernel="tc", prefetch="off")
             per = {k: [] for k in arms}
             for k, fn in arms.items():  # warm each arm
                 fn(q, bt, lens, scale)
@@ -456,13 +462,22 @@ def main():
                     "prefetch_off_us": med["paper_off"],
                     "prefetch_speedup": med["paper_off"] / med["paper_on"],
                     "desc": "paper structure: grid [Hq,B], 4 warps, warp-per-block LDG, Alg. 1 bulk d=4",
+                    "line_d4_evict_last_us": med["paper_line_el"],
+                    "line_d4_evict_last_speedup": med["paper_off"] / med["paper_line_el"],
                 },
                 "arms_us": {k: spread(v) for k, v in us.items()},
                 "speedup_spread": {"line_d4": ratio("off", "on"), "bulk_d4": ratio("off", "bulk"),
-                                   "paper_bulk_d4": ratio("paper_off", "paper_on")},
+                                   "paper_bulk_d4": ratio("paper_off", "paper_on"),
+                                   "paper_line_d4_evict_last": ratio("paper_off", "paper_line_el")},
                 "arms_timing": f"{n_rep} interleaved rounds (A B C D E, A B C D E, ...), per-step CUDA events; "
                                f"medians, p10/p90; speedups = off/on paired per round",
             }
+            if "tc" in med:
+                extras["tc_kernel"] = {
+                    "us_per_step": med["tc"], "speedup_vs_default": med["off"] / med["tc"],
+                    "spread_us": spread(us["tc"]), "gbs": local_bytes / (med["tc"] * 1e3),
+                    "desc": "tcgen05 kernel: persistent CTA per SM, QK^T / PV on tcgen05.mma with S, O in TMEM "
+                            "(kernel='tc'; not the default: slower than split-K here)"}
             # FP8 (e4m3) KV-cache variant of the same step
             if cfg.head_dim == 128:
                 q8 = synth.quantize_kv_e4m3(inp)
