@@ -43,7 +43,7 @@ using namespace br;
 constexpr int kTcTile = 128;                      // tokens per tile = UMMA M of QK^T (thread = token)
 constexpr int kTcBlocks = kTcTile / kBlockSize;  // 16-token blocks per tile
 #ifndef PDA_TC_STAGES
-#define PDA_TC_STAGES 3  // 68 KiB stages: the ring takes 204 KiB of shared memory
+#define PDA_TC_STAGES 3  // K ring 3 x 36 KiB + V ring 3 x 32 KiB of shared memory
 #endif
 constexpr int kTcStages = PDA_TC_STAGES;
 constexpr int kTcNQ = 16;  // q rows per tile (the GQA group, padded; UMMA N of QK^T)
@@ -56,7 +56,11 @@ constexpr int kTcThreads = (kTcSoftWarps + 2) * 32;
 constexpr int kTcKBytes = 2 * kTcTile * 128;
 constexpr int kTcVBytes = kTcBlocks * 4096;        // one slab [chunk][16 tokens][128 B] per block
 constexpr int kTcQBytes = 2 * kTcNQ * 128;         // [chunk][16 rows][128 B]
-constexpr int kTcStageBytes = kTcKBytes + kTcVBytes + kTcQBytes;
+// Separate K and V rings (tile granular): a K stage (K tile + q rows) is free
+// as soon as QK^T has read it, a V stage only after PV -- so K runs ahead and
+// the V ring holds bytes in flight rather than bytes waiting for the softmax
+constexpr int kTcKStageBytes = kTcKBytes + kTcQBytes;
+constexpr int kTcRing = 16;  // tile descriptors / block rows in flight (K runs <= ~9 tiles ahead of PV)
 constexpr int kTcPBytes = kTcTile * 32 * 2;        // one P buffer: tile tokens x (16 hi + 16 lo) columns
 constexpr int kTcPSbo = (kTcTile / 8) * 128;       // P core-matrix stride between 8-column groups
 // TMEM: S of group 0 / 1 at columns [0,16) / [16,32); O^T of (group, segment parity) 32 columns each
@@ -74,10 +78,11 @@ struct TcTileInfo {
 };
 
 struct TcShared {
-    uint64_t full[kTcStages], empty[kTcStages];
+    uint64_t kfull[kTcStages], kempty[kTcStages], vfull[kTcStages], vempty[kTcStages];
     uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
     uint64_t o_full[2][2], o_free[2][2], st_ready[2][2];
-    TcTileInfo info[kTcStages];
+    TcTileInfo info[kTcRing];
+    int rows[kTcRing][kTcBlocks];  // cache row (phys * Hkv + kvh) * 16 of each block of a tile
     uint32_t tmem;
     int n_tiles;
     int n_segs, end_j;
@@ -90,7 +95,8 @@ struct TcShared {
     float st_m[2][2][2][kTcNQ], st_l[2][2][2][kTcNQ];
 };
 
-constexpr size_t kTcSmemBytes = 1024 + kTcStages * kTcStageBytes + 2 * kTcPBytes + sizeof(TcShared) + 64;
+constexpr size_t kTcSmemBytes =
+    1024 + kTcStages * (kTcKStageBytes + kTcVBytes) + 2 * kTcPBytes + sizeof(TcShared) + 64;
 
 // float -> uint key whose unsigned order is the float order (for redux.max)
 __device__ __forceinline__ uint32_t fkey(float x) {
@@ -114,8 +120,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     constexpr int NP = BF16 ? 32 : 16;  // P columns: hi (+ lo)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* stages = smem;
-    uint8_t* pbuf = smem + kTcStages * kTcStageBytes;
+    uint8_t* kst = smem;                                 // K stages [kTcStages][K tile | q rows]
+    uint8_t* vst = smem + kTcStages * kTcKStageBytes;    // V stages [kTcStages][8 slabs]
+    uint8_t* pbuf = vst + kTcStages * kTcVBytes;
     TcShared* sh = reinterpret_cast<TcShared*>(pbuf + 2 * kTcPBytes);  // P: one buffer per softmax group
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
@@ -145,8 +152,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             sh->end_j = rp.end_j;
             sh->start = rp.start;
             for (int s = 0; s < kTcStages; ++s) {
-                mbar_init(&sh->full[s], 1);
-                mbar_init(&sh->empty[s], 1);
+                mbar_init(&sh->kfull[s], 1);
+                // released by QK^T's commit AND by the softmax group having read the
+                // tile's info: the group waits kfull on the stage, which must not
+                // complete again (K of tile i + 3) before that wait -- parity aliasing
+                mbar_init(&sh->kempty[s], 2);
+                mbar_init(&sh->vfull[s], 1);
+                mbar_init(&sh->vempty[s], 1);
             }
             for (int s = 0; s < 2; ++s) {
                 mbar_init(&sh->s_full[s], 1);
@@ -187,57 +199,85 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         Cursor cur = sh->start;
         const int n_segs = sh->n_segs, end_j = sh->end_j;
         const bool starts_row = cur.j == 0;
-        int tile = 0;
         int wrow = -1, wbase = 0, w0 = 0;  // 32 block ids [wbase, wbase + 32) of row wrow
         int ouse[2][2] = {{0, 0}, {0, 0}}, suse[2][2] = {{0, 0}, {0, 0}};  // barrier use counts
-        for (int seg = 0; tile < n_tiles; ++seg) {
-            const int jend = seg == n_segs - 1 ? end_j : cur.n - 1;
-            const int kind = tc_kind(seg, n_segs, end_j, cur.n, starts_row);
-            const int32_t* btrow = p.bt + (size_t)cur.b * p.max_blocks;
-            const int t0 = tile, nt = (jend - cur.j + kTcBlocks) / kTcBlocks;  // this segment's tiles
-            const int ob = seg & 1;
+        // the current segment: blocks [j, jend] of row cur; tiles t0 .. t0 + nt - 1
+        int seg = 0, j = cur.j, jend = 0, kind = 0, t0 = 0, nt = 0, ob = 0, u0 = 0, u1 = 0, us = 0;
+        const int32_t* btrow = nullptr;
+        auto start_seg = [&](int first_tile) {
+            jend = seg == n_segs - 1 ? end_j : cur.n - 1;
+            kind = tc_kind(seg, n_segs, end_j, cur.n, starts_row);
+            btrow = p.bt + (size_t)cur.b * p.max_blocks;
+            t0 = first_tile;
+            nt = (jend - cur.j + kTcBlocks) / kTcBlocks;
+            ob = seg & 1;
             const int merger = (t0 + nt - 1) & 1;  // the group of the final tile merges both groups
             // use indices of this segment's O buffers / state handoff (see TcTileInfo)
-            const int u0 = ouse[0][ob], u1 = ouse[1][ob], us = suse[merger ^ 1][ob];
+            u0 = ouse[0][ob];
+            u1 = ouse[1][ob];
+            us = suse[merger ^ 1][ob];
             for (int gg = 0; gg < 2; ++gg)
                 if (nt >= 2 || (t0 & 1) == gg) ++ouse[gg][ob];
             if (nt >= 2) ++suse[merger ^ 1][ob];
-            for (int j = cur.j; j <= jend; j += kTcBlocks, ++tile) {
+        };
+        if (n_tiles > 0) start_seg(0);
+        // event loop: the next K tile when its K stage is free, the next V tile
+        // (never ahead of K) when its V stage is free
+        int nk = 0, nv = 0;
+        while (nv < n_tiles) {
+            if (nk < n_tiles &&
+                (nk < kTcStages || mbar_test(&sh->kempty[nk % kTcStages], ((nk / kTcStages) - 1) & 1))) {
+                if (j > jend) {  // next segment
+                    next_row(cur, p.lens, p.B, p.Hkv, max_tokens);
+                    ++seg;
+                    j = cur.j;
+                    start_seg(nk);
+                }
                 const int nblk = jend - j + 1 < kTcBlocks ? jend - j + 1 : kTcBlocks;
                 if (cur.b != wrow || j < wbase || j + nblk > wbase + 32) {  // refill the id window
                     wrow = cur.b;
                     wbase = j;
                     w0 = wbase + lane < p.max_blocks ? __ldg(btrow + wbase + lane) : 0;
                 }
-                const int st = tile % kTcStages;
-                if (tile >= kTcStages) mbar_wait(&sh->empty[st], ((tile / kTcStages) - 1) & 1);
-                uint8_t* sb = stages + st * kTcStageBytes;
+                const int st = nk % kTcStages, ri = nk % kTcRing;
+                uint8_t* sb = kst + st * kTcKStageBytes;
+                const int phys = __shfl_sync(kAllLanes, w0, (j - wbase + lane) & 31);
+                const int row = (phys * p.Hkv + cur.kvh) * kBlockSize;
+                if (lane < nblk) sh->rows[ri][lane] = row;
                 if (lane == 0) {
-                    TcTileInfo& in = sh->info[st];
+                    TcTileInfo& in = sh->info[ri];
                     in.b = cur.b;
                     in.kvh = cur.kvh;
                     in.j0 = j;
                     in.nblk = nblk;
                     in.L = cur.L;
-                    const int k = tile - t0;
+                    const int k = nk - t0;
                     in.flags = (k < 2 ? kFirstG : 0) | (k >= nt - 2 ? kLastG : 0) | (k == nt - 1 ? kFinal : 0) |
                                (nt >= 2 ? kBoth : 0) | (kind << 4) | (ob << 6);
                     in.ouse[0] = u0;
                     in.ouse[1] = u1;
                     in.suse = us;
-                    mbar_arrive_expect_tx(&sh->full[st], kTcQBytes + nblk * 8192);
-                    tma_load_3d(sb + kTcKBytes + kTcVBytes, &tmQ, 0, cur.b * p.Hq + cur.kvh * g, 0, &sh->full[st]);
+                    mbar_arrive_expect_tx(&sh->kfull[st], kTcQBytes + nblk * 4096);
+                    tma_load_3d(sb + kTcKBytes, &tmQ, 0, cur.b * p.Hq + cur.kvh * g, 0, &sh->kfull[st]);
                 }
                 __syncwarp();  // lane 0's expect_tx precedes every lane's copies
-                // lane b issues block b: K as one 4-D box, V as one 3-D box
-                const int phys = __shfl_sync(kAllLanes, w0, (j - wbase + lane) & 31);
-                if (lane < nblk) {
-                    const int row = (phys * p.Hkv + cur.kvh) * kBlockSize;
-                    tma_load_4d_hint(sb + lane * 4096, &tmK, 0, 0, 0, row >> 3, &sh->full[st], pol_first);
-                    tma_load_3d_hint(sb + kTcKBytes + lane * 4096, &tmV, 0, row, 0, &sh->full[st], pol_first);
-                }
+                // lane b issues block b's K as one 4-D box
+                if (lane < nblk) tma_load_4d_hint(sb + lane * 4096, &tmK, 0, 0, 0, row >> 3, &sh->kfull[st], pol_first);
+                j += kTcBlocks;
+                ++nk;
+                continue;
             }
-            if (tile < n_tiles) next_row(cur, p.lens, p.B, p.Hkv, max_tokens);
+            if (nv < nk && (nv < kTcStages || mbar_test(&sh->vempty[nv % kTcStages], ((nv / kTcStages) - 1) & 1))) {
+                const int st = nv % kTcStages, ri = nv % kTcRing;
+                __syncwarp();  // the ring entries this warp wrote
+                const int nblk = sh->info[ri].nblk;
+                const int row = lane < nblk ? sh->rows[ri][lane] : 0;
+                if (lane == 0) mbar_arrive_expect_tx(&sh->vfull[st], nblk * 4096);
+                __syncwarp();
+                if (lane < nblk)
+                    tma_load_3d_hint(vst + st * kTcVBytes + lane * 4096, &tmV, 0, row, 0, &sh->vfull[st], pol_first);
+                ++nv;
+            }
         }
     } else if (warp == kTcMmaWarp) {
         // ============================ MMA issuer ============================
@@ -247,8 +287,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint32_t pb = smem_u32(pbuf);
             auto pv = [&](int j) {
                 const int st = j % kTcStages, gj = j & 1;
-                const TcTileInfo in = sh->info[st];
+                const TcTileInfo in = sh->info[j % kTcRing];
                 mbar_wait(&sh->p_full[gj], (j >> 1) & 1);
+                mbar_wait(&sh->vfull[st], (j / kTcStages) & 1);
                 tc::fence_after();
                 const int ob = (in.flags >> 6) & 1;
                 const bool first = in.flags & kFirstG;
@@ -257,7 +298,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     mbar_wait(&sh->o_free[gj][ob], (use - 1) & 1);
                     tc::fence_after();
                 }
-                const uint32_t vb = smem_u32(stages + st * kTcStageBytes + kTcKBytes);
+                const uint32_t vb = smem_u32(vst + st * kTcVBytes);
                 for (int blk = 0; blk < in.nblk; ++blk) {
                     const uint64_t a = tc::smem_desc(vb + blk * 4096, 2048, 1024, tc::kLayoutSw128);
                     const uint64_t bd = tc::smem_desc(pb + gj * kTcPBytes + blk * 256, 128, kTcPSbo,
@@ -265,7 +306,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tc::mma_f16_ss(tm + tc_ocol(gj, ob), a, bd, idp, !(first && blk == 0));
                 }
                 tc::commit(&sh->p_free[gj]);
-                tc::commit(&sh->empty[st]);
+                tc::commit(&sh->vempty[st]);
                 if (in.flags & kLastG) tc::commit(&sh->o_full[gj][ob]);
             };
             // event loop: QK^T of tile i as soon as its data and its group's S
@@ -276,11 +317,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             while (j < n_tiles) {
                 if (i < n_tiles && i < j + 2) {
                     const int st = i % kTcStages, sb = i & 1;
-                    if (mbar_test(&sh->full[st], (i / kTcStages) & 1) &&
+                    if (mbar_test(&sh->kfull[st], (i / kTcStages) & 1) &&
                         (i < 2 || mbar_test(&sh->s_free[sb], ((i >> 1) - 1) & 1))) {
                         tc::fence_after();
-                        const uint32_t kb = smem_u32(stages + st * kTcStageBytes);
-                        const uint32_t qb = kb + kTcKBytes + kTcVBytes;
+                        const uint32_t kb = smem_u32(kst + st * kTcKStageBytes);
+                        const uint32_t qb = kb + kTcKBytes;
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
                             const uint64_t a =
@@ -290,6 +331,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             tc::mma_f16_ss(tm + 16 * sb, a, bd, idq, kk > 0);
                         }
                         tc::commit(&sh->s_full[sb]);
+                        tc::commit(&sh->kempty[st]);  // QK^T has read the K tile and q
                         ++i;
                         continue;
                     }
@@ -311,8 +353,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const float scale_log2 = p.scale_log2;
         for (int i = gr; i < n_tiles; i += 2) {
             const int st = i % kTcStages, it = i >> 1;
-            mbar_wait(&sh->full[st], (i / kTcStages) & 1);  // acquire the producer's tile info
-            const TcTileInfo in = sh->info[st];
+            mbar_wait(&sh->kfull[st], (i / kTcStages) & 1);  // acquire the producer's tile info
+            const TcTileInfo in = sh->info[i % kTcRing];
+            if (threadIdx.x % (kTcGroupWarps * 32) == 0) mbar_arrive(&sh->kempty[st]);
             mbar_wait(&sh->s_full[gr], it & 1);
             tc::fence_after();
             uint32_t r[16];
@@ -405,9 +448,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 *reinterpret_cast<uint4*>(prow + 2 * kTcPSbo) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                 *reinterpret_cast<uint4*>(prow + 3 * kTcPSbo) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
             }
-            if (!valid && t < in.nblk * kBlockSize) {
+            const bool zero_v = !valid && t < in.nblk * kBlockSize;
+            if (__any_sync(kAllLanes, zero_v)) mbar_wait(&sh->vfull[st], (i / kTcStages) & 1);  // V landed
+            if (zero_v) {
                 // a loaded token past the context end: zero its V row (0 * NaN would poison PV)
-                uint8_t* vrow = stages + st * kTcStageBytes + kTcKBytes + (t >> 4) * 4096 + (t & 15) * 128;
+                uint8_t* vrow = vst + st * kTcVBytes + (t >> 4) * 4096 + (t & 15) * 128;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     *reinterpret_cast<uint4*>(vrow + u * 16) = make_uint4(0, 0, 0, 0);
