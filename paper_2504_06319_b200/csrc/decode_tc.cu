@@ -310,12 +310,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (in.flags & kLastG) tc::commit(&sh->o_full[gj][ob]);
             };
             // event loop: QK^T of tile i as soon as its data and its group's S
-            // buffer are there (up to 2 tiles ahead of PV), PV of tile j as soon
+            // buffer are there (its group has read the previous S), PV of tile j as soon
             // as its group's P is written -- the two softmax groups never wait
             // for each other through this thread's program order
             int i = 0, j = 0;
             while (j < n_tiles) {
-                if (i < n_tiles && i < j + 2) {
+                if (i < n_tiles) {
                     const int st = i % kTcStages, sb = i & 1;
                     if (mbar_test(&sh->kfull[st], (i / kTcStages) & 1) &&
                         (i < 2 || mbar_test(&sh->s_free[sb], ((i >> 1) - 1) & 1))) {
