@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
         volatile int* done = misc->done;
         while (done[slot] < use) {
         }
+        __threadfence_block();  // acquire: the merge that freed this slot read it before its release
         float* acc_s = reinterpret_cast<float*>(slots + slot * Lay::kSlotBytes);
         float* m_s = reinterpret_cast<float*>(slots + slot * Lay::kSlotBytes + Lay::kSlotAcc);
         float* l_s = m_s + kConsumerWarps * NH;
