@@ -453,3 +453,28 @@ def test_prefetch_auto_policy():
     for kw in (dict(q_len=2), dict(kv_dtype=3, head_dim=128)):
         s = shape(**kw)
         assert pda.plan(s, opts(prefetch=3)) == pda.plan(s, opts(prefetch=0))
+
+
+def test_tc_and_tile_split_plans():
+    """kernel=tc: one persistent CTA per SM (grid = num_sms), 320 threads, the
+    balanced-style workspace; unsupported shapes are refused before launch.
+    Tile split: two-tile 16-bit steps whose grid is one wave at 2 CTAs/SM run
+    256-thread CTAs with an 8-stage ring; multi-wave, e4m3 or 4-stage grids
+    keep the 4-warp two-tile kernel."""
+    s = shape(num_q_heads=16, num_kv_heads=2, head_dim=128)
+    p = pda.plan(s, opts(kernel=5, prefetch=0))
+    assert (p["kernel"], p["grid_x"], p["grid_y"], p["grid_z"], p["threads"]) == (5, 148, 1, 1, 320)
+    assert pda.plan(s, opts(kernel=5, prefetch=0, num_sms=7))["grid_x"] == 7
+    assert p["workspace_bytes"] >= 148 * 2 * 8 * 128 * 4
+    for bad in (dict(head_dim=64), dict(q_len=2, head_dim=128), dict(kv_dtype=3, head_dim=128)):
+        assert pda.check_args(shape(**bad), opts(kernel=5, prefetch=0)) == 3
+    assert pda.check_args(shape(head_dim=128), opts(kernel=5, prefetch=0, smem_stages=8)) == 3
+    # g = 16: B=2 x 2 kv heads -> a one-wave grid at 2 CTAs/SM -> tile split
+    g16 = shape(num_q_heads=32, num_kv_heads=2, head_dim=128)
+    p = pda.plan(g16, opts(prefetch=0))
+    assert p["threads"] == 256 and p["smem_stages"] == 8
+    assert pda.plan(g16, opts(prefetch=0, smem_stages=4))["threads"] == 128
+    assert pda.plan(g16, opts(prefetch=0, issue_mode=1))["threads"] == 160   # producer-warp form
+    # many rows: more than one wave -> the two-tile kernel
+    big = shape(num_seqs=512, num_q_heads=32, num_kv_heads=2, head_dim=128, num_blocks=8192)
+    assert pda.plan(big, opts(prefetch=0))["threads"] == 128
