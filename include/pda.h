@@ -84,8 +84,9 @@ typedef enum {
     PDA_PF_LINE_L2 = 2, /* prefetch.global.L2 of every 128-byte line of each slab */
     PDA_PF_AUTO = 3     /* the planner decides where the paper's prefetch pays (measured on B200,
                            profiles/r02_prefetch_policy.jsonl): with kernel AUTO,
-                           a latency-bound tiny step (one query token, 16-bit KV, at most
-                           kAutoPaperBytes = 2 MiB of KV: B * max_blocks * Hkv * M_block * 2)
+                           a latency-bound tiny step (one query token, 16-bit KV, contexts of
+                           at most 512 tokens (max_blocks * 16) and at most 2 MiB of KV:
+                           B * max_blocks * Hkv * M_block * 2)
                            runs the paper-structure kernel with Alg. 1's line prefetch at
                            distance 4 and evict_last prefetches (eviction AUTO) -- 1.13-1.39x
                            over split-K there; every other step runs split-K without prefetch,

@@ -110,9 +110,14 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 // prefetch = AUTO with kernel = AUTO: latency-bound tiny steps run the
 // paper-structure kernel with Alg. 1's prefetch (include/pda.h PDA_PF_AUTO)
 constexpr double kAutoPaperBytes = 2097152.0;
+constexpr int64_t kAutoPaperMaxTokens = 512;
 bool auto_paper(const pda_shape* s, const pda_options* o) {
     if (o->kernel != PDA_KERNEL_AUTO || o->prefetch != PDA_PF_AUTO) return false;
     if (s->kv_dtype == PDA_E4M3 || q_tokens(s) > 1) return false;
+    // short contexts only: one CTA per (sequence, q head) walks the whole
+    // context serially (B=1, 4 heads, ctx 1024: 22.5 vs 14.4 us on split-K,
+    // profiles/r02_shape_scan.jsonl)
+    if ((int64_t)s->max_blocks_per_seq * s->block_size > kAutoPaperMaxTokens) return false;
     const double kv = 4.0 * s->num_seqs * (double)s->max_blocks_per_seq * s->block_size * s->num_kv_heads *
                       s->head_dim;
     return kv <= kAutoPaperBytes;

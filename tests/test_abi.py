@@ -448,8 +448,11 @@ def test_prefetch_auto_policy():
     # the 2 MiB boundary (upper bound B * max_blocks * 16 * Hkv * D * 2 B * 2)
     edge = shape(num_seqs=1, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=32, num_blocks=64)
     assert pda.plan(edge, opts(prefetch=3))["kernel"] == 1
-    over = shape(num_seqs=1, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=33, num_blocks=64)
+    over = shape(num_seqs=2, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=32, num_blocks=64)
     assert pda.plan(over, opts(prefetch=3)) == pda.plan(over, opts(prefetch=0))
+    # and the 512-token context bound (the paper kernel walks a whole context per CTA)
+    long_ctx = shape(num_seqs=1, num_kv_heads=4, num_q_heads=4, head_dim=128, max_blocks_per_seq=64, num_blocks=64)
+    assert pda.plan(long_ctx, opts(prefetch=3)) == pda.plan(long_ctx, opts(prefetch=0))
     for kw in (dict(q_len=2), dict(kv_dtype=3, head_dim=128)):
         s = shape(**kw)
         assert pda.plan(s, opts(prefetch=3)) == pda.plan(s, opts(prefetch=0))
