@@ -46,6 +46,10 @@ constexpr int kTcBlocks = kTcTile / kBlockSize;  // 16-token blocks per tile
 #define PDA_TC_STAGES 3  // K ring 3 x 36 KiB + V ring 3 x 32 KiB of shared memory
 #endif
 constexpr int kTcStages = PDA_TC_STAGES;
+#ifndef PDA_TC_STAMPS
+#define PDA_TC_STAMPS 0  // measurement builds only: per-tile clock64 stamps after the workspace
+#endif
+constexpr int kTcStampTiles = 64, kTcStampEvents = 8;
 constexpr int kTcNQ = 16;  // q rows per tile (the GQA group, padded; UMMA N of QK^T)
 constexpr int kTcGroupWarps = 4;                       // softmax warps per group (one per TMEM lane quarter)
 constexpr int kTcSoftWarps = 2 * kTcGroupWarps;        // two groups, alternating tiles
@@ -179,6 +183,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     tc::fence_after();
     const int n_tiles = sh->n_tiles;
+    // PDA_TC_STAMPS: [cta][tile][event] clock64 right after the seq_prefix region
+    unsigned long long* stamps = nullptr;
+    if constexpr (PDA_TC_STAMPS != 0)
+        stamps = reinterpret_cast<unsigned long long*>(p.seq_prefix + p.B + 1) + (size_t)c * kTcStampTiles * kTcStampEvents;
+    auto stamp = [&](int tile, int ev) {
+        if constexpr (PDA_TC_STAMPS != 0)
+            if (tile < kTcStampTiles) stamps[tile * kTcStampEvents + ev] = clock64();
+    };
     const uint32_t tm = sh->tmem;
 
     // context_len == 0 rows: zeros (reading R6), sequences strided over the grid
@@ -263,6 +275,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();  // lane 0's expect_tx precedes every lane's copies
                 // lane b issues block b's K as one 4-D box
                 if (lane < nblk) tma_load_4d_hint(sb + lane * 4096, &tmK, 0, 0, 0, row >> 3, &sh->kfull[st], pol_first);
+                if (lane == 0) stamp(nk, 0);  // K issued
                 j += kTcBlocks;
                 ++nk;
                 continue;
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 if (lane < nblk)
                     tma_load_3d_hint(vst + st * kTcVBytes + lane * 4096, &tmV, 0, row, 0, &sh->vfull[st], pol_first);
+                if (lane == 0) stamp(nv, 1);  // V issued
                 ++nv;
             }
         }
@@ -331,12 +345,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             tc::mma_f16_ss(tm + 16 * sb, a, bd, idq, kk > 0);
                         }
                         tc::commit(&sh->s_full[sb]);
+                        stamp(i, 2);  // QK^T issued
                         tc::commit(&sh->kempty[st]);  // QK^T has read the K tile and q
                         ++i;
                         continue;
                     }
                 }
                 if (j < i && mbar_test(&sh->p_full[j & 1], (j >> 1) & 1)) {
+                    stamp(j, 5);  // PV issued
                     pv(j);
                     ++j;
                 }
@@ -357,6 +373,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const TcTileInfo in = sh->info[i % kTcRing];
             if (threadIdx.x % (kTcGroupWarps * 32) == 0) mbar_arrive(&sh->kempty[st]);
             mbar_wait(&sh->s_full[gr], it & 1);
+            if (threadIdx.x % (kTcGroupWarps * 32) == 0) stamp(i, 3);  // S ready
             tc::fence_after();
             uint32_t r[16];
             tc::ld_32x32b_x16(tm + lane_base + 16 * gr, r);
@@ -463,6 +480,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sh->p_full[gr]);
+            if (threadIdx.x % (kTcGroupWarps * 32) == 0) stamp(i, 4);  // P written
 
             if (in.flags & kLastG) {
                 // ---- S7: this group's share of the segment: (m, l) per column
@@ -585,6 +603,9 @@ cudaError_t launch_tc_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const 
 size_t tc_smem_bytes() { return kTcSmemBytes; }
 
 int tc_threads() { return kTcThreads; }
+size_t tc_stamp_bytes(int grid) {
+    return PDA_TC_STAMPS ? (size_t)grid * kTcStampTiles * kTcStampEvents * 8 + 256 : 0;
+}
 
 cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUtensorMap& tmQ,
                       const BalancedParams& p, bool bf16, int grid, cudaStream_t stream) {

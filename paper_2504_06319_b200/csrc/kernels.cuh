@@ -188,6 +188,7 @@ cudaError_t launch_tc(const CUtensorMap& tmK, const CUtensorMap& tmV, const CUte
                       const BalancedParams& p, bool bf16, int grid, cudaStream_t stream);
 size_t tc_smem_bytes();
 int tc_threads();
+size_t tc_stamp_bytes(int grid);  // 0 unless built with PDA_TC_STAMPS (measurement builds)
 
 cudaError_t launch_combine(const CombineParams& p, int head_dim, cudaStream_t stream);
 

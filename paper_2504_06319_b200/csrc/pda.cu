@@ -227,7 +227,7 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         pl->trace_records = 0;
         const size_t gx = (size_t)pl->grid_x;
         pl->workspace_bytes = align256(gx * 2 * nh * D * 4) + align256(gx * 2 * nh * 4) +
-                              align256(((size_t)B + 1) * 8);
+                              align256(((size_t)B + 1) * 8) + pda::tc_stamp_bytes(pl->grid_x);
         return PDA_OK;
     }
     if (o->kernel == PDA_KERNEL_BALANCED) {
