@@ -423,7 +423,7 @@ def main():
                 "off": make_step(**{**opt_kw, "prefetch": "off"}),
                 "paper_on": make_step(kernel="paper", prefetch="bulk", prefetch_distance=4),
                 "paper_off": make_step(kernel="paper", prefetch="off"),
-                # the paper kernel as prefetch AUTO runs it on tiny steps: line d4, evict_last
+                # the paper kernel as prefetch AUTO runs it on short GQA steps: line d4, evict_last
                 "paper_line_el": make_step(kernel="paper", prefetch="line", prefetch_distance=4,
                                            eviction="prefetch_last"),
             }

@@ -82,13 +82,13 @@ typedef enum {
     PDA_PF_OFF = 0,     /* no prefetch: the ablation baseline */
     PDA_PF_BULK_L2 = 1, /* cp.async.bulk.prefetch.L2 of each K and V slab (one instruction per slab) */
     PDA_PF_LINE_L2 = 2, /* prefetch.global.L2 of every 128-byte line of each slab */
-    PDA_PF_AUTO = 3     /* the planner decides where the paper's prefetch pays (measured on B200,
-                           profiles/r02_prefetch_policy.jsonl): with kernel AUTO,
-                           a latency-bound tiny step (one query token, 16-bit KV, contexts of
-                           at most 512 tokens (max_blocks * 16) and at most 2 MiB of KV:
-                           B * max_blocks * Hkv * M_block * 2)
-                           runs the paper-structure kernel with Alg. 1's line prefetch at
-                           distance 4 and evict_last prefetches (eviction AUTO) -- 1.13-1.39x
+    PDA_PF_AUTO = 3     /* the planner decides where the paper's structure and prefetch pay
+                           (measured on B200): with kernel AUTO, a short-context
+                           step (one query token, 16-bit KV, contexts of at most 512 tokens)
+                           with GQA groups of >= 4 and 128 <= B * Hq <= 512 q-head rows
+                           (<= 256 at contexts above 256 tokens) runs the paper-structure
+                           kernel -- one CTA per q-head row -- with Alg. 1's line prefetch at
+                           distance 4 and evict_last prefetches (eviction AUTO): 1.12-1.52x
                            over split-K there; every other step runs split-K without prefetch,
                            where no prefetch variant was ever faster (p10 of the paired speedup
                            < 1 on all cells).  prefetch_distance is ignored.  A step that fuses

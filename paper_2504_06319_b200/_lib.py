@@ -28,7 +28,7 @@ KERNEL = {"auto": 0, "paper": 1, "splitk": 2, "stream": 3, "balanced": 4, "tc": 
 # computed, so the extra L2 prefetch (the paper's instruction, or per-line) is
 # measured 0-9 % slower on every cell with self-issuing consumers -> off by
 # default; "line" / "bulk" with a distance remain the ablation switch.
-DEFAULT_PREFETCH = "auto"  # planner: the paper kernel + Alg. 1 prefetch on tiny steps, else off (pda.h)
+DEFAULT_PREFETCH = "auto"  # planner: the paper kernel + Alg. 1 prefetch on short GQA steps, else off (pda.h)
 DEFAULT_DISTANCE = 4
 
 

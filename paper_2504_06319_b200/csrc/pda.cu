@@ -107,20 +107,24 @@ bool self_issue(const pda_shape* s, const pda_options* o) {
 // multi-wave (combine kernel, not a cluster merge) although it would fit one
 // wave at 4/SM.  The split sizes and thresholds below were measured with this
 // convention.
-// prefetch = AUTO with kernel = AUTO: latency-bound tiny steps run the
-// paper-structure kernel with Alg. 1's prefetch (include/pda.h PDA_PF_AUTO)
-constexpr double kAutoPaperBytes = 2097152.0;
+// prefetch = AUTO with kernel = AUTO: short-context steps whose q-head rows
+// (B * Hq, one CTA each in the paper's grid) fill the chip better than
+// split-K's (sequence, kv head) units run the paper-structure kernel with
+// Alg. 1's prefetch.  Measured band (105 uniform cells, ctx 128-512, 30
+// interleaved rounds each, profiles/r02_short_ctx.jsonl): GQA groups >= 4 with
+// 128 <= B * Hq <= 512 (<= 256 at ctx 512) gain 1.12-1.52x over split-K
+// (e.g. B=8, 32/8 heads, ctx 256: 12.3 vs 16.4 us); below the band the two
+// tie within the 2 us event resolution, above it the paper grid is 0.3-0.9x
+// (every CTA walks a whole context); MHA is mixed and stays on split-K.
 constexpr int64_t kAutoPaperMaxTokens = 512;
 bool auto_paper(const pda_shape* s, const pda_options* o) {
     if (o->kernel != PDA_KERNEL_AUTO || o->prefetch != PDA_PF_AUTO) return false;
     if (s->kv_dtype == PDA_E4M3 || q_tokens(s) > 1) return false;
-    // short contexts only: one CTA per (sequence, q head) walks the whole
-    // context serially (B=1, 4 heads, ctx 1024: 22.5 vs 14.4 us on split-K,
-    // profiles/r02_shape_scan.jsonl)
-    if ((int64_t)s->max_blocks_per_seq * s->block_size > kAutoPaperMaxTokens) return false;
-    const double kv = 4.0 * s->num_seqs * (double)s->max_blocks_per_seq * s->block_size * s->num_kv_heads *
-                      s->head_dim;
-    return kv <= kAutoPaperBytes;
+    const int64_t max_tokens = (int64_t)s->max_blocks_per_seq * s->block_size;
+    if (max_tokens > kAutoPaperMaxTokens) return false;
+    if (s->num_q_heads / s->num_kv_heads < 4) return false;
+    const int64_t rows = (int64_t)s->num_seqs * s->num_q_heads;
+    return rows >= 128 && rows <= (max_tokens <= 256 ? 512 : 256);
 }
 
 int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {

@@ -432,30 +432,31 @@ def test_planner_invariants(B, g, hkv, D, max_blocks, q_len, kv8, dt):
 
 
 def test_prefetch_auto_policy():
-    """PDA_PF_AUTO (include/pda.h): with kernel AUTO a latency-bound tiny step
-    (16-bit, one query token, <= 2 MiB of KV) plans the paper-structure kernel
-    (its prefetch evict_last under eviction AUTO) and reports split-K's
-    workspace, which the same call needs with a fused append / gather; larger,
-    e4m3 or multi-token steps plan split-K exactly as with prefetch off."""
-    tiny = shape()  # 2 x 256 tokens x 2 kv heads x D 64 x 2 B x (K+V) = 256 KiB
-    p = pda.plan(tiny, opts(prefetch=3, eviction=4))
-    ref = pda.plan(tiny, opts(prefetch=0, eviction=4, kernel=2))
+    """PDA_PF_AUTO (include/pda.h): with kernel AUTO a short-context step
+    (16-bit, one query token, <= 512 tokens) with GQA groups >= 4 and
+    128 <= B * Hq <= 512 (<= 256 above 256 tokens) plans the paper-structure
+    kernel (its prefetch evict_last under eviction AUTO) and reports split-K's
+    workspace, which the same call needs with a fused append / gather; every
+    other step plans split-K exactly as with prefetch off."""
+    def sh(B, hq, hkv, ctx, **kw):
+        return shape(num_seqs=B, num_q_heads=hq, num_kv_heads=hkv, head_dim=128, max_blocks_per_seq=ctx // 16,
+                     num_blocks=B * ctx // 16, **kw)
+    band = sh(8, 32, 8, 256)  # B * Hq = 256, g = 4, ctx 256
+    p = pda.plan(band, opts(prefetch=3, eviction=4))
+    ref = pda.plan(band, opts(prefetch=0, eviction=4, kernel=2))
     assert p["kernel"] == 1 and p["eviction"] == 2
     assert p["workspace_bytes"] == ref["workspace_bytes"]
     # explicit prefetch or an explicit kernel: no policy
-    assert pda.plan(tiny, opts(prefetch=2, eviction=4))["kernel"] == 2
-    assert pda.plan(tiny, opts(prefetch=3, kernel=2))["kernel"] == 2
-    # the 2 MiB boundary (upper bound B * max_blocks * 16 * Hkv * D * 2 B * 2)
-    edge = shape(num_seqs=1, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=32, num_blocks=64)
-    assert pda.plan(edge, opts(prefetch=3))["kernel"] == 1
-    over = shape(num_seqs=2, num_kv_heads=8, num_q_heads=32, head_dim=128, max_blocks_per_seq=32, num_blocks=64)
-    assert pda.plan(over, opts(prefetch=3)) == pda.plan(over, opts(prefetch=0))
-    # and the 512-token context bound (the paper kernel walks a whole context per CTA)
-    long_ctx = shape(num_seqs=1, num_kv_heads=4, num_q_heads=4, head_dim=128, max_blocks_per_seq=64, num_blocks=64)
-    assert pda.plan(long_ctx, opts(prefetch=3)) == pda.plan(long_ctx, opts(prefetch=0))
-    for kw in (dict(q_len=2), dict(kv_dtype=3, head_dim=128)):
-        s = shape(**kw)
-        assert pda.plan(s, opts(prefetch=3)) == pda.plan(s, opts(prefetch=0))
+    assert pda.plan(band, opts(prefetch=2, eviction=4))["kernel"] == 2
+    assert pda.plan(band, opts(prefetch=3, kernel=2))["kernel"] == 2
+    # the band's edges
+    assert pda.plan(sh(4, 32, 8, 256), opts(prefetch=3))["kernel"] == 1      # 128 rows
+    assert pda.plan(sh(16, 32, 8, 256), opts(prefetch=3))["kernel"] == 1     # 512 rows
+    assert pda.plan(sh(8, 32, 8, 512), opts(prefetch=3))["kernel"] == 1      # 256 rows at ctx 512
+    for off in (sh(2, 32, 8, 256), sh(32, 32, 8, 256), sh(16, 32, 8, 512), sh(8, 32, 8, 528),
+                sh(8, 32, 32, 256), sh(8, 32, 16, 256), sh(8, 32, 8, 256, q_len=2),
+                sh(8, 32, 8, 256, kv_dtype=3)):
+        assert pda.plan(off, opts(prefetch=3)) == pda.plan(off, opts(prefetch=0))
 
 
 def test_tc_and_tile_split_plans():

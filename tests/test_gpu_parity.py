@@ -849,11 +849,11 @@ def test_fuzz_parity_vs_oracle(pda, oracle_mod, case):
 
 
 def test_prefetch_auto_policy_vs_oracle(pda, oracle_mod):
-    """The library default (prefetch AUTO): latency-bound tiny steps run the
-    paper-structure kernel with Alg. 1's line prefetch and
-    evict_last prefetches; larger steps split-K.  Every row against
-    the fp64 oracle, and the tiny step with a fused KV append / output gather
-    (which keep split-K) too."""
+    """The library default (prefetch AUTO): short-context GQA steps in the
+    measured band run the paper-structure kernel with Alg. 1's line prefetch
+     and evict_last prefetches; other steps split-K.  Every
+    row against the fp64 oracle, and a band step with a fused output gather
+    (which keeps split-K) too."""
     for cfg in SHAPES:
         inp = synth.make_inputs(cfg, seed=21)
         dev = to_dev(inp)
@@ -861,14 +861,18 @@ def test_prefetch_auto_policy_vs_oracle(pda, oracle_mod):
                                          dev["context_lens"], dev["scale"])
         torch.cuda.synchronize()
         assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL, cfg.name
-    # C1 is tiny: the plan is the paper kernel, and it matches the explicit call bit for bit
-    inp = synth.make_inputs(synth.C1_TINY, seed=22)
+    # a band step (B * Hq = 128, g = 4, ragged <= 256 tokens): the plan is the paper
+    # kernel, and it matches the explicit call bit for bit
+    band = synth.Config("auto_band", 8, 16, 4, 128, (256, 17, 200, 1, 64, 0, 255, 129), "bf16", poison_blocks=2)
+    inp = synth.make_inputs(band, seed=22)
     dev = to_dev(inp)
     a = pda.paged_decode_attention(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
                                    dev["context_lens"], dev["scale"])
     b = gpu(pda, dev, kernel="paper", prefetch="line", prefetch_distance=4, eviction="prefetch_last")
     torch.cuda.synchronize()
+    assert pda.plan(pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"]), pda.make_options())["kernel"] == 1
     assert torch.equal(a, b)
+    assert max_err(a, oracle_out(oracle_mod, inp)) <= TOL
     # gather with the default options: split-K underneath, every row vs the oracle
     peers = [torch.zeros_like(dev["q"]) for _ in range(2)]
     pda.paged_decode_attention_gather(dev["q"], dev["k_cache"], dev["v_cache"], dev["block_tables"],
