@@ -358,9 +358,13 @@ def main():
 
     step_spread = {}
 
-    def time_steps(fn, steps, warmup, join=None, key=None):
+    def time_steps(fn, steps, warmup, join=None, key=None, join_end=None):
         """Mean device ms per step over `steps` timed steps (max over ranks); with
-        `key`, the per-step spread (median / p10 / p90, us) is kept in step_spread."""
+        `key`, the per-step spread (median / p10 / p90, us) is kept in step_spread.
+        join: multi-stream steps, the timer's stream waits for all of them after
+        every step; join_end: only once, after the last step (a pipelined loop:
+        step k's side-stream copies overlap step k + 1's kernels; the span still
+        ends after every copy of every step)."""
         for _ in range(warmup):
             fn(q, bt, lens, scale)
         if join:
@@ -375,8 +379,8 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 fn(q, bt, lens, scale)
-                if join:
-                    join(stream)
+                if join or join_end:  # individually timed (flushed) steps: every step's copies inside
+                    (join or join_end)(stream)
                 e1.record(stream)
                 spans.append((e0, e1))
             torch.cuda.synchronize()
@@ -392,6 +396,8 @@ def main():
                 fn(q, bt, lens, scale)
                 if join:
                     join(stream)  # multi-stream steps: the timer's stream waits for all of them
+                if join_end and i == steps - 1:
+                    join_end(stream)
                 ev[i + 1].record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -605,12 +611,13 @@ def main():
 
         def e2e_step(*_):
             host(qh, bth, lh, scale)
-        e2e_ms = time_steps(e2e_step, max(10, args.steps // 2), 2, join=host.join)
+        e2e_ms = time_steps(e2e_step, max(10, args.steps // 2), 2, join_end=host.join)
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": host.h2d_bytes(),
                "d2h_bytes_per_step": host.d2h_bytes(),
                "path": "pda_decode_step_host (H2D q/bt/lens from pinned memory, kernels, D2H out), "
-                       "2 staging slots, copies on per-slot copy streams overlapping the previous step's kernels; kernels in order on one stream"}
+                       "2 staging slots, copies on per-slot copy streams overlapping the neighbouring steps' kernels; "
+                       "kernels in order on one stream; the timed span ends after the last step's D2H"}
     elif not args.no_extras:
         # N > 1: the TP step end to end -- this rank's q slice, the tables and the
         # lengths from pinned host memory, the kernels, the output all-gather
