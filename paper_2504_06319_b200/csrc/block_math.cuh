@@ -120,7 +120,9 @@ __device__ __forceinline__ void prefetch_kv_slabs(const uint16_t* k, const uint1
 // rows in that order so that its V^T fragments come straight from a
 // transposing byte ldmatrix, see BlockMathKV8); the contraction over tokens
 // is order-free, only the masks need the mapping.
-template <bool BF16, int D, int NT, bool TOKPERM = false>
+// MS = 2 (D split): this warp accumulates only output rows d in
+// [16 i0, 16 i0 + D / 2) of O^T; QK^T and the softmax are computed in full.
+template <bool BF16, int D, int NT, bool TOKPERM = false, int MS = 1>
 struct BlockMath {
     // rows m = 2c + e -> token 4c + e, rows 8 + 2c + e -> token 4c + 2 + e
     static __device__ __forceinline__ int tok_of_row(int m) {
@@ -129,10 +131,12 @@ struct BlockMath {
 
     static constexpr int KSTEPS = D / 16;
     static constexpr int MT = D / 16;
+    static constexpr int MTL = MT / MS;               // m-tiles of O^T this warp accumulates
     static constexpr int kSlab = kBlockSize * D * 2;  // Eq. 1
 
     uint32_t qf[KSTEPS][NT][2];  // Q as the B operand of S^T = K Q^T (register-resident)
-    float acc[MT][NT][4];        // O^T accumulators: (d = 16i + lane/4 + 8(r/2), h = 2(lane%4) + r%2)
+    float acc[MTL][NT][4];       // O^T accumulators: (d = 16(i0 + i) + lane/4 + 8(r/2), h = 2(lane%4) + r%2)
+    int i0 = 0;                  // first m-tile (D split)
     float m_run[NT][2];          // running max per head column (log2 domain)
     float l_run[NT][2];          // per-lane partial row sums (reduced at the end)
     // multi-token decode: column (query token i, head) of this lane may see
@@ -142,7 +146,7 @@ struct BlockMath {
 
     __device__ __forceinline__ void reset() {
 #pragma unroll
-        for (int i = 0; i < MT; ++i)
+        for (int i = 0; i < MTL; ++i)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -289,7 +293,7 @@ struct BlockMath {
                 pr[c + 2] = ex2(s[nt][c + 2] - m_ref);
                 l_run[nt][c] = l_run[nt][c] * alpha + pr[c] + pr[c + 2];
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
+                for (int i = 0; i < MTL; ++i) {
                     acc[i][nt][c] *= alpha;
                     acc[i][nt][c + 2] *= alpha;
                 }
@@ -326,9 +330,9 @@ struct BlockMath {
         const int v_t = (lane & 7) + (lane >> 4) * 8;
         const int v_c = ((lane >> 3) & 1) * 8;
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
+        for (int i = 0; i < MTL; ++i) {
             uint32_t a[4];
-            ldsm_x4_trans(vbase + swz(v_t, i * 16 + v_c), a[0], a[1], a[2], a[3]);
+            ldsm_x4_trans(vbase + swz(v_t, (i0 + i) * 16 + v_c), a[0], a[1], a[2], a[3]);
             if (TAIL && valid < kBlockSize) mask_v(a, valid, lane);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {

@@ -131,16 +131,16 @@ int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
     return (n_tiles > 1 && s->kv_dtype != PDA_E4M3 && !self_issue(s, o)) ? 2 : 3;
 }
 
-// Two-head-tile 16-bit steps (g = 16, or q_len * g > 8) whose grid of `units`
-// CTAs is one wave at 2 CTAs/SM run the tile-split kernel (8 consumer warps,
-// one head tile each; splitk_impl.cuh TS): B=128 32/2 ctx 8k 170 vs 174 us,
+// 16-bit steps whose grid of `units` CTAs is one wave at 2 CTAs/SM run the
+// split kernel (8 consumer warps, two per block; splitk_impl.cuh TS): with
+// two head tiles (g = 16, or q_len * g > 8) one tile each, with one tile one
+// half of the output rows d each (D split).  Two tiles: B=128 32/2 ctx 8k 170 vs 174 us,
 // B=32 57.3 vs 61.4, B=16 ctx 32k 94.2 vs 98.3, B=64 64/4 170 vs 172; grids of
 // more waves keep the 4-warp kernel at 3 CTAs/SM (B=256 ctx 4k 203 vs 195, C5
 // with 2 query tokens 2408 vs 2399; profiles/r02_ab_ts.log).  Ring 8 or 12.
 // PDA_TILE_SPLIT=0 / 1 forces it off / on (A/B measurements only).
 bool tile_split(const pda_shape* s, const pda_options* o, int64_t units, int sms, int stages) {
     if (s->kv_dtype == PDA_E4M3 || !self_issue(s, o)) return false;
-    if (q_tokens(s) * (s->num_q_heads / s->num_kv_heads) <= 8) return false;
     if (stages != 8 && stages != 12) return false;
     static const char* env = std::getenv("PDA_TILE_SPLIT");
     if (env) return std::atoi(env) != 0;

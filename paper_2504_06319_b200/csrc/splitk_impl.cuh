@@ -46,22 +46,23 @@ struct Geometry {
     static constexpr int kChunks = kSlab / 2048;          // boxes per slab
 };
 
-template <bool BF16, int D, int NT, bool KV8>
+template <bool BF16, int D, int NT, bool KV8, int MS = 1>
 struct MathFor {
-    using type = BlockMath<BF16, D, NT>;
+    using type = BlockMath<BF16, D, NT, false, MS>;
 };
-template <bool BF16, int D, int NT>
-struct MathFor<BF16, D, NT, true> {
+template <bool BF16, int D, int NT, int MS>
+struct MathFor<BF16, D, NT, true, MS> {
     using type = BlockMathKV8<BF16, NT>;
 };
 
 // Self-issue mode (always for e4m3 caches): no producer warp -- each consumer
 // warp refills the ring stages it owns (4 issuers instead of 1; the 2 KiB e4m3
 // slabs need twice the issue rate of the 16-bit path).
-// Tile split (TS, two head tiles, 16-bit): 8 consumer warps, warp w computes
-// head tile w / 4 of the blocks j = w (mod 4); the two warps of a block share
-// its ring stage and the second to finish it refills it.  Half the math per
-// warp and twice the warps of the two-tile kernel, at 2 CTAs/SM.
+// Split (TS, 16-bit): 8 consumer warps, the two warps w and w + 4 share the
+// blocks j = w (mod 4) -- with two head tiles each computes one tile; with
+// one tile (D split) both compute S and P and each accumulates half of the
+// output rows d of O^T.  The second warp to finish a block refills its stage.
+// Less math per warp and twice the warps, at 2 CTAs/SM.
 template <bool SELF, bool TS = false>
 constexpr int splitk_block_threads() { return TS ? 2 * kConsumerWarps * 32 : (kConsumerWarps + (SELF ? 0 : 1)) * 32; }
 
@@ -88,13 +89,14 @@ template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF, b
 __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_blocks<KV8, STAGES, NT, SELF, TS>())
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
-    static_assert(!TS || (SELF && !KV8 && NT == 2), "tile split: two 16-bit head tiles, self-issue");
+    static_assert(!TS || (SELF && !KV8), "split: 16-bit, self-issue");
     constexpr bool TRACE = MODE == 1;
     const bool clustered = MODE != 0 && p.cluster > 1;
     using G = Geometry<D, KV8>;
-    constexpr int NTW = TS ? 1 : NT;                       // head tiles per warp
+    constexpr bool DSPLIT = TS && NT == 1;                 // D split (else head-tile split)
+    constexpr int NTW = TS && !DSPLIT ? 1 : NT;            // head tiles per warp
     constexpr int NW = TS ? 2 * kConsumerWarps : kConsumerWarps;  // consumer warps
-    using BM = typename MathFor<BF16, D, NTW, KV8>::type;
+    using BM = typename MathFor<BF16, D, NTW, KV8, DSPLIT ? 2 : 1>::type;
     constexpr int NH = 8 * NT;  // padded heads per CTA
     constexpr int MT = D / 16;  // m-tiles of O^T
 
@@ -117,9 +119,11 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
 
     const int part = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
     const int lane = threadIdx.x & 31;
-    // TS: warp = block slot (mod 4), tile = head tile; else tile 0
+    // TS: warp = block slot (mod 4), sub = which of its two warps; sub is the
+    // head tile (two tiles) or the half of d (D split)
     const int warp = TS ? (threadIdx.x >> 5) & (kConsumerWarps - 1) : threadIdx.x >> 5;
-    const int tile = TS ? threadIdx.x >> 7 : 0;
+    const int sub = TS ? threadIdx.x >> 7 : 0;
+    const int tile = DSPLIT ? 0 : sub;
     const int g = p.g;
 
     // PDL: everything this grid reads may come from the previous grid in the
@@ -312,6 +316,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
 
     // ============================== consumer warps ==============================
     BM bm;
+    if constexpr (DSPLIT) bm.i0 = sub * (MT / 2);
     bm.set_q_tokens(p.q_len, g, lane, 8 * tile);
     bm.load_q_tokens(p.q, b, kvh, p.Hq, p.q_len, g, lane, 8 * tile);
     bm.reset();
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                 ++npf;
             }
         };
-        for (int pos = PAIR * warp; tile == 0 && pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
+        for (int pos = PAIR * warp; sub == 0 && pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
             if (pos >= jn0 && pos <= jn1) write_new(pos);
             issue(pos);
             if (PAIR == 2 && pos + 1 < n) {
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                 else
                     bm.template block<false>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
             }
-            if (tile == 0) mine += two ? 2 : 1;
+            if (sub == 0) mine += two ? 2 : 1;
             // our ldmatrix reads of the stages are complete (their registers fed the
             // MMAs above); order them before the async-proxy refills
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
     const int r0 = lane >> 2;
     const int t0 = 2 * (lane & 3);
     asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // ring reads done
-    if (lane < 4) {
+    if (lane < 4 && !(DSPLIT && sub == 1)) {  // (D split: both halves hold the same m, l)
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
@@ -475,12 +480,12 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
             }
     }
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < BM::MTL; ++i)
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const int dd = BM::dcol(i, lane, r);
+                const int dd = BM::dcol(i, lane, r) + 16 * bm.i0;
                 const int h = (tile + nt) * 8 + t0 + (r & 1);
                 merge_acc[(warp * NH + h) * (D + 4) + dd] = bm.acc[i][nt][r];
             }
@@ -569,11 +574,11 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
 template <bool BF16, int D, int NT, int MODE, bool SELF>
 cudaError_t dispatch_stages(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                             int stages, dim3 grid, cudaStream_t s) {
-    if constexpr (NT == 2 && SELF) {
+    if constexpr (SELF) {
         if (p.tile_split) {
             switch (stages) {
-                case 8: return launch_one<BF16, D, 2, 8, MODE, false, true, true>(tmK, tmV, p, grid, s);
-                case 12: return launch_one<BF16, D, 2, 12, MODE, false, true, true>(tmK, tmV, p, grid, s);
+                case 8: return launch_one<BF16, D, NT, 8, MODE, false, true, true>(tmK, tmV, p, grid, s);
+                case 12: return launch_one<BF16, D, NT, 12, MODE, false, true, true>(tmK, tmV, p, grid, s);
                 default: return cudaErrorInvalidValue;
             }
         }
