@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         continue;
                     }
                 }
-                if (j < i && mbar_test(&sh->p_full[j & 1], (j >> 1) & 1)) {
+                // PV only once its V tile has landed too: a blocking wait here
+                // would stall QK^T of later tiles behind the V stream
+                if (j < i && mbar_test(&sh->p_full[j & 1], (j >> 1) & 1) &&
+                    mbar_test(&sh->vfull[j % kTcStages], (j / kTcStages) & 1)) {
                     stamp(j, 5);  // PV issued
                     pv(j);
                     ++j;

@@ -926,3 +926,58 @@ def test_tc_kernel_rescale_paths(pda, oracle_mod):
         out = gpu(pda, dev, kernel="tc")
         torch.cuda.synchronize()
         assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL, kind
+
+
+def _score_pattern(inp, kind):
+    """Set k[..., 0] (with q = e_0) so that the log2-domain score of token t
+    follows `kind`: ramp (+0.2 per token: the running max rises on every
+    block, by 3.2 per block), steep (+1 per token: by 16 per block), descend
+    (the first block holds the max), step (a plateau 12 units higher from the
+    middle on: one late jump), needle (one token 60 above the rest)."""
+    q, k = inp["q"], inp["k_cache"]
+    q[:] = 0
+    q[..., 0] = 1.0
+    unit = 1.0 / inp["scale"] / 1.4426950408889634
+    bt = inp["block_tables"]
+    for b, L in enumerate(inp["cfg"].context_lens):
+        for tok in range(L):
+            v = {"ramp": 0.2 * tok, "steep": 1.0 * tok, "descend": -0.1 * tok,
+                 "step": 12.0 if tok >= L // 2 else 0.0, "needle": 60.0 if tok == L - 3 else 0.0}[kind]
+            k[bt[b, tok // 16], :, tok % 16, 0] = v * unit
+
+
+RESCALE_CFGS = [synth.Config("rs_g8", 2, 8, 1, 128, (1500, 700), "bf16"),
+             synth.Config("rs_mha", 2, 4, 4, 128, (900, 333), "fp16")]
+
+
+@pytest.mark.parametrize("cfg", RESCALE_CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("kind", ["ramp", "steep", "descend", "step", "needle"])
+@pytest.mark.parametrize("kw", [dict(), dict(num_sms=1), dict(partition_tokens=256), dict(kernel="balanced"),
+                                dict(kernel="stream")],
+                         ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
+def test_softmax_rescale_patterns_vs_oracle(pda, oracle_mod, cfg, kind, kw):
+    """Online-softmax rescale paths (S5): score patterns whose running max
+    rises on every block, once late, or never after the first block, through
+    the split kernel (default plan, one wave), the 4-warp kernel (num_sms=1:
+    a multi-wave plan), a fixed partition, the balanced and the stream
+    kernels, all vs the fp64 oracle."""
+    inp = synth.make_inputs(cfg, seed=11)
+    _score_pattern(inp, kind)
+    out = gpu(pda, to_dev(inp), **kw)
+    assert max_err(out, oracle_out(oracle_mod, inp)) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["ramp", "steep", "descend", "step", "needle"])
+@pytest.mark.parametrize("kw", [dict(), dict(smem_stages=16, partition_tokens=256), dict(smem_stages=12)],
+                         ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()) or "default")
+def test_softmax_rescale_patterns_kv8_vs_oracle(pda, oracle_mod, kind, kw):
+    """Same patterns through the e4m3 path (one-block and paired-block
+    softmax), K scale chosen so the pattern fits e4m3's range."""
+    cfg = synth.Config("rs_kv8", 2, 8, 2, 128, (1500, 700), "fp16")
+    inp = synth.make_inputs(cfg, seed=12)
+    _score_pattern(inp, kind)
+    kf = inp["k_cache"].float()
+    kmax = float(kf[kf.isfinite()].abs().max())  # poison blocks hold NaN
+    inp = kv8(inp, ks=kmax / 400.0)  # code = k / ks <= 400 < 448
+    out = gpu_kv8(pda, to_dev(inp), **kw)
+    assert max_err(out, oracle_kv8(oracle_mod, inp)) <= TOL
