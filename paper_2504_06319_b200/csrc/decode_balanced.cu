@@ -44,11 +44,14 @@ struct BGeom {
 
 // Per-CTA shared state written by S0 and the segment slots' bookkeeping.
 struct BMisc {
+    // per slot: parked[] completes when all consumer warps have parked their
+    // state for the slot's current segment (the merger waits on it: acquire),
+    // freed[] when the merger has read the slot out (the next users wait on it)
+    uint64_t parked[2], freed[2];
     long long T, k0, k1;
     int Ge, n_segs, end_j, pad0;
     Cursor start;
-    int arrive[2];          // warps parked in the slot for its current segment
-    int done[2];            // segments merged out of the slot so far
+    int arrive[2];          // warps parked in the slot for its current segment (elects the merger)
     long long slot_row[2];  // first output row (b * Hq + kvh * g) of the slot's segment
     int slot_kind[2];       // 0: whole row -> out, 1: partial -> workspace slot 0, 2: slot 1
 };
@@ -102,7 +105,11 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
             misc->n_segs = rp.n_segs;
             misc->end_j = rp.end_j;
             misc->start = rp.start;
-            for (int s = 0; s < 2; ++s) misc->arrive[s] = misc->done[s] = 0;
+            for (int s = 0; s < 2; ++s) {
+                misc->arrive[s] = 0;
+                mbar_init(&misc->parked[s], kConsumerWarps * 32);  // every consumer thread
+                mbar_init(&misc->freed[s], 32);                    // the merging warp's threads
+            }
             for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
             fence_barrier_init();
         }
@@ -197,10 +204,7 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
     auto park = [&](int s, bool mine, const Cursor& row) {
         const int slot = s % Lay::kSlots;
         const int use = s / Lay::kSlots;
-        volatile int* done = misc->done;
-        while (done[slot] < use) {
-        }
-        __threadfence_block();  // acquire: the merge that freed this slot read it before its release
+        if (use > 0) mbar_wait(&misc->freed[slot], (use - 1) & 1);  // the previous merge read the slot out
         float* acc_s = reinterpret_cast<float*>(slots + slot * Lay::kSlotBytes);
         float* m_s = reinterpret_cast<float*>(slots + slot * Lay::kSlotBytes + Lay::kSlotAcc);
         float* l_s = m_s + kConsumerWarps * NH;
@@ -237,13 +241,16 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
             m_s[warp * NH + lane] = -INFINITY;  // no block of this segment was this warp's
             l_s[warp * NH + lane] = 0.f;
         }
-        __threadfence_block();
+        mbar_arrive(&misc->parked[slot]);  // release: this thread's slot writes
         __syncwarp();
         int last = 0;
         if (lane == 0) last = atomicAdd(&misc->arrive[slot], 1) == kConsumerWarps - 1;
         last = __shfl_sync(kFullMask, last, 0);
         if (!last) return;
-        __threadfence_block();
+        // the last warp to count itself merges; every thread arrived on
+        // parked[] before its warp's atomicAdd, so this wait returns at once --
+        // it is the acquire
+        mbar_wait(&misc->parked[slot], use & 1);
         const long long row0 = misc->slot_row[slot];
         const int kind = misc->slot_kind[slot];
         for (int idx = lane; idx < g * D; idx += 32) {
@@ -269,11 +276,8 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
             }
         }
         __syncwarp();
-        if (lane == 0) {
-            misc->arrive[slot] = 0;
-            __threadfence_block();
-            atomicAdd(&misc->done[slot], 1);
-        }
+        if (lane == 0) misc->arrive[slot] = 0;
+        mbar_arrive(&misc->freed[slot]);  // release: this thread's reads above (lane 0: the reset)
     };
 
     Cursor cc = start;
