@@ -129,6 +129,7 @@ struct BlockMath {
         return TOKPERM ? 4 * ((m & 7) >> 1) + (m & 1) + ((m >> 3) << 1) : m;
     }
 
+    static constexpr int kNT = NT;
     static constexpr int KSTEPS = D / 16;
     static constexpr int MT = D / 16;
     static constexpr int MTL = MT / MS;               // m-tiles of O^T this warp accumulates
@@ -217,6 +218,15 @@ struct BlockMath {
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk(kbase, lane, s, s2);
+        finish<TAIL>(s, s2, vbase, vq, scale_log2, lane);
+    }
+
+    // S5 + S6 of a block whose scores qk() produced earlier: the split-K
+    // consumers issue the QK^T of their next block before this one's softmax
+    // and PV (two independent dependency chains in flight per warp).
+    template <bool TAIL = true>
+    __device__ __forceinline__ void finish(float (&s)[NT][4], const float (&s2)[NT][4], uint32_t vbase, int vq,
+                                           float scale_log2, int lane) {
         uint32_t pb[NT][2], pb_lo[NT][2];
         softmax<TAIL>(s, s2, vq, scale_log2, lane, pb, pb_lo);
         pv<TAIL>(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb, pb_lo);
@@ -475,14 +485,25 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
         }
     }
 
+    // the split-K consumers' software pipeline calls qk() / finish() / finish2()
+    __device__ __forceinline__ void qk(uint32_t kbase, int lane, float (&s)[NT][4], float (&s2)[NT][4]) {
+        qk8(kbase, lane, s, s2);
+    }
+
+    template <bool TAIL = true>
+    __device__ __forceinline__ void finish(float (&s)[NT][4], const float (&s2)[NT][4], uint32_t vbase, int vq,
+                                           float scale_log2, int lane) {
+        uint32_t pb[NT][2], pb_lo[NT][2];
+        this->template softmax<TAIL>(s, s2, vq, scale_log2, lane, pb, pb_lo);
+        pv8<TAIL>(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb);
+    }
+
     template <bool TAIL = true>
     __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
         qk8(kbase, lane, s, s2);
-        uint32_t pb[NT][2], pb_lo[NT][2];
-        this->template softmax<TAIL>(s, s2, vq, scale_log2, lane, pb, pb_lo);
-        pv8<TAIL>(vbase, vq < kBlockSize ? vq : kBlockSize, lane, pb);
+        finish<TAIL>(s, s2, vbase, vq, scale_log2, lane);
     }
 
     // Two blocks (32 tokens) per step: independent QK chains, ONE online-softmax
@@ -494,6 +515,14 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
         float sa[NT][4], sa2[NT][4], sb[NT][4], sb2[NT][4];
         qk8(kb0, lane, sa, sa2);
         qk8(kb1, lane, sb, sb2);
+        finish2<TAIL>(sa, sa2, sb, sb2, vb0, vq0, vb1, vq1, scale_log2, lane);
+    }
+
+    // S5 + S6 of a block pair whose scores qk() produced earlier
+    template <bool TAIL = true>
+    __device__ __forceinline__ void finish2(float (&sa)[NT][4], const float (&sa2)[NT][4], float (&sb)[NT][4],
+                                            const float (&sb2)[NT][4], uint32_t vb0, int vq0, uint32_t vb1,
+                                            int vq1, float scale_log2, int lane) {
         uint32_t pa[NT][2], pbb[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)

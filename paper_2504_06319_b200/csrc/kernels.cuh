@@ -32,6 +32,16 @@ constexpr int kConsumerWarps = 4;  // split-K kernel consumer warps
 // 16-bit D = 128 slabs (two 128-byte column chunks) load as ONE 3-D TMA box
 // per slab (K and V: 2 UTMALDG per block instead of 4); 0 = two 2-D boxes
 constexpr bool kTma3d = PDA_TMA3D != 0;
+#ifndef PDA_SWP
+#define PDA_SWP 0
+#endif
+// split-K self-issue consumers: QK^T of a warp's next block(s) is issued
+// before the softmax / PV of the current one (software pipeline across
+// blocks); 0 (default) = one block's QK^T -> softmax -> PV chain at a time.
+// Measured 2-26 % slower (profiles/r02_ab_swp.log): the next block's stage was
+// refilled only one iteration earlier, so waiting for it before the current
+// softmax halves the ring's lookahead per warp (even from L2).
+constexpr bool kSwp = PDA_SWP != 0;
 constexpr int kPaperWarps = 4;     // paper kernel: 128 threads = 4 warps (Table 2)
 
 enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };

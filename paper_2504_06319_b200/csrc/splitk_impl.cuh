@@ -384,11 +384,35 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
         for (int j = jn0 > STAGES ? jn0 : STAGES; j <= jn1; ++j)
             if ((j / PAIR) % kConsumerWarps == warp && !TS) write_new(j);  // (TS: no fused append)
         int mine = 0;
-        for (int j = PAIR * warp; j < n; j += PAIR * kConsumerWarps) {
+        // Software pipeline (kSwp): the scores of the warp's next block(s) are
+        // computed before the softmax / PV of the current ones, so two
+        // independent chains (next QK^T, current softmax -> PV) interleave in
+        // the warp's instruction stream.  Needs the next block's stage to be a
+        // different one from the current (ring depth >= 2 strides); one head
+        // tile per warp only (the two-tile kernels would spill at 3 CTAs/SM).
+        constexpr int STRIDE = PAIR * kConsumerWarps;
+        constexpr bool SWP = kSwp && STAGES >= 2 * STRIDE && BM::kNT == 1;  // (two tiles: spills)
+        float ca[BM::kNT][4], ca2[BM::kNT][4], cb[BM::kNT][4], cb2[BM::kNT][4];  // current block(s)
+        float na[BM::kNT][4], na2[BM::kNT][4], nb[BM::kNT][4], nb2[BM::kNT][4];  // next block(s)
+        auto scores = [&](int jj, float (&xa)[BM::kNT][4], float (&xa2)[BM::kNT][4], float (&xb)[BM::kNT][4],
+                          float (&xb2)[BM::kNT][4]) {  // wait for block(s) jj (, jj + 1) and run QK^T
+            const bool two = PAIR == 2 && jj + 1 < n;
+            mbar_wait(&full[jj % STAGES], (jj / STAGES) & 1);
+            bm.qk(smem_u32(ring + (jj % STAGES) * G::kStage), lane, xa, xa2);
+            if (two) {
+                mbar_wait(&full[(jj + 1) % STAGES], ((jj + 1) / STAGES) & 1);
+                bm.qk(smem_u32(ring + ((jj + 1) % STAGES) * G::kStage), lane, xb, xb2);
+            }
+        };
+        if (SWP && PAIR * warp < n) scores(PAIR * warp, ca, ca2, cb, cb2);
+        for (int j = PAIR * warp; j < n; j += STRIDE) {
             const bool two = PAIR == 2 && j + 1 < n;
             const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
-            mbar_wait(&full[st0], (j / STAGES) & 1);
-            if (two) mbar_wait(&full[st1], ((j + 1) / STAGES) & 1);
+            if (SWP) {
+                if (j + STRIDE < n) scores(j + STRIDE, na, na2, nb, nb2);
+            } else {
+                scores(j, ca, ca2, cb, cb2);
+            }
             const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
             const int v0 = L - (sb + j) * kBlockSize;  // tokens of the context from this block on
             // masking only where a context / causal limit falls inside the block(s):
@@ -397,19 +421,32 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                 if (two) {
                     const int v1 = L - (sb + j + 1) * kBlockSize;
                     if (bm.needs_mask(v1))
-                        bm.template block2<true>(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2,
-                                                 lane);
+                        bm.template finish2<true>(ca, ca2, cb, cb2, kb0 + G::kSlab, v0, kb1 + G::kSlab, v1,
+                                                  p.scale_log2, lane);
                     else
-                        bm.template block2<false>(kb0, kb0 + G::kSlab, v0, kb1, kb1 + G::kSlab, v1, p.scale_log2,
-                                                  lane);
+                        bm.template finish2<false>(ca, ca2, cb, cb2, kb0 + G::kSlab, v0, kb1 + G::kSlab, v1,
+                                                   p.scale_log2, lane);
                 } else {
-                    bm.template block<true>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                    bm.template finish<true>(ca, ca2, kb0 + G::kSlab, v0, p.scale_log2, lane);
                 }
             } else {
                 if (bm.needs_mask(v0))
-                    bm.template block<true>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                    bm.template finish<true>(ca, ca2, kb0 + G::kSlab, v0, p.scale_log2, lane);
                 else
-                    bm.template block<false>(kb0, kb0 + G::kSlab, v0, p.scale_log2, lane);
+                    bm.template finish<false>(ca, ca2, kb0 + G::kSlab, v0, p.scale_log2, lane);
+            }
+            if (SWP) {
+#pragma unroll
+                for (int nt = 0; nt < BM::kNT; ++nt)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        ca[nt][r] = na[nt][r];
+                        ca2[nt][r] = na2[nt][r];
+                        if constexpr (PAIR == 2) {
+                            cb[nt][r] = nb[nt][r];
+                            cb2[nt][r] = nb2[nt][r];
+                        }
+                    }
             }
             if (sub == 0) mine += two ? 2 : 1;
             // our ldmatrix reads of the stages are complete (their registers fed the
