@@ -96,6 +96,8 @@ struct SplitKParams {
                        // (seq, kv head) row) that merge their partials through DSMEM
     int pdl;           // launched with programmatic stream serialization (PDL)
     int tile_split;    // two head tiles on 8 consumer warps, one tile each (16-bit, self-issue)
+    int* query_clusters;  // host-side planner query, not a launch: when set, launch_splitk_m2
+                          // stores cudaOccupancyMaxActiveClusters of the kernel it would launch
 };
 
 struct PaperParams {

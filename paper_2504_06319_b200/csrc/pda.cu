@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "../../include/pda.h"
@@ -145,6 +146,47 @@ bool tile_split(const pda_shape* s, const pda_options* o, int64_t units, int sms
     static const char* env = std::getenv("PDA_TILE_SPLIT");
     if (env) return std::atoi(env) != 0;
     return units <= 2 * (int64_t)sms;
+}
+
+// Can all n_clusters clusters of `cluster` CTAs of the chosen split-K kernel
+// be resident at once?  Asked of the current device
+// (cudaOccupancyMaxActiveClusters, cached per configuration): clusters are
+// placed per GPC, so a count of CTA slots can say "one wave" when it is not --
+// 296 CTAs in clusters of 4 at 2 CTAs/SM on 148 SMs ran as two waves (150 vs
+// 104 us with the combine kernel).  Planning for an assumed SM
+// count (num_sms given) or without a device: the slot count decides.
+bool clusters_fit(const pda_shape* s, const pda_options* o, int n_tiles, int stages, bool ts, int cluster,
+                  int64_t n_clusters) {
+    if (o->num_sms != 0) return true;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    const bool kv8 = s->kv_dtype == PDA_E4M3, self = self_issue(s, o);
+    const int64_t key = ((((((((int64_t)dev * 2 + (s->dtype == PDA_BF16)) * 256 + s->head_dim) * 4 + n_tiles) * 32 +
+                           stages) * 2 + kv8) * 2 + self) * 2 + ts) * 32 + cluster;
+    static std::mutex mu;
+    static std::map<int64_t, int> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second <= 0 || n_clusters <= it->second;
+    }
+    pda::SplitKParams p{};
+    int n = 0;
+    p.cluster = cluster;
+    p.tile_split = ts;
+    p.query_clusters = &n;
+    CUtensorMap none{};
+    if (pda::launch_splitk_m2(none, none, p, s->dtype == PDA_BF16, s->head_dim, n_tiles, stages, dim3(cluster, 1, 1),
+                              nullptr, kv8, self) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;  // unknown: the slot count decides
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = n;
+    return n <= 0 || n_clusters <= n;
 }
 
 pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
@@ -346,9 +388,12 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
     // partner (B=16-64, ctx 4k: 14-15 % slower) -- DESIGN.md 7.
     if (p_max > 1 && o->merge != 1) {
         if (o->merge == 2 && p_max > kMaxCluster) return PDA_ERR_UNSUPPORTED;
-        const int64_t conc = (int64_t)sms * splitk_ctas_per_sm(s, o, n_tiles);
+        const int64_t conc = (int64_t)sms * (ts ? 2 : splitk_ctas_per_sm(s, o, n_tiles));
         const bool one_wave = (int64_t)B * Hkv * p_max <= conc;
-        if (o->merge == 2 || (p_max <= kAutoMaxCluster && one_wave)) pl->cluster = (int32_t)p_max;
+        if (o->merge == 2 ||
+            (p_max <= kAutoMaxCluster && one_wave &&
+             clusters_fit(s, o, n_tiles, stages, ts, (int)p_max, (int64_t)B * Hkv)))
+            pl->cluster = (int32_t)p_max;
     }
     const size_t rows = (size_t)B * q_tokens(s) * Hq;
     pl->workspace_bytes = p_max > 1 && pl->cluster == 0

@@ -579,6 +579,23 @@ cudaError_t launch_one(const CUtensorMap& tmK, const CUtensorMap& tmV, const Spl
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
+    if (MODE == 2 && p.query_clusters != nullptr) {
+        // planner query: how many clusters of p.cluster CTAs of this kernel can be
+        // resident at once (GPC placement included -- a count of CTA slots is not
+        // enough: 296 CTAs in clusters of 4 on 148 SMs at 2 CTAs/SM do not all fit)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)p.cluster, 1, 1);
+        cfg.blockDim = dim3(splitk_block_threads<SELF, TS>(), 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)p.cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaOccupancyMaxActiveClusters(p.query_clusters, kern, &cfg);
+    }
     if (p.cluster > 1 || p.pdl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;

@@ -981,3 +981,23 @@ def test_softmax_rescale_patterns_kv8_vs_oracle(pda, oracle_mod, kind, kw):
     inp = kv8(inp, ks=kmax / 400.0)  # code = k / ks <= 400 < 448
     out = gpu_kv8(pda, to_dev(inp), **kw)
     assert max_err(out, oracle_kv8(oracle_mod, inp)) <= TOL
+
+
+@pytest.mark.parametrize("B,ctx,p_max,cluster", [
+    (74, 16384, 4, 0),   # 296 CTAs (2/SM, tile split) in clusters of 4: not all resident -> combine
+    (128, 8192, 2, 2),   # 256 CTAs in clusters of 2: resident -> cluster merge
+    (32, 32768, 8, 8),   # 256 CTAs in clusters of 8
+])
+def test_planner_clusters_only_when_resident(pda, B, ctx, p_max, cluster):
+    """The auto cluster merge (S8 over DSMEM) asks the device whether every
+    (seq, kv head) cluster fits at once (cudaOccupancyMaxActiveClusters): a
+    CTA-slot count said one wave for 296 CTAs in clusters of 4 on 148 SMs,
+    which ran as two waves (150 vs 104 us with the combine kernel)."""
+    from paper_2504_06319_b200 import _lib
+    s = _lib.Shape(num_seqs=B, num_q_heads=8, num_kv_heads=1, head_dim=128, block_size=16, num_blocks=100000,
+                   max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1, kv_dtype=1, q_len=1)
+    o = _lib.Options(prefetch=0, prefetch_distance=0, partition_tokens=0, smem_stages=0, kernel=2, num_sms=0,
+                     stream_warps=0, eviction=0, issue_mode=0, k_scale=0.0, v_scale=0.0, merge=0)
+    p = pda.plan(s, o)
+    assert (p["p_max"], p["cluster"]) == (p_max, cluster)
+    assert (p["workspace_bytes"] > 0) == (cluster == 0)
