@@ -391,11 +391,14 @@ __device__ __forceinline__ void cvt_e4m3x4(uint32_t w, uint32_t& lo, uint32_t& h
         : "r"(w));
 }
 
-template <bool Q_BF16, int NT>
-struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
-    using Base = BlockMath<false, 128, NT, true>;
+// MS = 2 (D split): this warp accumulates output rows d in [16 i0, 16 i0 + 64)
+// only (PV converts and multiplies half of V); QK^T and the softmax in full.
+template <bool Q_BF16, int NT, int MS = 1>
+struct BlockMathKV8 : BlockMath<false, 128, NT, true, MS> {
+    using Base = BlockMath<false, 128, NT, true, MS>;
     static constexpr int D = 128;
     static constexpr int MT = D / 16;
+    static constexpr int MTL = MT / MS;  // m-tiles of O^T this warp accumulates
     static constexpr int kSlab = kBlockSize * D;  // 1 byte per element
 
     // Q B fragments: qf[2j + half][nt] = Q[col][32j + 16 half + 4(lane%4) + {0,1 | 2,3}],
@@ -468,8 +471,10 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
     __device__ __forceinline__ void pv8(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2]) {
         const int vr = lane & 15;
 #pragma unroll
-        for (int ip = 0; ip < MT / 2; ++ip) {
-            const int unit = 2 * ip + (lane >> 4);  // 16 d columns per matrix: tiles 2 ip, 2 ip + 1
+        for (int ip = 0; ip < MTL / 2; ++ip) {
+            // 16 d columns per matrix: tiles 2 gp, 2 gp + 1 (gp: this warp's first
+            // tile pair i0 / 2 on, D split)
+            const int unit = 2 * (ip + this->i0 / 2) + (lane >> 4);
             uint32_t r[4];
             ldsm_x2_trans_b8(vbase + vr * 128 + ((unit ^ (vr & 7)) << 4), r[0], r[1], r[2], r[3]);
 #pragma unroll
@@ -554,7 +559,7 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true> {
                 prb[c + 2] = ex2(sb[nt][c + 2] - m_ref);
                 this->l_run[nt][c] = this->l_run[nt][c] * alpha + (pra[c] + pra[c + 2]) + (prb[c] + prb[c + 2]);
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
+                for (int i = 0; i < MTL; ++i) {
                     this->acc[i][nt][c] *= alpha;
                     this->acc[i][nt][c + 2] *= alpha;
                 }

@@ -141,7 +141,13 @@ int splitk_ctas_per_sm(const pda_shape* s, const pda_options* o, int n_tiles) {
 // with 2 query tokens 2408 vs 2399; profiles/r02_ab_ts.log).  Ring 8 or 12.
 // PDA_TILE_SPLIT=0 / 1 forces it off / on (A/B measurements only).
 bool tile_split(const pda_shape* s, const pda_options* o, int64_t units, int sms, int stages) {
-    if (s->kv_dtype == PDA_E4M3 || !self_issue(s, o)) return false;
+    if (!self_issue(s, o)) return false;
+    if (s->kv_dtype == PDA_E4M3) {
+        // e4m3 D split (16 / 24 stages, one head tile): A/B switch only
+        static const char* kv8 = std::getenv("PDA_TILE_SPLIT_KV8");
+        return kv8 && std::atoi(kv8) != 0 && (stages == 16 || stages == 24) &&
+               q_tokens(s) * (s->num_q_heads / s->num_kv_heads) <= 8;
+    }
     if (stages != 8 && stages != 12) return false;
     static const char* env = std::getenv("PDA_TILE_SPLIT");
     if (env) return std::atoi(env) != 0;
@@ -368,9 +374,10 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         const int64_t units = (int64_t)B * Hkv * p_max;
         if (units > (int64_t)sms * 3 && units <= (int64_t)sms * 4 * 2) stages = 4;
     }
+    const bool kv8 = s->kv_dtype == PDA_E4M3;
     const bool ts = tile_split(s, o, (int64_t)B * Hkv * p_max, sms,
-                               o->smem_stages ? stages : kDefaultTileSplitStages);
-    if (ts && o->smem_stages == 0) stages = kDefaultTileSplitStages;
+                               o->smem_stages || kv8 ? stages : kDefaultTileSplitStages);
+    if (ts && o->smem_stages == 0 && !kv8) stages = kDefaultTileSplitStages;
     pl->kernel = PDA_KERNEL_SPLITK;
     pl->partition_tokens = (int32_t)(P < max_tokens ? P : ceil_div(max_tokens, s->block_size) * s->block_size);
     pl->p_max = (int32_t)p_max;

@@ -52,7 +52,7 @@ struct MathFor {
 };
 template <bool BF16, int D, int NT, int MS>
 struct MathFor<BF16, D, NT, true, MS> {
-    using type = BlockMathKV8<BF16, NT>;
+    using type = BlockMathKV8<BF16, NT, MS>;
 };
 
 // Self-issue mode (always for e4m3 caches): no producer warp -- each consumer
@@ -89,7 +89,8 @@ template <bool BF16, int D, int NT, int STAGES, int MODE, bool KV8, bool SELF, b
 __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_blocks<KV8, STAGES, NT, SELF, TS>())
     splitk_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const SplitKParams p) {
-    static_assert(!TS || (SELF && !KV8), "split: 16-bit, self-issue");
+    static_assert(!TS || SELF, "split: self-issue");
+    static_assert(!TS || !KV8 || NT == 1, "e4m3 split: D split only");
     constexpr bool TRACE = MODE == 1;
     const bool clustered = MODE != 0 && p.cluster > 1;
     using G = Geometry<D, KV8>;
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                     if (old & 1) {
                         __threadfence_block();
                         issue(j + STAGES);
+                        if (two && j + 1 + STAGES < n) issue(j + 1 + STAGES);  // (e4m3 pairs: st0 counts both)
                     }
                 }
             } else {
@@ -649,6 +651,15 @@ template <bool BF16, int NT, int MODE>
 cudaError_t dispatch_stages_kv8(const CUtensorMap& tmK, const CUtensorMap& tmV, const SplitKParams& p,
                                 int stages, dim3 grid, cudaStream_t s) {
     // 4 KiB stages, consumed in pairs (depth a multiple of 8) or singly (12)
+    if constexpr (NT == 1) {
+        if (p.tile_split) {  // D split: 8 consumer warps, two per block pair, 2 CTAs/SM
+            switch (stages) {
+                case 16: return launch_one<BF16, 128, 1, 16, MODE, true, true, true>(tmK, tmV, p, grid, s);
+                case 24: return launch_one<BF16, 128, 1, 24, MODE, true, true, true>(tmK, tmV, p, grid, s);
+                default: return cudaErrorInvalidValue;
+            }
+        }
+    }
     switch (stages) {
         case 8: return launch_one<BF16, 128, NT, 8, MODE, true, true>(tmK, tmV, p, grid, s);
         case 12: return launch_one<BF16, 128, NT, 12, MODE, true, true>(tmK, tmV, p, grid, s);
