@@ -32,21 +32,48 @@ namespace pda {
 namespace {
 
 // S8: out = sum_p 2^(lse_p - M) o_p / sum_p 2^(lse_p - M), partitions in fixed order.
+// One warp per output row.  Every load is issued before any result is needed
+// -- the sequence length, the row's lse (lane i: partition i) and the first
+// kPre partials' o -- so the row costs one memory round trip instead of three
+// dependent ones (lens -> lse -> o); entries at or past the row's partition
+// count are loaded but never used (they may hold anything).  The arithmetic
+// (w_p = 2^(lse_p - M), den and acc accumulated in partition order) is the
+// cluster merge's, so the two stay bitwise equal.
 template <int D>
 __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
     constexpr int PER = D / 32;
+    constexpr int kPre = 8;
     pdl_wait();  // the partials come from the split-K grid before this one
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= p.B * p.q_len * p.Hq) return;
     const int b = row / (p.q_len * p.Hq);
+    const float* lse = p.ws_lse + (size_t)row * p.p_max;
+    const float* o_base = p.ws_o + (size_t)row * p.p_max * D + lane * PER;
     int L = p.lens[b];
+    const float lse_l = lane < p.p_max ? lse[lane] : -INFINITY;
+    float pre[kPre][PER];
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+        if (q < p.p_max) {
+            if constexpr (PER == 4) {
+                const float4 x = *reinterpret_cast<const float4*>(o_base + (size_t)q * D);
+                pre[q][0] = x.x;
+                pre[q][1] = x.y;
+                pre[q][2] = x.z;
+                pre[q][3] = x.w;
+            } else {
+                const float2 x = *reinterpret_cast<const float2*>(o_base + (size_t)q * D);
+                pre[q][0] = x.x;
+                pre[q][1] = x.y;
+            }
+        }
+    }
     L = L < p.max_tokens ? L : p.max_tokens;
     const int n_parts = (L + p.part_tokens - 1) / p.part_tokens;
     if (n_parts <= 1) return;  // written by the main kernel
-    const float* lse = p.ws_lse + (size_t)row * p.p_max;
-    float M = -INFINITY;
-    for (int i = lane; i < n_parts; i += 32) M = fmaxf(M, lse[i]);
+    float M = lane < n_parts ? lse_l : -INFINITY;
+    for (int i = 32 + lane; i < n_parts; i += 32) M = fmaxf(M, lse[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
     if (M == -INFINITY) M = 0.f;  // every partition empty for this column
@@ -54,10 +81,18 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineParams p) {
 #pragma unroll
     for (int e = 0; e < PER; ++e) accv[e] = 0.f;
     float den = 0.f;
-    const float* o_base = p.ws_o + (size_t)row * p.p_max * D + lane * PER;
-#pragma unroll 4
-    for (int part = 0; part < n_parts; ++part) {
-        const float w = ex2(lse[part] - M);
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+        const float lq = __shfl_sync(kFull, lse_l, q);
+        if (q < n_parts) {
+            const float w = ex2(lq - M);
+            den += w;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) accv[e] += w * pre[q][e];
+        }
+    }
+    for (int part = kPre; part < n_parts; ++part) {
+        const float w = ex2((part < 32 ? __shfl_sync(kFull, lse_l, part) : lse[part]) - M);
         den += w;
         const float* op = o_base + (size_t)part * D;
         if constexpr (PER == 4) {
