@@ -131,6 +131,18 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
     // stream (q, the tables, the appended KV): wait before the first load
     pdl_wait();
     const int max_tokens = p.max_blocks * kBlockSize;
+    // S1 ahead of S0: this partition's first 64 block ids are loaded alongside
+    // the sequence length (its start part * P does not depend on it), so the
+    // first TMA issue waits for one global round trip, not two.  Ids past the
+    // unit's end are never used.
+    int pre_w0 = 0, pre_w1 = 0;
+    if constexpr (SELF) {
+        const int sb0 = part * p.part_tokens / kBlockSize;  // < max_blocks: part < p_max
+        const int32_t* bt0 = p.bt + (size_t)b * p.max_blocks + sb0;
+        const int lane0 = threadIdx.x & 31, lim = p.max_blocks - sb0;
+        pre_w0 = lane0 < lim ? __ldg(bt0 + lane0) : 0;
+        pre_w1 = 32 + lane0 < lim ? __ldg(bt0 + 32 + lane0) : 0;
+    }
     int L = p.lens[b];
     L = L < max_tokens ? L : max_tokens;
     const int P = p.part_tokens;
@@ -337,8 +349,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
             prefetch_tmap(&tmV);
         }
         int wbase = 0;  // block-id window [wbase, wbase + 64) of this unit, 2 ids per lane
-        int w0 = lane < n ? btrow[lane] : 0;
-        int w1 = 32 + lane < n ? btrow[32 + lane] : 0;
+        int w0 = pre_w0, w1 = pre_w1;  // loaded at entry (sb == part * P here: the unit is not empty)
         int npf = 0;
         auto id_at = [&](int pos) {
             const int o = pos - wbase;

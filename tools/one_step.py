@@ -14,7 +14,7 @@ from bench import workload_config
 
 cfg = workload_config(sys.argv[1])
 kw = eval(sys.argv[2]) if len(sys.argv) > 2 else {}
-inp = synth.make_inputs(cfg, seed=1234, device="cuda")
+inp = synth.make_inputs(cfg, seed=1234, device="cuda", shuffle=os.environ.get("PSWEEP_CONTIGUOUS") != "1")
 if len(sys.argv) > 3 and sys.argv[3] == "kv8":
     inp = synth.quantize_kv_e4m3(inp)
     kw.update(k_scale=inp["k_scale"], v_scale=inp["v_scale"])
