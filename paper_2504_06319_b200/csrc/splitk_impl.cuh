@@ -129,6 +129,15 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
 
     // PDL: everything this grid reads may come from the previous grid in the
     // stream (q, the tables, the appended KV): wait before the first load
+    if constexpr (SELF) {
+        // the tensor maps are kernel parameters (not produced by a previous
+        // grid): fetch the descriptors before anything else, so the first TMA
+        // issue does not wait for them
+        if (threadIdx.x == 0) {
+            prefetch_tmap(&tmK);
+            prefetch_tmap(&tmV);
+        }
+    }
     pdl_wait();
     const int max_tokens = p.max_blocks * kBlockSize;
     // S1 ahead of S0: this partition's first 64 block ids are loaded alongside
@@ -144,6 +153,19 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
         pre_w1 = 32 + lane0 < lim ? __ldg(bt0 + 32 + lane0) : 0;
     }
     int L = p.lens[b];
+    // ring barriers initialised while the length is in flight (independent of it)
+    // TS: the empty-barrier words are per-stage consumer counters instead
+    int* done_cnt = reinterpret_cast<int*>(empty);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);  // producer's arrive.expect_tx (+ TMA bytes)
+            if constexpr (TS)
+                done_cnt[s] = 0;
+            else
+                mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
+        }
+        fence_barrier_init();
+    }
     L = L < max_tokens ? L : max_tokens;
     const int P = p.part_tokens;
     const int s_tok = part * P < L ? part * P : L;
@@ -249,23 +271,13 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
     const int jn0 = t_new0 < e_tok ? t_new0 / kBlockSize - sb : n;
     const int jn1 = t_new0 < e_tok ? (e_tok - 1) / kBlockSize - sb : n - 1;
 
-    // TS: the empty-barrier words are per-stage consumer counters instead
-    int* done_cnt = reinterpret_cast<int*>(empty);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);  // producer's arrive.expect_tx (+ TMA bytes)
-            if constexpr (TS)
-                done_cnt[s] = 0;
-            else
-                mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
-        }
-        fence_barrier_init();
-        if constexpr (TRACE && SELF) {
+    if constexpr (TRACE && SELF) {
+        if (threadIdx.x == 0) {
             rec[2] = 0;
             rec[3] = 0;
         }
     }
-    __syncthreads();
+    __syncthreads();  // the ring barriers (initialised at entry) are visible to every warp
 
     if (!SELF && warp == kConsumerWarps) {
         // ============================ producer warp ============================
@@ -344,10 +356,6 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;  // <= 32 (validated)
         const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-        if (lane == 0 && warp == 0) {
-            prefetch_tmap(&tmK);
-            prefetch_tmap(&tmV);
-        }
         int wbase = 0;  // block-id window [wbase, wbase + 64) of this unit, 2 ids per lane
         int w0 = pre_w0, w1 = pre_w1;  // loaded at entry (sb == part * P here: the unit is not empty)
         int npf = 0;
