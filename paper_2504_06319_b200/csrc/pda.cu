@@ -2,6 +2,7 @@
 // planner (S0), TMA tensor-map construction and kernel dispatch.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -24,6 +25,7 @@ constexpr size_t kSmemReservedPerCta = 1024;
 constexpr int kDefaultSms = 148;  // B200
 constexpr int kMaxCluster = 16;     // non-portable cluster size limit (split-K merge in a cluster)
 constexpr int kAutoMaxCluster = 8;  // planner: portable cluster sizes only
+constexpr int kSmallGridRows = 8;   // planner: <= 8 (seq, kv head) rows take the small-grid split
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -352,7 +354,21 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
                 one_wave = sp;
                 break;
             }
-        if (one_wave) {
+        if (units0 <= kSmallGridRows) {
+            // A handful of (sequence, kv head) rows (latency-bound steps): at most
+            // 128 CTAs (no cluster -- the combine kernel, see below) of partitions
+            // >= min(ctx / 16, 1024) tokens and >= 128.  Measured over 80 small
+            // grids x partition counts 1-64 (profiles/r02_small_grid_sweep.jsonl):
+            // B=1 8/1 ctx 8k 18.4 vs 27.7 us (64 x 128-token partitions before),
+            // ctx 16k 24.5 vs 43.0, ctx 32k (B=1-4) 31-33 vs 33-39; short contexts
+            // keep 128-token partitions (B=1-4, ctx 512-2048).  An e4m3 CTA streams
+            // half the bytes per block at a similar per-block cost, so e4m3 steps go
+            // to 256 CTAs (B=1 32/8 ctx 32k: 32 x 1024 tokens 32.8 vs 16 x 2048 36.9 us).
+            const int64_t min_p = std::max<int64_t>(128, std::min<int64_t>(max_tokens / 16, 1024));
+            const int64_t max_ctas = s->kv_dtype == PDA_E4M3 ? 256 : 128;
+            split = 1;
+            while (units0 * split * 2 <= max_ctas && max_tokens / (split * 2) >= min_p) split *= 2;
+        } else if (one_wave) {
             split = one_wave;
         } else {
             while (units0 * split < 4 * conc &&
@@ -397,8 +413,14 @@ pda_status plan(const pda_shape* s, const pda_options* o, pda_plan_info* pl) {
         if (o->merge == 2 && p_max > kMaxCluster) return PDA_ERR_UNSUPPORTED;
         const int64_t conc = (int64_t)sms * (ts ? 2 : splitk_ctas_per_sm(s, o, n_tiles));
         const bool one_wave = (int64_t)B * Hkv * p_max <= conc;
+        // ... and with at least one CTA per SM: below that the combine kernel
+        // (PDL-launched, one memory round trip) is 0-2 us faster than the cluster
+        // barriers + DSMEM merge (profiles/r02_small_grid_sweep.jsonl: e.g. B=1,
+        // 4 heads, ctx 1k 12.3 vs 14.4 us); from 256 CTAs on the cluster wins
+        // or ties (B=8 32/8 ctx 2k 22.5 vs 24.6, B=2 MHA ctx 8k 51.2 vs 53.2)
+        const bool fills = (int64_t)B * Hkv * p_max >= sms;
         if (o->merge == 2 ||
-            (p_max <= kAutoMaxCluster && one_wave &&
+            (p_max <= kAutoMaxCluster && one_wave && fills &&
              clusters_fit(s, o, n_tiles, stages, ts, (int)p_max, (int64_t)B * Hkv)))
             pl->cluster = (int32_t)p_max;
     }

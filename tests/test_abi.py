@@ -136,7 +136,9 @@ def test_workspace_required():
     s, o = shape(max_blocks_per_seq=64), opts(partition_tokens=256, merge=1)  # combine kernel
     need = pda.workspace_bytes(s, o)
     assert need > 0
-    assert pda.workspace_bytes(s, opts(partition_tokens=256)) == 0  # auto: merge in a cluster of 4
+    # auto: merge in a cluster of 4 once the grid has a CTA per SM (num_sms=16 here: 16 units)
+    assert pda.workspace_bytes(s, opts(partition_tokens=256, num_sms=16)) == 0
+    assert pda.workspace_bytes(s, opts(partition_tokens=256)) == need  # 16 CTAs < 148 SMs: combine kernel
     base = 0x10000000
     rc = L.paged_decode_attention(base, base, base, base, base, 1.0, base, ctypes.byref(s),
                                   ctypes.byref(o), None, 0, None)
@@ -287,9 +289,11 @@ def test_host_async_entry_rejects_before_launch():
 
 
 def test_cluster_merge_planning():
-    """Auto: clusters for 2 <= P_max <= 8; explicit cluster up to 16; beyond: unsupported."""
+    """Auto: clusters for 2 <= P_max <= 8 on one-wave grids with a CTA per SM;
+    explicit cluster up to 16; beyond: unsupported."""
     s = shape(max_blocks_per_seq=64)  # 1024 tokens
-    assert pda.plan(s, opts(partition_tokens=128))["cluster"] == 8
+    assert pda.plan(s, opts(partition_tokens=128, num_sms=32))["cluster"] == 8  # 32 CTAs on 32 SMs
+    assert pda.plan(s, opts(partition_tokens=128))["cluster"] == 0  # 32 CTAs < 148 SMs: combine
     p16 = pda.plan(s, opts(partition_tokens=64))
     assert p16["cluster"] == 0 and p16["workspace_bytes"] > 0  # auto: 16 > 8 -> combine kernel
     assert pda.plan(s, opts(partition_tokens=64, merge=2))["cluster"] == 16
@@ -301,14 +305,14 @@ def test_cluster_merge_planning():
 
 
 @pytest.mark.parametrize("B,ctx,P,p_max,cluster", [
-    (1, 512, 128, 4, 4),      # tiny grid: down to 128-token partitions, merged in clusters
-    (4, 512, 128, 4, 4),
+    (1, 512, 128, 4, 0),      # tiny grid: down to 128-token partitions, combine kernel (< 1 CTA per SM)
+    (4, 512, 128, 4, 0),
     (16, 512, 512, 1, 0),     # 128 units at 512: no split
-    (1, 4096, 512, 8, 8),     # 64 units, one wave: cluster merge
+    (1, 4096, 256, 16, 0),    # 8 rows (small grid): 16 x 256-token partitions, combine kernel
     (16, 4096, 2048, 2, 2),   # 256 units: one well-filled wave of 2048-token partitions
     (64, 4096, 1024, 4, 0),   # 512 rows: four waves of 1024-token partitions, combine kernel
     (16, 32768, 2048, 16, 0),  # long partitions prefer many waves
-    (1, 32768, 1024, 32, 0),  # > 8 partitions: combine kernel
+    (1, 32768, 2048, 16, 0),  # small grid: partitions >= 1024 tokens, <= 128 CTAs, combine kernel
 ])
 def test_planner_partitions_and_merge(B, ctx, P, p_max, cluster):
     _check_planner(B, ctx, P, p_max, cluster, 8)

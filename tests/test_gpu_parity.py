@@ -692,7 +692,9 @@ def test_cluster_merge_bitwise_equals_combine(pda, oracle_mod, cfg, kw):
     inp = synth.make_inputs(cfg, seed=23)
     dev = to_dev(inp)
     kw = dict(kw)
-    mode = kw.pop("merge", "auto")
+    # the planner's auto mode merges in clusters only from one CTA per SM on:
+    # these small cases force it
+    mode = kw.pop("merge", "cluster")
     info = pda.plan(pda.make_shape(dev["q"], dev["k_cache"], dev["block_tables"]),
                     pda.make_options(merge=mode, prefetch="off", **kw))
     assert info["cluster"] == info["p_max"] > 1
@@ -705,18 +707,19 @@ def test_cluster_merge_bitwise_equals_combine(pda, oracle_mod, cfg, kw):
 def test_cluster_merge_multi_token_kv8_gather_trace(pda, oracle_mod):
     # multi-token
     dev = to_dev(synth.with_query_tokens(synth.make_inputs(MQ_CASES[1][0], seed=24), 4))
-    assert torch.equal(gpu(pda, dev, partition_tokens=64), gpu(pda, dev, partition_tokens=64, merge="combine"))
+    assert torch.equal(gpu(pda, dev, partition_tokens=64, merge="cluster"),
+                       gpu(pda, dev, partition_tokens=64, merge="combine"))
     # e4m3 cache
     d8 = to_dev(kv8(synth.make_inputs(KV8_SHAPES[1], seed=25)))
-    assert torch.equal(gpu_kv8(pda, d8, partition_tokens=128), gpu_kv8(pda, d8, partition_tokens=128,
-                                                                         merge="combine"))
+    assert torch.equal(gpu_kv8(pda, d8, partition_tokens=128, merge="cluster"),
+                       gpu_kv8(pda, d8, partition_tokens=128, merge="combine"))
     # fused TP gather destinations
     cfg = synth.Config("cl_fg", 3, 8, 2, 128, (300, 17, 64), "bf16", poison_blocks=2)
     d = to_dev(synth.make_inputs(cfg, seed=26))
     ref = gpu(pda, d, partition_tokens=64, merge="combine")
     peers = [torch.full((3, 16, 128), 7.0, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     pda.paged_decode_attention_gather(d["q"], d["k_cache"], d["v_cache"], d["block_tables"], d["context_lens"],
-                                      d["scale"], peers, 8, 16, partition_tokens=64)
+                                      d["scale"], peers, 8, 16, partition_tokens=64, merge="cluster")
     torch.cuda.synchronize()
     for pb in peers:
         assert torch.equal(pb[:, 8:], ref) and (pb[:, :8] == 7.0).all()
@@ -724,7 +727,7 @@ def test_cluster_merge_multi_token_kv8_gather_trace(pda, oracle_mod):
     # the kernel's own bookkeeping is unchanged by the merge mode
     inp = synth.make_inputs(SHAPES[2], seed=27)
     dv = to_dev(inp)
-    _, tr_a, _ = gpu(pda, dv, partition_tokens=128, trace=True)
+    _, tr_a, _ = gpu(pda, dv, partition_tokens=128, merge="cluster", trace=True)
     _, tr_b, _ = gpu(pda, dv, partition_tokens=128, merge="combine", trace=True)
     assert torch.equal(tr_a, tr_b)
 
