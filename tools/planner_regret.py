@@ -64,12 +64,15 @@ def main():
     ap.add_argument("--cells", default=None, help="comma-separated B_Hq_Hkv_ctx filter")
     ap.add_argument("--check", action="store_true", help="synchronize after every first replay (debug)")
     ap.add_argument("--small", action="store_true", help="partition-count sweep of small grids")
+    ap.add_argument("--c4", action="store_true", help="ragged batch x context cells (BASELINE configs[3])")
     a = ap.parse_args()
     only = set(a.cells.split(",")) if a.cells else None
     flush = L2Flush(torch)
     ws = torch.zeros(1 << 30, dtype=torch.uint8, device="cuda")
     f = open(a.out, "w")
     heads, batch, ctxs = (SMALL_HEADS, SMALL_BATCH, SMALL_CTX) if a.small else (HEADS, BATCH, CTX)
+    if a.c4:
+        heads, batch, ctxs = [(32, 8)], [1, 4, 16, 32, 64, 128, 256], [512, 2048, 4096, 8192, 16384, 32768]
     for hq, hkv in heads:
         for B in batch:
             for ctx in ctxs:
@@ -78,7 +81,11 @@ def main():
                     continue
                 if only and f"{B}_{hq}_{hkv}_{ctx}" not in only:
                     continue
-                cfg = synth.uniform(f"u_{B}_{hq}_{hkv}_128_{ctx}_bf16", B, hq, hkv, 128, ctx, "bf16")
+                cfg = (synth.sweep_cell(B, ctx) if a.c4 else
+                       synth.uniform(f"u_{B}_{hq}_{hkv}_128_{ctx}_bf16", B, hq, hkv, 128, ctx, "bf16"))
+                kv = cfg.kv_bytes()
+                if kv > a.max_gb * 1e9:
+                    continue
                 inp = synth.make_inputs(cfg, seed=0, device="cuda", poison=False)
                 args = (inp["q"], inp["k_cache"], inp["v_cache"], inp["block_tables"], inp["context_lens"],
                         inp["scale"])
