@@ -173,7 +173,10 @@ typedef struct {
     float k_scale;             /* e4m3 cache only: K dequantisation scale (0 = 1.0) */
     float v_scale;             /* e4m3 cache only: V dequantisation scale (0 = 1.0) */
     int32_t merge;             /* split-K partition merge (S8) when P_max > 1: 0 = auto (cluster
-                                  when P_max <= 8, else combine kernel), 1 = combine kernel
+                                  when P_max <= 8, the grid is one wave with at least one CTA
+                                  per SM and the device can hold all its clusters at once --
+                                  cudaOccupancyMaxActiveClusters, asked when num_sms is 0 --
+                                  else combine kernel), 1 = combine kernel
                                   through the workspace, 2 = cluster (P_max <= 16): the
                                   partitions of a (seq, kv head) row run as one thread-block
                                   cluster and merge through distributed shared memory, no
