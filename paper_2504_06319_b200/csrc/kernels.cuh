@@ -42,6 +42,12 @@ constexpr bool kTma3d = PDA_TMA3D != 0;
 // refilled only one iteration earlier, so waiting for it before the current
 // softmax halves the ring's lookahead per warp (even from L2).
 constexpr bool kSwp = PDA_SWP != 0;
+#ifndef PDA_KV8_PAIRS
+#define PDA_KV8_PAIRS 1
+#endif
+// e4m3 rings of 8 / 16 / 24 stages consumed in pairs (one softmax update per
+// 32 tokens); 0 = one block at a time (A/B builds)
+constexpr bool kKv8Pairs = PDA_KV8_PAIRS != 0;
 constexpr int kPaperWarps = 4;     // paper kernel: 128 threads = 4 warps (Table 2)
 
 enum PrefetchMode { kPfOff = 0, kPfBulk = 1, kPfLine = 2 };

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
         // stages it just read: it owns every stage s with (s / PAIR) % 4 == w, so
         // no empty barriers are needed and a parity wait always refers to the
         // warp's own previous fill.
-        constexpr int PAIR = (KV8 && STAGES % 8 == 0) ? 2 : 1;
+        constexpr int PAIR = (KV8 && kKv8Pairs && STAGES % 8 == 0) ? 2 : 1;
         static_assert(STAGES % (PAIR * kConsumerWarps) == 0, "stages must split evenly over the warps");
         const int32_t* btrow = p.bt + (size_t)b * p.max_blocks + sb;
         const int d = p.pf_mode != kPfOff ? p.pf_dist : 0;  // <= 32 (validated)
