@@ -72,6 +72,27 @@ __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* 
     }
 }
 
+// S3 for one slab (K or V) of a block: the split K / V ring, where a K slab is
+// refilled as soon as QK^T has read it and a V slab once PV has.
+template <int kSlab, int kChunks, int kBoxCols>
+__device__ __forceinline__ void issue_slab(uint8_t* dst, const CUtensorMap* tm, int row, uint64_t* bar,
+                                           int eviction, uint64_t pol_first) {
+    if constexpr (kChunks > 1 && kTma3d) {
+        if (eviction & 1)
+            tma_load_3d_hint(dst, tm, 0, row, 0, bar, pol_first);
+        else
+            tma_load_3d(dst, tm, 0, row, 0, bar);
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch) {
+            if (eviction & 1)
+                tma_load_2d_hint(dst + ch * 2048, tm, ch * kBoxCols, row, bar, pol_first);
+            else
+                tma_load_2d(dst + ch * 2048, tm, ch * kBoxCols, row, bar);
+        }
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                                int row, uint64_t* bar, int eviction, uint64_t pol_first) {
@@ -333,6 +354,14 @@ struct BlockMath {
         a[3] &= m1;
     }
 
+    // S6 with the fragments softmax() produced (the split K / V ring waits for
+    // the V slab between the two)
+    template <bool TAIL = true>
+    __device__ __forceinline__ void pv_any(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2],
+                                           const uint32_t (&pb_lo)[NT][2]) {
+        pv<TAIL>(vbase, valid, lane, pb, pb_lo);
+    }
+
     // ---- S6: O^T[d][h] += sum_t V^T[d][t] P[t][h]
     template <bool TAIL = true>
     __device__ __forceinline__ void pv(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2],
@@ -504,6 +533,12 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true, MS> {
     }
 
     template <bool TAIL = true>
+    __device__ __forceinline__ void pv_any(uint32_t vbase, int valid, int lane, const uint32_t (&pb)[NT][2],
+                                           const uint32_t (&)[NT][2]) {
+        pv8<TAIL>(vbase, valid, lane, pb);
+    }
+
+    template <bool TAIL = true>
     __device__ __forceinline__ void block(uint32_t kbase, uint32_t vbase, int vq, float scale_log2,
                                           int lane) {
         float s[NT][4], s2[NT][4];
@@ -529,6 +564,16 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true, MS> {
                                             const float (&sb2)[NT][4], uint32_t vb0, int vq0, uint32_t vb1,
                                             int vq1, float scale_log2, int lane) {
         uint32_t pa[NT][2], pbb[NT][2];
+        softmax2<TAIL>(sa, sa2, sb, sb2, vq0, vq1, scale_log2, lane, pa, pbb);
+        pv8<TAIL>(vb0, vq0 < kBlockSize ? vq0 : kBlockSize, lane, pa);
+        pv8<TAIL>(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
+    }
+
+    // S5 of a block pair: one online-softmax update for both, P fragments out
+    template <bool TAIL = true>
+    __device__ __forceinline__ void softmax2(float (&sa)[NT][4], const float (&sa2)[NT][4], float (&sb)[NT][4],
+                                             const float (&sb2)[NT][4], int vq0, int vq1, float scale_log2,
+                                             int lane, uint32_t (&pa)[NT][2], uint32_t (&pbb)[NT][2]) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -569,8 +614,6 @@ struct BlockMathKV8 : BlockMath<false, 128, NT, true, MS> {
             pbb[nt][0] = movmatrix_trans(pack2<false>(prb[0], prb[1]));
             pbb[nt][1] = movmatrix_trans(pack2<false>(prb[2], prb[3]));
         }
-        pv8<TAIL>(vb0, vq0 < kBlockSize ? vq0 : kBlockSize, lane, pa);
-        pv8<TAIL>(vb1, vq1 < kBlockSize ? vq1 : kBlockSize, lane, pbb);
     }
 
 };

@@ -42,6 +42,16 @@ constexpr bool kTma3d = PDA_TMA3D != 0;
 // refilled only one iteration earlier, so waiting for it before the current
 // softmax halves the ring's lookahead per warp (even from L2).
 constexpr bool kSwp = PDA_SWP != 0;
+#ifndef PDA_KV_SPLIT
+#define PDA_KV_SPLIT 0
+#endif
+// split K / V ring (self-issue, 4 consumer warps): each stage has a K and a V
+// mbarrier; a warp refills the K slabs of its stages as soon as QK^T has read
+// them and the V slabs after PV -- K loads go out a softmax + PV earlier.
+// Off (default): measured 1 % slower on 16-bit and 4-7 % on e4m3 steps -- the
+// second barrier wait, fence and issue per block cost more on the consumer
+// chain than the earlier K loads save (profiles/r02_ab_kvsplit.log)
+constexpr bool kKvSplit = PDA_KV_SPLIT != 0;
 #ifndef PDA_KV8_PAIRS
 #define PDA_KV8_PAIRS 1
 #endif

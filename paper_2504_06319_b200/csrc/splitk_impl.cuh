@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
     const bool clustered = MODE != 0 && p.cluster > 1;
     using G = Geometry<D, KV8>;
     constexpr bool DSPLIT = TS && NT == 1;                 // D split (else head-tile split)
+    constexpr bool KVS = kKvSplit && SELF && !TS;          // split K / V ring barriers
     constexpr int NTW = TS && !DSPLIT ? 1 : NT;            // head tiles per warp
     constexpr int NW = TS ? 2 * kConsumerWarps : kConsumerWarps;  // consumer warps
     using BM = typename MathFor<BF16, D, NTW, KV8, DSPLIT ? 2 : 1>::type;
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
             if constexpr (TS)
                 done_cnt[s] = 0;
             else
-                mbar_init(&empty[s], 32);  // every lane of the consuming warp releases its reads
+                mbar_init(&empty[s], KVS ? 1 : 32);  // KVS: the V slab's full barrier; else every lane
+                                                     // of the consuming warp releases its reads
         }
         fence_barrier_init();
     }
@@ -391,12 +393,56 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                 ++npf;
             }
         };
+        // split K / V ring (KVS): the K slab of block `pos` on full[st], its V slab
+        // on empty[st] (used as a second full barrier); issue_k returns the id
+        auto issue_k = [&](int pos) {
+            while (pos >= wbase + 32) {
+                w0 = w1;
+                wbase += 32;
+                w1 = wbase + 32 + lane < n ? btrow[wbase + 32 + lane] : 0;
+            }
+            const int phys = id_at(pos);
+            const bool pf = d > 0 && pos + d < n;  // Alg. 1 guard against the unit end
+            const int tgt = pf ? id_at(pos + d) : -1;
+            const int st = pos % STAGES;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&full[st], G::kSlab);
+                issue_slab<G::kSlab, G::kChunks, G::kBoxCols>(ring + st * G::kStage, &tmK,
+                                                              (phys * p.Hkv + kvh) * kBlockSize, &full[st],
+                                                              p.eviction, pol_first);
+                if constexpr (TRACE) rec[4 + pos] = phys;
+            }
+            if (pf) {
+                prefetch_kv_bytes<G::kSlab>(p.k, p.v, ((size_t)tgt * p.Hkv + kvh) * G::kSlab, p.pf_mode, lane,
+                                            p.eviction, pol_last);
+                if constexpr (TRACE) {
+                    if (lane == 0) rec[4 + (p.trace_rec_len - 4) / 2 + pos] = tgt;
+                }
+                ++npf;
+            }
+            return phys;
+        };
+        auto issue_v = [&](int pos, int phys) {
+            const int st = pos % STAGES;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&empty[st], G::kSlab);
+                issue_slab<G::kSlab, G::kChunks, G::kBoxCols>(ring + st * G::kStage + G::kSlab, &tmV,
+                                                              (phys * p.Hkv + kvh) * kBlockSize, &empty[st],
+                                                              p.eviction, pol_first);
+            }
+        };
         for (int pos = PAIR * warp; sub == 0 && pos < STAGES && pos < n; pos += PAIR * kConsumerWarps) {
             if (pos >= jn0 && pos <= jn1) write_new(pos);
-            issue(pos);
+            if constexpr (KVS)
+                issue_v(pos, issue_k(pos));
+            else
+                issue(pos);
             if (PAIR == 2 && pos + 1 < n) {
                 if (pos + 1 >= jn0 && pos + 1 <= jn1) write_new(pos + 1);
-                issue(pos + 1);
+                if constexpr (KVS)
+                    issue_v(pos + 1, issue_k(pos + 1));
+                else
+                    issue(pos + 1);
             }
         }
         // new-token blocks past the prologue: written now (overlapping the
@@ -424,8 +470,73 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
                 bm.qk(smem_u32(ring + ((jj + 1) % STAGES) * G::kStage), lane, xb, xb2);
             }
         };
-        if (SWP && PAIR * warp < n) scores(PAIR * warp, ca, ca2, cb, cb2);
-        for (int j = PAIR * warp; j < n; j += STRIDE) {
+        if constexpr (KVS) {
+            for (int j = PAIR * warp; j < n; j += STRIDE) {
+                const bool two = PAIR == 2 && j + 1 < n;
+                const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
+                const uint32_t ph0 = (j / STAGES) & 1, ph1 = ((j + 1) / STAGES) & 1;
+                const uint32_t kb0 = smem_u32(ring + st0 * G::kStage), kb1 = smem_u32(ring + st1 * G::kStage);
+                mbar_wait(&full[st0], ph0);
+                bm.qk(kb0, lane, ca, ca2);
+                if (two) {
+                    mbar_wait(&full[st1], ph1);
+                    bm.qk(kb1, lane, cb, cb2);
+                }
+                // the K slabs are read (their registers fed QK^T): their stages' next
+                // K loads go out now, a softmax + PV before the V loads
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                int nph0 = 0, nph1 = 0;
+                if (j + STAGES < n) nph0 = issue_k(j + STAGES);
+                if (two && j + 1 + STAGES < n) nph1 = issue_k(j + 1 + STAGES);
+                const int v0 = L - (sb + j) * kBlockSize;  // tokens of the context from this block on
+                const int val0 = v0 < kBlockSize ? v0 : kBlockSize;
+                uint32_t pa[BM::kNT][2], pa_lo[BM::kNT][2];
+                if constexpr (PAIR == 2) {
+                    if (two) {
+                        const int v1 = L - (sb + j + 1) * kBlockSize;
+                        const int val1 = v1 < kBlockSize ? v1 : kBlockSize;
+                        uint32_t pbb[BM::kNT][2];
+                        const bool m = bm.needs_mask(v1);
+                        if (m)
+                            bm.template softmax2<true>(ca, ca2, cb, cb2, v0, v1, p.scale_log2, lane, pa, pbb);
+                        else
+                            bm.template softmax2<false>(ca, ca2, cb, cb2, v0, v1, p.scale_log2, lane, pa, pbb);
+                        mbar_wait(&empty[st0], ph0);
+                        mbar_wait(&empty[st1], ph1);
+                        if (m) {
+                            bm.template pv8<true>(kb0 + G::kSlab, val0, lane, pa);
+                            bm.template pv8<true>(kb1 + G::kSlab, val1, lane, pbb);
+                        } else {
+                            bm.template pv8<false>(kb0 + G::kSlab, val0, lane, pa);
+                            bm.template pv8<false>(kb1 + G::kSlab, val1, lane, pbb);
+                        }
+                    } else {
+                        bm.template softmax<true>(ca, ca2, v0, p.scale_log2, lane, pa, pa_lo);
+                        mbar_wait(&empty[st0], ph0);
+                        bm.template pv_any<true>(kb0 + G::kSlab, val0, lane, pa, pa_lo);
+                    }
+                } else {
+                    const bool m = bm.needs_mask(v0);
+                    if (m)
+                        bm.template softmax<true>(ca, ca2, v0, p.scale_log2, lane, pa, pa_lo);
+                    else
+                        bm.template softmax<false>(ca, ca2, v0, p.scale_log2, lane, pa, pa_lo);
+                    mbar_wait(&empty[st0], ph0);
+                    if (m)
+                        bm.template pv_any<true>(kb0 + G::kSlab, val0, lane, pa, pa_lo);
+                    else
+                        bm.template pv_any<false>(kb0 + G::kSlab, val0, lane, pa, pa_lo);
+                }
+                mine += two ? 2 : 1;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (j + STAGES < n) issue_v(j + STAGES, nph0);
+                if (two && j + 1 + STAGES < n) issue_v(j + 1 + STAGES, nph1);
+            }
+        }
+        if (SWP && !KVS && PAIR * warp < n) scores(PAIR * warp, ca, ca2, cb, cb2);
+        for (int j = PAIR * warp; !KVS && j < n; j += STRIDE) {
             const bool two = PAIR == 2 && j + 1 < n;
             const int st0 = j % STAGES, st1 = (j + 1) % STAGES;
             if (SWP) {
