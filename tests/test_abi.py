@@ -326,6 +326,24 @@ def test_planner_one_wave_fills_every_sm(B, ctx, P, p_max, cluster):
     _check_planner(B, ctx, P, p_max, cluster, 2)
 
 
+@pytest.mark.parametrize("B,hkv,ctx,kv8,P,p_max", [
+    (1, 1, 8192, False, 512, 16),    # small grid: <= 128 CTAs of >= min(ctx/16, 1024)-token partitions
+    (1, 1, 4096, False, 256, 16),
+    (2, 1, 32768, False, 1024, 32),
+    (4, 8, 2048, False, 512, 4),     # 32 rows > 8: the general rules (>= 512-token partitions)
+    (1, 8, 32768, False, 2048, 16),  # 8 rows x 16 = 128 CTAs
+    (1, 8, 32768, True, 1024, 32),   # e4m3: up to 256 CTAs
+])
+def test_planner_small_grids(B, hkv, ctx, kv8, P, p_max):
+    """<= 8 (seq, kv head) rows: the measured small-grid split (DESIGN.md 6,
+    profiles/r02_small_grid_sweep.jsonl); such grids merge with the combine kernel."""
+    s = shape(num_seqs=B, num_q_heads=8 * hkv, num_kv_heads=hkv, head_dim=128, num_blocks=100000,
+              max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1, kv_dtype=3 if kv8 else 1)
+    p = pda.plan(s, opts(kernel=2))
+    assert (p["partition_tokens"], p["p_max"]) == (P, p_max)
+    assert p["cluster"] == 0  # fewer CTAs than SMs: combine kernel
+
+
 def _check_planner(B, ctx, P, p_max, cluster, hkv):
     s = shape(num_seqs=B, num_q_heads=32, num_kv_heads=hkv, head_dim=128, num_blocks=100000,
               max_blocks_per_seq=ctx // 16, dtype=1, out_dtype=1)
