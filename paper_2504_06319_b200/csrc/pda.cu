@@ -187,11 +187,17 @@ bool clusters_fit(const pda_shape* s, const pda_options* o, int n_tiles, int sta
     p.tile_split = ts;
     p.query_clusters = &n;
     CUtensorMap none{};
+    // the first plan of a configuration may run inside a stream capture: the
+    // occupancy query (and the attribute calls before it) are made with this
+    // thread's capture mode relaxed, so a global-mode capture stays valid
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     if (pda::launch_splitk_m2(none, none, p, s->dtype == PDA_BF16, s->head_dim, n_tiles, stages, dim3(cluster, 1, 1),
                               nullptr, kv8, self) != cudaSuccess) {
         cudaGetLastError();
         n = 0;  // unknown: the slot count decides
     }
+    cudaThreadExchangeStreamCaptureMode(&mode);
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = n;
     return n <= 0 || n_clusters <= n;

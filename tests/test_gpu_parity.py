@@ -1004,3 +1004,33 @@ def test_planner_clusters_only_when_resident(pda, B, ctx, p_max, cluster):
     p = pda.plan(s, o)
     assert (p["p_max"], p["cluster"]) == (p_max, cluster)
     assert (p["workspace_bytes"] > 0) == (cluster == 0)
+
+
+def test_first_plan_inside_graph_capture(tmp_path):
+    """The planner's first cluster-residency query for a configuration may run
+    inside a (global-mode) CUDA graph capture: it relaxes the thread's capture
+    mode, so the capture stays valid and the replay matches an eager call.
+    A fresh process, so the query cache is empty."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2504_06319_b200 as pda, synth
+cfg = synth.uniform("cap", 128, 8, 1, 128, 8192, "bf16")
+d = synth.make_inputs(cfg, seed=5, device="cuda")
+args = (d["q"], d["k_cache"], d["v_cache"], d["block_tables"], d["context_lens"], d["scale"])
+out = torch.empty_like(d["q"])
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):  # the first plan of this configuration happens here
+    pda.paged_decode_attention(*args, out=out, prefetch="off")
+g.replay()
+ref = pda.paged_decode_attention(*args, prefetch="off")
+torch.cuda.synchronize()
+info = pda.plan(pda.make_shape(d["q"], d["k_cache"], d["block_tables"]), pda.make_options(prefetch="off"))
+assert info["cluster"] == 2, info
+assert torch.equal(out, ref)
+print("ok")
+''' % (str(__import__("pathlib").Path(__file__).resolve().parents[1]),)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
