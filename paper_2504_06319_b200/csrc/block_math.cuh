@@ -93,6 +93,33 @@ __device__ __forceinline__ void issue_slab(uint8_t* dst, const CUtensorMap* tm, 
     }
 }
 
+// issue_kv_slabs from a converged warp: all 32 lanes call it, one elected lane
+// issues each load (see ptx.cuh; same loads, same barrier).
+template <int kSlab, int kChunks, int kBoxCols>
+__device__ __forceinline__ void issue_kv_slabs_elect(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                                                     int row, uint64_t* bar, int eviction, uint64_t pol_first) {
+    if constexpr (kChunks > 1 && kTma3d) {
+        if (eviction & 1) {
+            tma_load_3d_hint_elect(dst, tmK, 0, row, 0, bar, pol_first);
+            tma_load_3d_hint_elect(dst + kSlab, tmV, 0, row, 0, bar, pol_first);
+        } else {
+            tma_load_3d_elect(dst, tmK, 0, row, 0, bar);
+            tma_load_3d_elect(dst + kSlab, tmV, 0, row, 0, bar);
+        }
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch) {
+            if (eviction & 1) {
+                tma_load_2d_hint_elect(dst + ch * 2048, tmK, ch * kBoxCols, row, bar, pol_first);
+                tma_load_2d_hint_elect(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar, pol_first);
+            } else {
+                tma_load_2d_elect(dst + ch * 2048, tmK, ch * kBoxCols, row, bar);
+                tma_load_2d_elect(dst + kSlab + ch * 2048, tmV, ch * kBoxCols, row, bar);
+            }
+        }
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void issue_kv_slabs(uint8_t* dst, const CUtensorMap* tmK, const CUtensorMap* tmV,
                                                int row, uint64_t* bar, int eviction, uint64_t pol_first) {

@@ -42,6 +42,12 @@ constexpr bool kTma3d = PDA_TMA3D != 0;
 // refilled only one iteration earlier, so waiting for it before the current
 // softmax halves the ring's lookahead per warp (even from L2).
 constexpr bool kSwp = PDA_SWP != 0;
+#ifndef PDA_ELECT_ISSUE
+#define PDA_ELECT_ISSUE 1
+#endif
+// self-issued refills from the converged warp with elect.sync inside each
+// statement (no per-load ptxas waterfall loop); 0 = a lane == 0 branch
+constexpr bool kElectIssue = PDA_ELECT_ISSUE != 0;
 #ifndef PDA_KV_SPLIT
 #define PDA_KV_SPLIT 0
 #endif

@@ -123,8 +123,11 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
     const int lane = threadIdx.x & 31;
     // TS: warp = block slot (mod 4), sub = which of its two warps; sub is the
     // head tile (two tiles) or the half of d (D split)
-    const int warp = TS ? (threadIdx.x >> 5) & (kConsumerWarps - 1) : threadIdx.x >> 5;
-    const int sub = TS ? threadIdx.x >> 7 : 0;
+    // warp-level indices through a lane-0 shuffle: ptxas then knows they are
+    // warp-uniform, and the ring-slot addresses and TMA coordinates derived
+    // from them go to uniform registers without a per-load ELECT loop
+    const int warp = __shfl_sync(0xffffffffu, TS ? (threadIdx.x >> 5) & (kConsumerWarps - 1) : threadIdx.x >> 5, 0);
+    const int sub = __shfl_sync(0xffffffffu, TS ? threadIdx.x >> 7 : 0, 0);
     const int tile = DSPLIT ? 0 : sub;
     const int g = p.g;
 
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
         pre_w0 = lane0 < lim ? __ldg(bt0 + lane0) : 0;
         pre_w1 = 32 + lane0 < lim ? __ldg(bt0 + 32 + lane0) : 0;
     }
-    int L = p.lens[b];
+    int L = __shfl_sync(0xffffffffu, p.lens[b], 0);  // (uniform, see warp above)
     // ring barriers initialised while the length is in flight (independent of it)
     // TS: the empty-barrier words are per-stage consumer counters instead
     int* done_cnt = reinterpret_cast<int*>(empty);
@@ -376,7 +379,15 @@ __global__ void __launch_bounds__(splitk_block_threads<SELF, TS>(), splitk_min_b
             const bool pf = d > 0 && pos + d < n;  // Alg. 1 guard against the unit end
             const int tgt = pf ? id_at(pos + d) : -1;
             const int st = pos % STAGES;
-            if (lane == 0) {
+            if constexpr (kElectIssue) {  // converged warp: one elected lane issues
+                mbar_arrive_expect_tx_elect(&full[st], G::kStage);
+                issue_kv_slabs_elect<G::kSlab, G::kChunks, G::kBoxCols>(ring + st * G::kStage, &tmK, &tmV,
+                                                                         (phys * p.Hkv + kvh) * kBlockSize,
+                                                                         &full[st], p.eviction, pol_first);
+                if constexpr (TRACE) {
+                    if (lane == 0) rec[4 + pos] = phys;
+                }
+            } else if (lane == 0) {
                 mbar_arrive_expect_tx(&full[st], G::kStage);
                 issue_kv_slabs<G::kSlab, G::kChunks, G::kBoxCols>(ring + st * G::kStage, &tmK, &tmV,
                                                                    (phys * p.Hkv + kvh) * kBlockSize, &full[st],
