@@ -55,6 +55,17 @@ __device__ __forceinline__ void advance(Cursor& c, int k, int& seg, const int32_
     }
 }
 
+// Lane 0's cursor in every lane, through shuffles (every lane holds the same
+// cursor anyway): ptxas can then treat the fields as warp-uniform.
+__device__ __forceinline__ void uniform_cursor(Cursor& c) {
+    c.b = __shfl_sync(0xffffffffu, c.b, 0);
+    c.kvh = __shfl_sync(0xffffffffu, c.kvh, 0);
+    c.j = __shfl_sync(0xffffffffu, c.j, 0);
+    c.n = __shfl_sync(0xffffffffu, c.n, 0);
+    c.L = __shfl_sync(0xffffffffu, c.L, 0);
+    c.pre = __shfl_sync(0xffffffffu, c.pre, 0);
+}
+
 // CTA owning item k: the largest c with floor(c*T/G) <= k.
 __device__ __forceinline__ int cta_of(long long k, long long T, int G) { return (int)(((k + 1) * G - 1) / T); }
 __device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }

@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(slots + Lay::kSlots * Lay::kSlotBytes);
     BMisc* misc = reinterpret_cast<BMisc*>(full + S);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index through a lane-0 shuffle: warp-uniform for ptxas (the refill
+    // issue then needs no per-load ELECT loop, see splitk_impl.cuh)
+    const int warp = __shfl_sync(kFullMask, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const int max_tokens = p.max_blocks * kBlockSize;
     const int g = p.g;
@@ -115,9 +117,10 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
         }
     }
     __syncthreads();
-    const long long total = misc->k1 - misc->k0;
-    const int n_segs = misc->n_segs, end_j = misc->end_j;
-    const Cursor start = misc->start;
+    const long long total = __shfl_sync(kFullMask, misc->k1 - misc->k0, 0);
+    const int n_segs = __shfl_sync(kFullMask, misc->n_segs, 0), end_j = __shfl_sync(kFullMask, misc->end_j, 0);
+    Cursor start = misc->start;
+    uniform_cursor(start);
 
     // context_len == 0 rows: zeros (reading R6), sequences strided over the grid
     for (int b = c; b < p.B; b += gridDim.x) {
@@ -138,7 +141,11 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
     Cursor ic = start;
     int iseg = 0;
     long long ipos = warp;
-    if (ipos < total) advance(ic, warp, iseg, p.lens, p.B, p.Hkv, max_tokens);
+    if (ipos < total) {
+        advance(ic, warp, iseg, p.lens, p.B, p.Hkv, max_tokens);
+        uniform_cursor(ic);
+        iseg = __shfl_sync(kFullMask, iseg, 0);
+    }
     int wb = -1, wbase = 0, w0 = 0, w1 = 0;  // block-id window [wbase, wbase + 64) of sequence wb
     auto issue = [&]() {
         const int32_t* row = p.bt + (size_t)ic.b * p.max_blocks;
@@ -162,10 +169,11 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
         const int st = (int)(ipos % S);
         int32_t* rec = nullptr;
         if constexpr (TRACE) rec = p.trace + ((size_t)ic.b * p.Hkv + ic.kvh) * p.trace_rec_len;
+        mbar_arrive_expect_tx_elect(&full[st], G::kStage);  // converged warp: one elected lane issues
+        issue_kv_slabs_elect<kBlockSize * D * 2, D / 64, 64>(ring + st * G::kStage, &tmK, &tmV,
+                                                             (phys * p.Hkv + ic.kvh) * kBlockSize, &full[st],
+                                                             p.eviction, pol_first);
         if (lane == 0) {
-            mbar_arrive_expect_tx(&full[st], G::kStage);
-            issue_kv_slabs<D>(ring + st * G::kStage, &tmK, &tmV, (phys * p.Hkv + ic.kvh) * kBlockSize, &full[st],
-                              p.eviction, pol_first);
             if constexpr (TRACE) {
                 rec[4 + ic.j] = phys;
                 atomicAdd(rec + 2, ic.j == 0 ? 2 : 1);  // block 0 cancels the -1 fill
@@ -190,7 +198,11 @@ __global__ void __launch_bounds__(kConsumerWarps * 32, NT == 1 ? 2 : 1)
             }
         }
         ipos += kConsumerWarps;
-        if (ipos < total) advance(ic, kConsumerWarps, iseg, p.lens, p.B, p.Hkv, max_tokens);
+        if (ipos < total) {
+            advance(ic, kConsumerWarps, iseg, p.lens, p.B, p.Hkv, max_tokens);
+            uniform_cursor(ic);
+            iseg = __shfl_sync(kFullMask, iseg, 0);
+        }
     };
     for (int k = 0; k < S / kConsumerWarps && ipos < total; ++k) issue();
 
